@@ -1,0 +1,128 @@
+/*
+ * pevd.h -- C ABI of libpevd.so, the B200 (sm_100a) pipelined two-stage FP64 symmetric EVD.
+ *
+ * Drop-in boundary for the reference package `pipeevd` (a pure-Python package; its "FFI" is the
+ * Python call `pipeevd.run(a, PipelineConfig(...))`, pkg/src/pipeevd/pipeline.py:511-548).  The
+ * Python package `paper_2511_16174_b200` binds these symbols with ctypes and re-exposes the
+ * reference's API names on top (see INTEGRATION.md for the binding).  Every entry point takes
+ * plain pointers and sizes; matrices are column-major (Fortran order, as SymmetricMatrix stores
+ * them, core.py:65-93).
+ *
+ * Return codes map to the reference's exception taxonomy:
+ *   PEVD_ERR_VALUE    -> ValueError     (bad shape / bandwidth / config, pipeline.py:74-82)
+ *   PEVD_ERR_CUDA     -> PipelineError  (device failure, pipeline.py:540-544)
+ *   PEVD_ERR_CONVERGE -> RuntimeError   (solver did not converge, tridiag.py:314-320)
+ * pevd_last_error() returns the message of the calling thread's last failure.
+ */
+#ifndef PEVD_H
+#define PEVD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PEVD_OK 0
+#define PEVD_ERR_CUDA 1
+#define PEVD_ERR_VALUE 2
+#define PEVD_ERR_CONVERGE 3
+#define PEVD_ERR_NOMEM 4
+
+/* back-transformation orders, PipelineConfig.order (pipeline.py:45, 57-82) */
+#define PEVD_ORDER_PIPELINED 0
+#define PEVD_ORDER_SEQUENTIAL 1
+#define PEVD_ORDER_CONVENTIONAL 2
+
+/* Per-stage device times (CUDA events on the launching streams), for TraceEvent /
+ * FlopCounter population (messaging.py:51-108).  Offsets are relative to the first event. */
+typedef struct pevd_stats {
+  double sbr_ms[2];        /* [start, end] */
+  double bc_ms[2];
+  double solver_ms[2];
+  double sbr_back_ms[2];
+  double bc_back_ms[2];
+  double final_ms[2];
+  double total_ms;         /* first start .. last end */
+  int64_t n_reflectors;    /* bulge reflector slots (sum_j (n-2-jb)) */
+  int64_t n_rounds;        /* SBR panels */
+} pevd_stats;
+
+const char* pevd_last_error(void);
+const char* pevd_version(void);
+
+/* ---------------------------------------------------------------- whole EVD
+ * Replaces pipeevd.run (pipeline.py:511) for one GPU: A = Q diag(lam) Q^T.
+ * lam ascending (tridiag.py:321); Q with columns the eigenvectors. */
+
+/* Device workspace needed by pevd_syevd_device (bytes). */
+int64_t pevd_syevd_workspace_bytes(int64_t n, int b, int want_vectors, int order);
+
+/* All pointers are DEVICE pointers.  A (n x n, lda; only the lower triangle is read) is
+ * destroyed.  Q (n x n, ldq) may be NULL when want_vectors == 0.  `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  Synchronous: returns after the result is complete. */
+int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
+                      int64_t ldq, int want_vectors, int order, void* workspace,
+                      int64_t workspace_bytes, void* stream, pevd_stats* stats);
+
+/* HOST pointers (A column-major, lda); allocates device memory itself, copies in and out.
+ * Q may be NULL when want_vectors == 0.  A is not modified. */
+int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q,
+               int64_t ldq, int want_vectors, int order, pevd_stats* stats);
+
+/* ---------------------------------------------------------------- per-stage (device pointers)
+ * Each replaces one reference function; `stream` is a cudaStream_t; all are asynchronous except
+ * where noted. */
+
+/* C = alpha op(A) op(B) + beta C (FP64 DMMA GEMM); core.py:309-319 matmul_counted. */
+int pevd_dgemm(int transA, int transB, int64_t m, int64_t n, int64_t k, double alpha,
+               const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+               int64_t ldc, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Householder panel QR, sbr.py:69-116.  P (m x k, ldp) read; R (k x k), Y (m x k, ldy),
+ * W (m x k, ldw), T (k x k) written (any output may be NULL except Y).  k <= 32. */
+int64_t pevd_panel_qr_workspace_bytes(void);
+int pevd_panel_qr(int64_t m, int k, const double* P, int64_t ldp, double* R, double* Y,
+                  int64_t ldy, double* W, int64_t ldw, double* T, void* workspace, void* stream);
+
+/* Band reduction sbr.py:155-188: A (n x n, lda, lower triangle) -> bands ((b+1) x n, C order,
+ * bands[d*n + j] = A[j+d, j], core.py:118-135).  A becomes the explicit-Y staircase, Tall
+ * (rounds x b x b) receives the panels' T factors (may be NULL). */
+int64_t pevd_sbr_workspace_bytes(int64_t n, int b);
+int pevd_sbr(int64_t n, int b, double* A, int64_t lda, double* bands, double* Tall,
+             void* workspace, void* stream);
+
+/* Bulge chasing bulge.py:299-309: bands -> d (n), e (n-1); reflectors (tau, V with stride vld)
+ * in fixed slots, canonical chase-step-major order (bulge.py:51-60): slot(i, j) =
+ * j (n-2) - b j (j-1)/2 + i; tau = 0 marks a step the reference skips.  tau/V may be NULL. */
+int64_t pevd_bc_num_reflectors(int64_t n, int b);
+int64_t pevd_bc_workspace_bytes(int64_t n, int b);
+int pevd_bc(int64_t n, int b, const double* bands, double* d, double* e, double* tau, double* V,
+            int vld, void* workspace, void* stream);
+
+/* Tridiagonal divide and conquer (replaces tridiag_eig, tridiag.py:298-334): d in/out (lam
+ * ascending), e (n-1) preserved, Q (n x n, ldq) eigenvectors with the reference sign convention.
+ * Synchronous (returns PEVD_ERR_CONVERGE on non-convergence). */
+int64_t pevd_stedc_workspace_bytes(int64_t n);
+int pevd_stedc(int64_t n, double* d, const double* e, double* Q, int64_t ldq, void* workspace,
+               void* stream);
+
+/* SBR-Back: Qs (n x n, ldq) = prod_x (I - Y_x T_x Y_x^T) (backtrans.py:128-192). */
+int64_t pevd_sbr_back_workspace_bytes(int64_t n, int b);
+int pevd_sbr_back_form(int64_t n, int b, const double* Ystair, const double* Tall, double* Qs,
+                       int64_t ldq, void* workspace, void* stream);
+/* X (n x ncols, ldx) <- Q_s X (conventional order, pipeline.py:380-384). */
+int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, const double* Tall, double* X,
+                       int64_t ldx, int64_t ncols, void* workspace, void* stream);
+
+/* BC-Back backtrans.py:277-310.  right: X (nrows x n, ldx) <- X Q_b ("reordered", i.e. the
+ * transpose of Q_b^T X^T).  left: X (n x ncols, ldx) <- Q_b X ("conventional"). */
+int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
+                       int64_t ldx, int64_t nrows, void* stream);
+int pevd_bc_back_left(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
+                      int64_t ldx, int64_t ncols, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PEVD_H */

@@ -1,0 +1,372 @@
+// C ABI of libpevd.so (include/pevd.h) and the single-GPU pipelined EVD orchestrator.
+//
+// Orchestration of pevd_syevd_device (pipeline.py:170-508 restated for one B200):
+//   stream main : SBR -> BC -> D&C -> (wait back) -> final GEMM Q = (Q_s Q_b) Q_d
+//   stream back : (wait SBR) SBR-Back forms Q_s -> (wait BC) BC-Back Q_s <- Q_s Q_b
+// so the compute-bound Q_s formation overlaps the latency-bound bulge chase and BC-Back
+// overlaps the divide and conquer ("pipelined").  "sequential" runs the same stages on one
+// stream; "conventional" applies Q_b then Q_s to Q_d from the left (pipeline.py:367-387).
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+#include <vector>
+#include "kernels.cuh"
+#include "../../include/pevd.h"
+
+namespace pevd {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+const char* last_error() { return g_err; }
+
+int num_sms() {
+  static int cache[64];
+  static bool init[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!init[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = v > 0 ? v : 1;
+    init[dev] = true;
+  }
+  return cache[dev];
+}
+
+namespace {
+
+struct Carve {
+  char* base;
+  int64_t off = 0, cap;
+  Carve(void* b, int64_t c) : base((char*)b), cap(c) {}
+  void* take(int64_t bytes) {
+    void* p = base ? base + off : nullptr;
+    off += (bytes + 255) / 256 * 256;
+    return p;
+  }
+};
+
+struct Layout {
+  double *bands, *Tall, *d, *e, *tau, *V, *Qs, *Qd;
+  void *ws_sbr, *ws_bc, *ws_dc, *ws_back;
+  int vld;
+  int64_t total;
+};
+
+Layout plan_layout(void* base, int64_t n, int b, int want_vectors, int order) {
+  Carve c(base, 0);
+  Layout L{};
+  const int64_t R = sbr_num_rounds(n, b);
+  L.vld = (int)pad8(b);
+  L.bands = (double*)c.take((int64_t)(b + 1) * n * 8);
+  L.Tall = (double*)c.take(std::max<int64_t>(R, 1) * b * b * 8);
+  L.d = (double*)c.take(n * 8);
+  L.e = (double*)c.take(std::max<int64_t>(n, 1) * 8);
+  const int64_t nref = (n >= 3) ? bc_num_reflectors(n, b) : 0;
+  if (want_vectors) {
+    L.tau = (double*)c.take(std::max<int64_t>(nref, 1) * 8);
+    L.V = (double*)c.take(std::max<int64_t>(nref, 1) * L.vld * 8);
+    if (order != PEVD_ORDER_CONVENTIONAL) L.Qs = (double*)c.take(n * n * 8);
+  }
+  L.Qd = (double*)c.take(n * n * 8);
+  L.ws_sbr = c.take(sbr_ws_bytes(n, b));
+  L.ws_bc = c.take(bc_ws_bytes(n, b));
+  L.ws_dc = c.take(stedc_ws_bytes(n));
+  L.ws_back = c.take(sbr_back_ws_bytes(n, b));
+  L.total = c.off;
+  return L;
+}
+
+__global__ void copy_lower_to_full_kernel(int64_t n, const double* src, int64_t lds, double* dst,
+                                          int64_t ldd) {
+  const int64_t total = n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % n, j = idx / n;
+    dst[i + j * ldd] = src[i + j * lds];
+  }
+}
+
+struct Ev {
+  cudaEvent_t a = nullptr, b = nullptr;
+};
+
+}  // namespace
+}  // namespace pevd
+
+using namespace pevd;
+
+extern "C" {
+
+const char* pevd_last_error(void) { return last_error(); }
+const char* pevd_version(void) { return "pevd 0.1.0 (sm_100a, FP64 DMMA)"; }
+
+int64_t pevd_syevd_workspace_bytes(int64_t n, int b, int want_vectors, int order) {
+  if (n < 1) return 0;
+  if (b > n - 1) b = (int)std::max<int64_t>(n - 1, 1);
+  return plan_layout(nullptr, n, b, want_vectors, order).total + 4096;
+}
+
+int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
+                      int64_t ldq, int want_vectors, int order, void* workspace,
+                      int64_t workspace_bytes, void* stream, pevd_stats* stats) {
+  if (n < 1 || lda < n || (want_vectors && (!Q || ldq < n)) || b < 1) {
+    set_error("pevd_syevd_device: bad arguments (n=%lld, b=%d)", (long long)n, b);
+    return ERR_VALUE;
+  }
+  if (order < 0 || order > 2) {
+    set_error("order must be 0 (pipelined), 1 (sequential) or 2 (conventional)");
+    return ERR_VALUE;
+  }
+  cudaStream_t sm = (cudaStream_t)stream;
+  if (stats) memset(stats, 0, sizeof(*stats));
+  // trivial sizes (pipeline.py:90-93: b = min(b, n-1); n == 1 has nothing to reduce)
+  if (n == 1) {
+    PEVD_CUDA(cudaMemcpyAsync(lam, A, 8, cudaMemcpyDeviceToDevice, sm));
+    if (want_vectors) {
+      const double one = 1.0;
+      PEVD_CUDA(cudaMemcpyAsync(Q, &one, 8, cudaMemcpyHostToDevice, sm));
+    }
+    PEVD_CUDA(cudaStreamSynchronize(sm));
+    return OK;
+  }
+  b = (int)std::min<int64_t>(b, n - 1);
+  if (b > 32) {
+    set_error("bandwidth b=%d > 32 is not supported by the device kernels", b);
+    return ERR_VALUE;
+  }
+  Layout L = plan_layout(workspace, n, b, want_vectors, order);
+  if (workspace_bytes < L.total) {
+    set_error("workspace too small: %lld < %lld bytes", (long long)workspace_bytes,
+              (long long)L.total);
+    return ERR_VALUE;
+  }
+  cudaStream_t sb = nullptr;
+  const bool two_streams = want_vectors && order == PEVD_ORDER_PIPELINED;
+  if (two_streams) PEVD_CUDA(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
+  Ev ev[6];
+  for (auto& e : ev) {
+    PEVD_CUDA(cudaEventCreate(&e.a));
+    PEVD_CUDA(cudaEventCreate(&e.b));
+  }
+  auto cleanup = [&]() {
+    for (auto& e : ev) {
+      if (e.a) cudaEventDestroy(e.a);
+      if (e.b) cudaEventDestroy(e.b);
+    }
+    if (sb) cudaStreamDestroy(sb);
+  };
+  int rc = OK;
+  int info = 0;
+  do {
+    cudaStream_t sback = two_streams ? sb : sm;
+    // ---- SBR
+    if ((rc = (cudaEventRecord(ev[0].a, sm) == cudaSuccess) ? OK : ERR_CUDA)) break;
+    if ((rc = sbr_reduce(sm, n, b, A, lda, L.bands, want_vectors ? L.Tall : nullptr, L.ws_sbr)))
+      break;
+    cudaEventRecord(ev[0].b, sm);
+    // ---- SBR-Back (forms Q_s) overlapping the chase
+    if (want_vectors && order != PEVD_ORDER_CONVENTIONAL) {
+      if (two_streams) cudaStreamWaitEvent(sback, ev[0].b, 0);
+      cudaEventRecord(ev[3].a, sback);
+      if ((rc = sbr_back_form(sback, n, b, A, L.Tall, L.Qs, n, L.ws_back))) break;
+      cudaEventRecord(ev[3].b, sback);
+    }
+    // ---- BC
+    cudaEventRecord(ev[1].a, sm);
+    if ((rc = bc_reduce(sm, n, b, L.bands, L.d, L.e, want_vectors ? L.tau : nullptr,
+                        want_vectors ? L.V : nullptr, L.vld, L.ws_bc)))
+      break;
+    cudaEventRecord(ev[1].b, sm);
+    // ---- BC-Back on Q_s (back stream) overlapping the divide and conquer
+    if (want_vectors && order != PEVD_ORDER_CONVENTIONAL) {
+      if (two_streams) cudaStreamWaitEvent(sback, ev[1].b, 0);
+      cudaEventRecord(ev[4].a, sback);
+      if ((rc = bc_back_right(sback, n, b, L.tau, L.V, L.vld, L.Qs, n, n))) break;
+      cudaEventRecord(ev[4].b, sback);
+    }
+    // ---- D&C
+    cudaEventRecord(ev[2].a, sm);
+    if ((rc = stedc(sm, n, L.d, L.e, L.Qd, n, L.ws_dc, &info))) break;
+    cudaEventRecord(ev[2].b, sm);
+    if ((rc = (cudaMemcpyAsync(lam, L.d, n * 8, cudaMemcpyDeviceToDevice, sm) == cudaSuccess)
+                  ? OK
+                  : ERR_CUDA))
+      break;
+    if (want_vectors) {
+      if (order == PEVD_ORDER_CONVENTIONAL) {
+        cudaEventRecord(ev[4].a, sm);
+        if ((rc = bc_back_left(sm, n, b, L.tau, L.V, L.vld, L.Qd, n, n))) break;
+        cudaEventRecord(ev[4].b, sm);
+        cudaEventRecord(ev[3].a, sm);
+        if ((rc = sbr_back_apply_left(sm, n, b, A, L.Tall, L.Qd, n, n, L.ws_back))) break;
+        cudaEventRecord(ev[3].b, sm);
+        cudaEventRecord(ev[5].a, sm);
+        if (cudaMemcpy2DAsync(Q, ldq * 8, L.Qd, n * 8, n * 8, n, cudaMemcpyDeviceToDevice, sm) !=
+            cudaSuccess) {
+          rc = ERR_CUDA;
+          break;
+        }
+        cudaEventRecord(ev[5].b, sm);
+      } else {
+        if (two_streams) cudaStreamWaitEvent(sm, ev[4].b, 0);
+        cudaEventRecord(ev[5].a, sm);
+        GemmArgs g{n, n, n, 1.0, 0.0, L.Qs, n, L.Qd, n, Q, ldq, 0, 0, A_GENERAL, C_ALL};
+        if ((rc = gemm(sm, g, nullptr, 0))) break;
+        cudaEventRecord(ev[5].b, sm);
+      }
+    }
+    if (cudaStreamSynchronize(sm) != cudaSuccess) {
+      set_error("device failure: %s", cudaGetErrorString(cudaGetLastError()));
+      rc = ERR_CUDA;
+      break;
+    }
+    if (info != 0) {
+      set_error(info > 0 ? "tridiagonal divide and conquer: leaf QL/QR did not converge near row %d"
+                         : "tridiagonal divide and conquer: secular equation did not converge "
+                           "(root %d)",
+                info > 0 ? info - 1 : -info - 1);
+      rc = ERR_CONVERGE;
+      break;
+    }
+    if (stats) {
+      auto el = [&](cudaEvent_t x) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[0].a, x);
+        return (double)ms;
+      };
+      stats->sbr_ms[0] = 0.0; stats->sbr_ms[1] = el(ev[0].b);
+      stats->bc_ms[0] = el(ev[1].a); stats->bc_ms[1] = el(ev[1].b);
+      stats->solver_ms[0] = el(ev[2].a); stats->solver_ms[1] = el(ev[2].b);
+      if (want_vectors) {
+        stats->sbr_back_ms[0] = el(ev[3].a); stats->sbr_back_ms[1] = el(ev[3].b);
+        stats->bc_back_ms[0] = el(ev[4].a); stats->bc_back_ms[1] = el(ev[4].b);
+        stats->final_ms[0] = el(ev[5].a); stats->final_ms[1] = el(ev[5].b);
+      }
+      double tot = stats->solver_ms[1];
+      tot = std::max(tot, stats->final_ms[1]);
+      stats->total_ms = tot;
+      stats->n_reflectors = bc_num_reflectors(n, b);
+      stats->n_rounds = sbr_num_rounds(n, b);
+    }
+  } while (0);
+  if (rc == ERR_CUDA && g_err[0] == '\0') set_error("CUDA failure");
+  cleanup();
+  return rc;
+}
+
+int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q, int64_t ldq,
+               int want_vectors, int order, pevd_stats* stats) {
+  if (n < 1 || lda < n || !A || !lam || (want_vectors && (!Q || ldq < n))) {
+    set_error("pevd_syevd: bad arguments");
+    return ERR_VALUE;
+  }
+  const int bb = (int)std::min<int64_t>(std::max(b, 1), std::max<int64_t>(n - 1, 1));
+  const int64_t wsb = pevd_syevd_workspace_bytes(n, bb, want_vectors, order);
+  double *dA = nullptr, *dlam = nullptr, *dQ = nullptr;
+  void* ws = nullptr;
+  int rc = OK;
+  auto fail_alloc = [&](const char* what) {
+    set_error("device allocation failed (%s)", what);
+    rc = ERR_NOMEM;
+  };
+  if (cudaMalloc(&dA, n * n * 8) != cudaSuccess) fail_alloc("A");
+  else if (cudaMalloc(&dlam, n * 8) != cudaSuccess) fail_alloc("lam");
+  else if (want_vectors && cudaMalloc(&dQ, n * n * 8) != cudaSuccess) fail_alloc("Q");
+  else if (cudaMalloc(&ws, wsb) != cudaSuccess) fail_alloc("workspace");
+  if (rc == OK) {
+    if (cudaMemcpy2D(dA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice) != cudaSuccess) {
+      set_error("H2D copy failed");
+      rc = ERR_CUDA;
+    }
+  }
+  if (rc == OK)
+    rc = pevd_syevd_device(n, b, dA, n, dlam, dQ, n, want_vectors, order, ws, wsb, nullptr, stats);
+  if (rc == OK) {
+    if (cudaMemcpy(lam, dlam, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) rc = ERR_CUDA;
+    if (rc == OK && want_vectors &&
+        cudaMemcpy2D(Q, ldq * 8, dQ, n * 8, n * 8, n, cudaMemcpyDeviceToHost) != cudaSuccess)
+      rc = ERR_CUDA;
+    if (rc != OK) set_error("D2H copy failed");
+  }
+  cudaFree(dA);
+  cudaFree(dlam);
+  cudaFree(dQ);
+  cudaFree(ws);
+  return rc;
+}
+
+int pevd_dgemm(int transA, int transB, int64_t m, int64_t n, int64_t k, double alpha,
+               const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+               int64_t ldc, void* workspace, int64_t workspace_bytes, void* stream) {
+  GemmArgs g{m, n, k, alpha, beta, A, lda, B, ldb, C, ldc, transA, transB, A_GENERAL, C_ALL};
+  return gemm((cudaStream_t)stream, g, (double*)workspace, workspace_bytes / 8);
+}
+
+int64_t pevd_panel_qr_workspace_bytes(void) { return panel_qr_ws_bytes(); }
+
+int pevd_panel_qr(int64_t m, int k, const double* P, int64_t ldp, double* R, double* Y,
+                  int64_t ldy, double* W, int64_t ldw, double* T, void* workspace, void* stream) {
+  return panel_qr((cudaStream_t)stream, m, k, P, ldp, R, Y, ldy, nullptr, 0, W, ldw, T, workspace);
+}
+
+int64_t pevd_sbr_workspace_bytes(int64_t n, int b) { return sbr_ws_bytes(n, b); }
+
+int pevd_sbr(int64_t n, int b, double* A, int64_t lda, double* bands, double* Tall,
+             void* workspace, void* stream) {
+  return sbr_reduce((cudaStream_t)stream, n, b, A, lda, bands, Tall, workspace);
+}
+
+int64_t pevd_bc_num_reflectors(int64_t n, int b) { return n >= 3 ? bc_num_reflectors(n, b) : 0; }
+int64_t pevd_bc_workspace_bytes(int64_t n, int b) { return bc_ws_bytes(n, b); }
+
+int pevd_bc(int64_t n, int b, const double* bands, double* d, double* e, double* tau, double* V,
+            int vld, void* workspace, void* stream) {
+  return bc_reduce((cudaStream_t)stream, n, b, bands, d, e, tau, V, vld, workspace);
+}
+
+int64_t pevd_stedc_workspace_bytes(int64_t n) { return stedc_ws_bytes(n); }
+
+int pevd_stedc(int64_t n, double* d, const double* e, double* Q, int64_t ldq, void* workspace,
+               void* stream) {
+  int info = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  PEVD_TRY(stedc(st, n, d, e, Q, ldq, workspace, &info));
+  PEVD_CUDA(cudaStreamSynchronize(st));
+  if (info != 0) {
+    set_error("tridiagonal divide and conquer did not converge (info=%d)", info);
+    return ERR_CONVERGE;
+  }
+  return OK;
+}
+
+int64_t pevd_sbr_back_workspace_bytes(int64_t n, int b) { return sbr_back_ws_bytes(n, b); }
+
+int pevd_sbr_back_form(int64_t n, int b, const double* Ystair, const double* Tall, double* Qs,
+                       int64_t ldq, void* workspace, void* stream) {
+  return sbr_back_form((cudaStream_t)stream, n, b, Ystair, Tall, Qs, ldq, workspace);
+}
+
+int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, const double* Tall, double* X,
+                       int64_t ldx, int64_t ncols, void* workspace, void* stream) {
+  return sbr_back_apply_left((cudaStream_t)stream, n, b, Ystair, Tall, X, ldx, ncols, workspace);
+}
+
+int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
+                       int64_t ldx, int64_t nrows, void* stream) {
+  return bc_back_right((cudaStream_t)stream, n, b, tau, V, vld, X, ldx, nrows);
+}
+
+int pevd_bc_back_left(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
+                      int64_t ldx, int64_t ncols, void* stream) {
+  return bc_back_left((cudaStream_t)stream, n, b, tau, V, vld, X, ldx, ncols);
+}
+
+}  // extern "C"

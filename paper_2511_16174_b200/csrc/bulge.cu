@@ -1,0 +1,243 @@
+// Bulge chasing, band -> symmetric tridiagonal (bulge.py:170-252), as a wavefront over sweeps.
+//
+// One warp executes one chase step (sweep gi, step j) at a time; the band (2b+1 stored
+// subdiagonals, ~25 MB at n=49152, b=32: L2-resident) lives in global memory, column-major with
+// leading dimension LDB: Bd[c*LDB + d] = S[c+d, c].  A persistent grid of warps takes sweeps
+// round-robin.  Sweep gi may run step j once sweep gi-1 has COMPLETED step j+2 (progress
+// counter >= j+3): the regions of (gi, j) and of (gi-1, >= j+3) are then column-disjoint, so the
+// wavefront performs exactly the sequential chase's operations (SURVEY.md §7 hard part 1).
+// Progress counters are published with gpu-scope release and read with acquire; band data is
+// read through L2 (ld.cg) so no stale L1 line is ever used.
+//
+// Per step the warp stages its region in shared memory (lane = row of the window):
+//   left block  S[w0:w0+L, cg:w0]     (the column to annihilate + the bulge columns between)
+//   window      S[w0:w0+L, w0:w0+L]   (symmetric, lower half stored)
+//   coupling    S[w0+L:w0+L+b, w0:w0+L]
+// and applies H = I - tau v v^T exactly as bulge.py:188-249: annihilate, left-apply, two-sided
+// window update, right coupling.  Reflector (gi, j) is written to slot offset(j) + gi, the
+// canonical chase-step-major order of bulge.py:51-60 (tau = 0 marks a step the reference
+// skips because the column is already reduced).
+#include "kernels.cuh"
+
+namespace pevd {
+
+namespace {
+
+constexpr int BMAX = 32;
+constexpr int LDS_ = BMAX + 1;
+constexpr int BC_WARPS = 2;  // warps per CTA
+constexpr int DONE = 1 << 30;
+
+struct WarpSmem {
+  double SL[BMAX * LDS_];
+  double SW[BMAX * LDS_];
+  double SC[BMAX * LDS_];
+  double vs[BMAX];
+  double wv[BMAX];
+};
+
+__global__ void band_to_work(int64_t n, int b, const double* __restrict__ bands,
+                             double* __restrict__ Bd, int64_t LDB, int* __restrict__ prog) {
+  const int64_t total = n * LDB;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx / LDB, d = idx % LDB;
+    Bd[idx] = (d <= b && c + d < n) ? bands[d * n + c] : 0.0;
+    if (d == 0) prog[c] = 0;
+  }
+}
+
+__global__ void work_to_tridiag(int64_t n, const double* __restrict__ Bd, int64_t LDB,
+                                double* __restrict__ d, double* __restrict__ e) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    d[i] = Bd[i * LDB];
+    if (i + 1 < n) e[i] = Bd[i * LDB + 1];
+  }
+}
+
+__global__ void __launch_bounds__(BC_WARPS * 32)
+    bc_chase_kernel(int64_t n, int b, double* __restrict__ Bd, int64_t LDB, int* prog,
+                    double* __restrict__ tau_out, double* __restrict__ V_out, int vld,
+                    int total_warps) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  WarpSmem& S = reinterpret_cast<WarpSmem*>(smraw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const int64_t wglob = (int64_t)blockIdx.x * BC_WARPS + (threadIdx.x >> 5);
+
+  for (int64_t gi = wglob; gi < n - 2; gi += total_warps) {
+    for (int64_t j = 0; gi + 1 + j * b <= n - 2; ++j) {
+      // ---- wait for the predecessor sweep to complete step j+2
+      if (gi > 0) {
+        if (lane == 0) {
+          const int need = (int)(j + 3);
+          while (ld_acquire(prog + gi - 1) < need) {
+          }
+        }
+        __syncwarp();
+      }
+      const int64_t cg = (j == 0) ? gi : gi + 1 + (j - 1) * b;
+      const int64_t w0 = gi + 1 + j * b;
+      const int L = (int)((b < n - w0) ? b : n - w0);
+      const int nleft = (int)(w0 - cg);  // 1 (j = 0) or b
+      const int64_t tend = (w0 + L + b < n) ? w0 + L + b : n;
+      const int nT = (int)(tend - (w0 + L));
+      const int64_t slot = (int64_t)j * (n - 2) - (int64_t)b * j * (j - 1) / 2 + gi;
+
+      // ---- stage the left block (column q = cg + q, rows w0 + r)
+      for (int q = 0; q < nleft; ++q) {
+        if (lane < L)
+          S.SL[lane * LDS_ + q] = __ldcg(Bd + (cg + q) * LDB + (w0 - cg - q) + lane);
+      }
+      __syncwarp();
+      const double x = (lane < L) ? S.SL[lane * LDS_] : 0.0;
+      const double tail = warp_sum((lane >= 1 && lane < L) ? x * x : 0.0);
+      if (tail == 0.0) {
+        // nothing to annihilate: the reference records no reflector here (tau = 0 slot)
+        if (tau_out) {
+          if (lane == 0) tau_out[slot] = 0.0;
+          for (int r = lane; r < vld; r += 32) V_out[slot * vld + r] = (r == 0) ? 1.0 : 0.0;
+        }
+      } else {
+        // ---- stage window (lower -> full) and coupling block
+        for (int c = 0; c < L; ++c) {
+          if (lane >= c && lane < L) {
+            const double val = __ldcg(Bd + (w0 + c) * LDB + (lane - c));
+            S.SW[lane * LDS_ + c] = val;
+            S.SW[c * LDS_ + lane] = val;
+          }
+          if (lane < nT) S.SC[lane * LDS_ + c] = __ldcg(Bd + (w0 + c) * LDB + (L + lane - c));
+        }
+        const double x0 = __shfl_sync(0xffffffffu, x, 0);
+        const double nrm = sqrt(x0 * x0 + tail);
+        const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+        const double denom = x0 - alpha;
+        const double v = (lane == 0) ? 1.0 : ((lane < L) ? x / denom : 0.0);
+        const double vsq = 1.0 + warp_sum((lane >= 1) ? v * v : 0.0);
+        const double tau = 2.0 / vsq;
+        S.vs[lane] = v;
+        if (lane < L) S.SL[lane * LDS_] = (lane == 0) ? alpha : 0.0;
+        __syncwarp();
+        // ---- H from the left on the bulge columns strictly between (lane = column q)
+        if (lane >= 1 && lane < nleft) {
+          const int q = lane;
+          double dot = 0.0;
+          for (int r = 0; r < L; ++r) dot += S.vs[r] * S.SL[r * LDS_ + q];
+          dot *= tau;
+          for (int r = 0; r < L; ++r) S.SL[r * LDS_ + q] -= dot * S.vs[r];
+        }
+        // ---- H A H on the window (lane = row r)
+        double u = 0.0;
+        if (lane < L) {
+          double acc = 0.0;
+          for (int c = 0; c < L; ++c) acc += S.SW[lane * LDS_ + c] * S.vs[c];
+          u = tau * acc;
+        }
+        const double gam = 0.5 * tau * warp_sum(v * u);
+        const double w = u - gam * v;
+        S.wv[lane] = w;
+        // ---- H from the right on the coupling rows (lane = row t)
+        if (lane < nT) {
+          double dot = 0.0;
+          for (int c = 0; c < L; ++c) dot += S.SC[lane * LDS_ + c] * S.vs[c];
+          dot *= tau;
+          for (int c = 0; c < L; ++c) S.SC[lane * LDS_ + c] -= dot * S.vs[c];
+        }
+        __syncwarp();
+        if (lane < L) {
+          for (int c = 0; c <= lane; ++c)
+            S.SW[lane * LDS_ + c] -= v * S.wv[c] + w * S.vs[c];
+        }
+        __syncwarp();
+        // ---- write back
+        for (int q = 0; q < nleft; ++q)
+          if (lane < L) Bd[(cg + q) * LDB + (w0 - cg - q) + lane] = S.SL[lane * LDS_ + q];
+        for (int c = 0; c < L; ++c) {
+          if (lane >= c && lane < L) Bd[(w0 + c) * LDB + (lane - c)] = S.SW[lane * LDS_ + c];
+          if (lane < nT) Bd[(w0 + c) * LDB + (L + lane - c)] = S.SC[lane * LDS_ + c];
+        }
+        if (tau_out) {
+          if (lane == 0) tau_out[slot] = tau;
+          for (int r = lane; r < vld; r += 32) V_out[slot * vld + r] = (r < L) ? S.vs[r] : 0.0;
+        }
+      }
+      // ---- publish progress
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        st_release(prog + gi, (int)(j + 1));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      st_release(prog + gi, DONE);
+    }
+  }
+}
+
+}  // namespace
+
+int64_t bc_num_reflectors(int64_t n, int b) {
+  int64_t tot = 0;
+  for (int64_t j = 0; n - 2 - j * b > 0; ++j) tot += n - 2 - j * b;
+  return tot;
+}
+
+int64_t bc_slot_offset(int64_t n, int b, int64_t j) {
+  return j * (n - 2) - (int64_t)b * j * (j - 1) / 2;
+}
+
+static int64_t bc_ldb(int b) { return (2 * b + 2 + 1) / 2 * 2; }
+
+int64_t bc_ws_bytes(int64_t n, int b) { return n * bc_ldb(b) * 8 + n * 4 + 256; }
+
+int bc_reduce(cudaStream_t st, int64_t n, int b, const double* bands_ref, double* d, double* e,
+              double* tau, double* V, int vld, void* ws) {
+  if (b < 1 || b > BMAX) {
+    set_error("bc_reduce: bandwidth %d outside [1, %d] (device kernel limit)", b, BMAX);
+    return ERR_VALUE;
+  }
+  if (tau && vld < b) {
+    set_error("bc_reduce: reflector stride %d < b=%d", vld, b);
+    return ERR_VALUE;
+  }
+  const int64_t LDB = bc_ldb(b);
+  double* Bd = (double*)ws;
+  int* prog = (int*)(Bd + n * LDB);
+  band_to_work<<<(unsigned)std::min<int64_t>(cdiv(n * LDB, 256), 8192), 256, 0, st>>>(
+      n, b, bands_ref, Bd, LDB, prog);
+  PEVD_LAUNCH_CHECK();
+  if (b >= 2 && n >= 3) {
+    const size_t smem = sizeof(WarpSmem) * BC_WARPS;
+    static int attr_dev = -1;
+    int dev;
+    PEVD_CUDA(cudaGetDevice(&dev));
+    if (attr_dev != dev) {
+      PEVD_CUDA(cudaFuncSetAttribute(bc_chase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+      attr_dev = dev;
+    }
+    int per_sm = 0;
+    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bc_chase_kernel,
+                                                            BC_WARPS * 32, smem));
+    if (per_sm < 1) {
+      set_error("bc_reduce: chase kernel cannot be resident");
+      return ERR_CUDA;
+    }
+    // every warp must be co-resident (warps wait on each other): never exceed one full wave
+    const int64_t need = cdiv(n - 2, BC_WARPS);
+    const int grid = (int)std::min<int64_t>((int64_t)per_sm * num_sms(), need);
+    bc_chase_kernel<<<grid, BC_WARPS * 32, smem, st>>>(n, b, Bd, LDB, prog, tau, V, vld,
+                                                       grid * BC_WARPS);
+    PEVD_LAUNCH_CHECK();
+  } else if (tau && n >= 3) {
+    PEVD_CUDA(cudaMemsetAsync(tau, 0, 8 * bc_num_reflectors(n, b), st));
+  }
+  work_to_tridiag<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4096), 256, 0, st>>>(n, Bd, LDB, d,
+                                                                                  e);
+  PEVD_LAUNCH_CHECK();
+  return OK;
+}
+
+}  // namespace pevd

@@ -1,0 +1,65 @@
+// Internal (C++) interfaces between the translation units of libpevd.so.
+#pragma once
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace pevd {
+
+// ---------------- panel QR (panel_qr.cu)
+int64_t panel_qr_ws_bytes();
+// Householder QR of the m x k panel (col-major, ld ldp): R (k x k, upper, col-major, may be
+// null), explicit unit-lower-trapezoidal Y to Y1/Y2 (either may be null; Y1 may alias the
+// panel), W = Y T (may be null) and T (k x k col-major, may be null).  Q = I - W Y^T, Q^T P = R.
+int panel_qr(cudaStream_t st, int64_t m, int k, const double* panel, int64_t ldp, double* R,
+             double* Y1, int64_t ldy1, double* Y2, int64_t ldy2, double* W, int64_t ldw,
+             double* T, void* ws);
+
+__host__ __device__ __forceinline__ int64_t bc_slot_offset_dev(int64_t n, int b, int64_t j) {
+  return j * (n - 2) - (int64_t)b * j * (j - 1) / 2;
+}
+
+// ---------------- SBR (sbr.cu)
+// Panel factors: panel x (round x of round_schedule(n, b): c0 = x b, t0 = c0 + b, m = n - t0)
+// leaves its explicit unit-lower Y_x in A[t0:, c0:c0+pw] (so after the reduction A holds the
+// "Y staircase": zero above the b-th subdiagonal) and T_x at Tall + x*b*b (pw x pw col-major).
+int64_t sbr_num_rounds(int64_t n, int b);
+int64_t sbr_ws_bytes(int64_t n, int b);
+// Dense (lower triangle of A, col-major lda) -> band.  Outputs: bands_ref (C-order (b+1) x n,
+// bands[d, j] = A[j+d, j]), Tall (may be null); A becomes the Y staircase.
+int sbr_reduce(cudaStream_t st, int64_t n, int b, double* A, int64_t lda, double* bands_ref,
+               double* Tall, void* ws);
+
+// ---------------- bulge chasing (bulge.cu)
+int64_t bc_num_reflectors(int64_t n, int b);     // fixed slots: sum_j (n - 2 - j b)
+int64_t bc_slot_offset(int64_t n, int b, int64_t j);
+int64_t bc_ws_bytes(int64_t n, int b);
+// band (C-order (b+1) x n, reference layout) -> d (n), e (n-1); reflector slots (tau, V with
+// stride vld) in canonical chase-step-major order when tau != null.
+int bc_reduce(cudaStream_t st, int64_t n, int b, const double* bands_ref, double* d, double* e,
+              double* tau, double* V, int vld, void* ws);
+
+// ---------------- tridiagonal divide and conquer (stedc.cu)
+int64_t stedc_ws_bytes(int64_t n);
+// d (n) in: diagonal, out: eigenvalues ascending; e (n-1) off-diagonal (preserved).
+// Q (n x n, ldq) out: eigenvectors.  Sign convention of tridiag.py:325-333 applied.
+int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int64_t ldq,
+          void* ws, int* info_host);
+
+// ---------------- back transformation (backtrans.cu)
+// Q_s = prod_x (I - Y_x T_x Y_x^T) formed explicitly into Qs (n x n, ldq).
+int64_t sbr_back_ws_bytes(int64_t n, int b);
+// (Yfull = the Y staircase left by sbr_reduce, leading dimension n.)
+int sbr_back_form(cudaStream_t st, int64_t n, int b, const double* Yfull, const double* Tall,
+                  double* Qs, int64_t ldq, void* ws);
+// Apply the SBR reflectors from the left to X (n x ncols): X <- Q_s X (conventional order).
+int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, const double* Tall,
+                        double* X, int64_t ldx, int64_t ncols, void* ws);
+// Right-apply the bulge reflectors to the rows of X (nrows x n, col-major ldx):
+// X <- X Q_b  (== (Q_b^T X^T)^T, the reordered BC-Back, backtrans.py:277-310).
+int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
+                  double* X, int64_t ldx, int64_t nrows);
+// Left-apply Q_b to X (n x ncols): X <- Q_b X (conventional BC-Back).
+int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
+                 double* X, int64_t ldx, int64_t ncols);
+
+}  // namespace pevd

@@ -1,0 +1,266 @@
+// Tall-skinny Householder panel QR (the SBR panel factorisation, sbr.py:69-116).
+//
+// One cooperative launch per panel.  Each CTA keeps a contiguous chunk of the m x k panel rows
+// resident in shared memory for the whole factorisation (m <= ~65k, k <= 32 -> <= ~120 KB), so
+// the panel is read from HBM once and written once.  Per column there is exactly one grid-wide
+// reduction: every CTA contributes, for its rows, the tail dot products x_tail^T a_c of the pivot
+// column with all remaining columns (which yields ||x_tail||^2 and v^T a_c = a_c[j] +
+// x_tail^T a_c,tail / (x0 - alpha) without a second pass) and, lagged by one column, the dot
+// products Y(:,0:j-1)^T v_{j-1} that build the T factor (W = Y T, Q = I - W Y^T = I - Y T Y^T).
+// Partials are reduced in a fixed order by every CTA, so all CTAs derive bit-identical alpha,
+// tau and T, and reruns are bitwise reproducible (no atomics on data).
+//
+// Householder convention (core.py:238-255): v[0] = 1, alpha = -sign(x0) ||x||, sign(0) = +,
+// zero tail -> tau = 0, alpha = x0.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace pevd {
+
+namespace {
+
+constexpr int QR_THREADS = 256;
+constexpr int KMAX = 32;
+constexpr int LDP = KMAX + 1;  // smem panel row stride (doubles)
+constexpr int NVAL = 2 * KMAX; // partial values per CTA per step: h[0..31], g[0..31]
+
+struct QrWork {
+  double* part;     // [2][MAXCTA][NVAL], double-buffered by step parity
+  double* piv;      // [2][KMAX]
+  unsigned* bar;    // [2] barrier count / generation
+};
+constexpr int MAXCTA = 1024;
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicExch(bar + 1, gen + 1);
+    } else {
+      while (*vgen == gen) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(QR_THREADS)
+    panel_qr_kernel(int64_t m, int k, const double* panel, int64_t ldp, double* Rout,
+                    double* Y1, int64_t ldy1, double* Y2, int64_t ldy2,
+                    double* __restrict__ W, int64_t ldw, double* __restrict__ Tout,
+                    QrWork wk, int64_t rows_per_cta) {
+  extern __shared__ __align__(16) double sm[];
+  double* P = sm;                                      // [rows_per_cta][LDP]
+  double* red = P + rows_per_cta * LDP;                // [4][NVAL]
+  double* hv = red + 4 * NVAL;                         // [NVAL] reduced values
+  double* T = hv + NVAL;                               // [KMAX][KMAX] col-major T
+  double* coef = T + KMAX * KMAX;                      // [KMAX]
+  double* scal = coef + KMAX;                          // [4]: denom, tau, alpha, flag
+  double* taus = scal + 4;                             // [KMAX]
+
+  const int tid = threadIdx.x;
+  const unsigned ncta = gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = r0 + rows_per_cta < m ? r0 + rows_per_cta : m;
+  const int nr = (int)(r1 > r0 ? r1 - r0 : 0);
+
+  // load the row chunk (coalesced along rows, column by column)
+  for (int c = 0; c < k; ++c)
+    for (int lr = tid; lr < nr; lr += QR_THREADS) P[lr * LDP + c] = panel[r0 + lr + c * ldp];
+  for (int i = tid; i < KMAX * KMAX; i += QR_THREADS) T[i] = 0.0;
+  __syncthreads();
+
+  for (int j = 0; j <= k; ++j) {
+    // ---- partial sums for this CTA's rows
+    {
+      const int vi = tid % NVAL, grp = tid / NVAL;  // 4 groups
+      double s = 0.0;
+      if (vi < KMAX) {
+        const int c = vi;
+        if (j < k && c >= j && c < k) {
+          for (int lr = grp; lr < nr; lr += 4) {
+            const int64_t r = r0 + lr;
+            if (r > j) s += P[lr * LDP + j] * P[lr * LDP + c];
+          }
+        }
+      } else {
+        const int q = vi - KMAX;
+        const int jp = j - 1;  // previous reflector
+        if (jp >= 1 && q < jp) {
+          for (int lr = grp; lr < nr; lr += 4) {
+            const int64_t r = r0 + lr;
+            if (r >= jp) {
+              const double v = (r == jp) ? 1.0 : P[lr * LDP + jp];
+              s += P[lr * LDP + q] * v;
+            }
+          }
+        }
+      }
+      red[grp * NVAL + vi] = s;
+    }
+    // the CTA holding the pivot row publishes it
+    // (buffers alternate by step parity: a CTA can run at most one barrier ahead, so it never
+    //  overwrites values a slower CTA has yet to read)
+    double* part = wk.part + (j & 1) * (MAXCTA * NVAL);
+    double* piv = wk.piv + (j & 1) * KMAX;
+    if (j < k && j >= r0 && j < r1 && tid < k) {
+      piv[tid] = P[(j - r0) * LDP + tid];
+    }
+    __syncthreads();
+    if (tid < NVAL) {
+      const double s = red[tid] + red[NVAL + tid] + red[2 * NVAL + tid] + red[3 * NVAL + tid];
+      part[(int64_t)blockIdx.x * NVAL + tid] = s;
+    }
+    grid_barrier(wk.bar, ncta);
+    // ---- deterministic reduction of all CTA partials (identical in every CTA)
+    {
+      const int vi = tid % NVAL, grp = tid / NVAL;
+      double s = 0.0;
+      for (unsigned p = grp; p < ncta; p += 4) s += __ldcg(part + (int64_t)p * NVAL + vi);
+      red[grp * NVAL + vi] = s;
+    }
+    __syncthreads();
+    if (tid < NVAL) hv[tid] = red[tid] + red[NVAL + tid] + red[2 * NVAL + tid] + red[3 * NVAL + tid];
+    if (tid < KMAX) coef[tid] = (j < k && tid >= j && tid < k) ? __ldcg(piv + tid) : 0.0;
+    __syncthreads();
+    // ---- T column j-1: T[0:jp, jp] = -tau_jp * T[0:jp, 0:jp] * g[0:jp]
+    if (j >= 1 && tid == 0) {
+      const int jp = j - 1;
+      const double tj = taus[jp];
+      T[jp + jp * KMAX] = tj;
+      for (int q = jp - 1; q >= 0; --q) {  // upper triangular mat-vec, rows q
+        double s = 0.0;
+        for (int t = q; t < jp; ++t) s += T[q + t * KMAX] * hv[KMAX + t];
+        T[q + jp * KMAX] = -tj * s;
+      }
+    }
+    if (j == k) break;
+    // ---- reflector j (thread 0 computes scalars; everyone reads them)
+    if (tid == 0) {
+      const double x0 = coef[j];
+      const double tail2 = hv[j];
+      if (tail2 == 0.0) {
+        scal[0] = 1.0; scal[1] = 0.0; scal[2] = x0; scal[3] = 0.0;
+      } else {
+        const double nrm = sqrt(x0 * x0 + tail2);
+        const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+        const double denom = x0 - alpha;
+        const double tau = 2.0 / (1.0 + tail2 / (denom * denom));
+        scal[0] = denom; scal[1] = tau; scal[2] = alpha; scal[3] = 1.0;
+      }
+      taus[j] = scal[1];
+    }
+    __syncthreads();
+    const double denom = scal[0], tau = scal[1], alpha = scal[2];
+    const bool active = scal[3] != 0.0;
+    // coefficients tau * v^T a_c for c > j
+    if (tid < KMAX) {
+      const int c = tid;
+      double cf = 0.0;
+      if (active && c > j && c < k) cf = tau * (coef[c] + hv[c] / denom);
+      red[c] = cf;  // reuse red[0..31] (all reads of red are done)
+    }
+    __syncthreads();
+    // ---- column j becomes v (rows > j) and alpha (row j); then apply H_j to columns > j
+    for (int lr = tid; lr < nr; lr += QR_THREADS) {
+      const int64_t r = r0 + lr;
+      if (r > j) P[lr * LDP + j] = active ? P[lr * LDP + j] / denom : 0.0;
+    }
+    __syncthreads();
+    if (active) {
+      for (int idx = tid; idx < nr * KMAX; idx += QR_THREADS) {
+        const int lr = idx / KMAX, c = idx % KMAX;
+        const int64_t r = r0 + lr;
+        if (r < j || c <= j || c >= k) continue;
+        const double v = (r == j) ? 1.0 : P[lr * LDP + j];
+        P[lr * LDP + c] -= red[c] * v;
+      }
+    }
+    __syncthreads();
+    if (j >= r0 && j < r1 && tid == 0) P[(j - r0) * LDP + j] = alpha;
+    __syncthreads();
+  }
+  __syncthreads();
+
+  // ---- outputs: R (k x k upper), explicit unit-lower Y (may overwrite the input panel), W, T
+  for (int c = 0; c < k; ++c) {
+    for (int lr = tid; lr < nr; lr += QR_THREADS) {
+      const int64_t r = r0 + lr;
+      const double pv = P[lr * LDP + c];
+      const double y = (r > c) ? pv : (r == c ? 1.0 : 0.0);
+      if (Rout && r < k) Rout[r + c * k] = (r <= c) ? pv : 0.0;
+      if (Y1) Y1[r + c * ldy1] = y;
+      if (Y2) Y2[r + c * ldy2] = y;
+    }
+  }
+  if (W) {
+    for (int idx = tid; idx < nr * k; idx += QR_THREADS) {
+      const int lr = idx % nr, c = idx / nr;
+      const int64_t r = r0 + lr;
+      double s = 0.0;
+      for (int q = 0; q <= c; ++q) {
+        const double y = (r > q) ? P[lr * LDP + q] : (r == q ? 1.0 : 0.0);
+        s += y * T[q + c * KMAX];
+      }
+      W[r + c * ldw] = s;
+    }
+  }
+  if (Tout && blockIdx.x == 0) {
+    for (int i = tid; i < k * k; i += QR_THREADS) {
+      const int q = i % k, c = i / k;
+      Tout[q + c * k] = T[q + c * KMAX];
+    }
+  }
+}
+
+}  // namespace
+
+int64_t panel_qr_ws_bytes() { return (int64_t)(2 * MAXCTA * NVAL + 2 * KMAX + 16) * 8; }
+
+int panel_qr(cudaStream_t st, int64_t m, int k, const double* panel, int64_t ldp, double* R,
+             double* Y1, int64_t ldy1, double* Y2, int64_t ldy2, double* W, int64_t ldw,
+             double* T, void* ws) {
+  if (k < 1 || k > KMAX) {
+    set_error("panel_qr: panel width %d outside [1, %d]", k, KMAX);
+    return ERR_VALUE;
+  }
+  if (m < k) {
+    set_error("panel_qr: panel must be at least as tall as wide (m=%lld, k=%d)", (long long)m, k);
+    return ERR_VALUE;
+  }
+  const int sms = num_sms();
+  int ncta = (int)std::min<int64_t>(sms, cdiv(m, 96));
+  if (ncta < 1) ncta = 1;
+  int64_t rows = cdiv(m, ncta);
+  ncta = (int)cdiv(m, rows);
+  const size_t smem = (size_t)(rows * LDP + 4 * NVAL + NVAL + KMAX * KMAX + KMAX + 4 + KMAX) * 8;
+  if (smem > 227 * 1024) {
+    set_error("panel_qr: panel too tall for the resident-panel kernel (m=%lld)", (long long)m);
+    return ERR_VALUE;
+  }
+  static int attr_dev = -1;
+  int dev;
+  PEVD_CUDA(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    PEVD_CUDA(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+    attr_dev = dev;
+  }
+  QrWork wk;
+  wk.part = (double*)ws;
+  wk.piv = wk.part + 2 * MAXCTA * NVAL;
+  wk.bar = (unsigned*)(wk.piv + 2 * KMAX);
+  PEVD_CUDA(cudaMemsetAsync(wk.bar, 0, 2 * sizeof(unsigned), st));
+  void* args[] = {&m, &k, &panel, &ldp, &R, &Y1, &ldy1, &Y2, &ldy2, &W, &ldw, &T, &wk, &rows};
+  PEVD_CUDA(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel, dim3(ncta),
+                                        dim3(QR_THREADS), args, smem, st));
+  return OK;
+}
+
+}  // namespace pevd

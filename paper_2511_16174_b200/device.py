@@ -1,0 +1,231 @@
+"""Per-stage device operations over the C ABI (include/pevd.h).
+
+Each function mirrors one reference function (file:line in the docstring) and runs it on the
+GPU through libpevd.so.  Matrices cross the boundary column-major (Fortran order): a
+column-major n x m matrix lives in a torch tensor of shape (m, n).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+
+def _torch():
+    return _lib.require_cuda()
+
+
+def _stream():
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def to_dev(a: np.ndarray):
+    """numpy matrix -> column-major device tensor (shape (cols, rows))."""
+    torch = _torch()
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim == 1:
+        return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
+
+
+def from_dev(t, rows: int | None = None) -> np.ndarray:
+    """column-major device tensor -> numpy (Fortran-ordered) matrix."""
+    h = t.detach().cpu().numpy()
+    if h.ndim == 1:
+        return h
+    return np.asfortranarray(h.T)
+
+
+def empty(rows: int, cols: int = 0):
+    torch = _torch()
+    if cols == 0:
+        return torch.empty(max(rows, 1), dtype=torch.float64, device="cuda")
+    return torch.empty((max(cols, 1), max(rows, 1)), dtype=torch.float64, device="cuda")
+
+
+def workspace(nbytes: int):
+    torch = _torch()
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device="cuda")
+
+
+def _p(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def dgemm(a, b, alpha=1.0, beta=0.0, c=None, trans_a=False, trans_b=False):
+    """C = alpha op(A) op(B) + beta C on the FP64 DMMA GEMM (core.py:309-319 matmul_counted)."""
+    L = _lib.load()
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    m = a.shape[1] if trans_a else a.shape[0]
+    k = a.shape[0] if trans_a else a.shape[1]
+    n = b.shape[0] if trans_b else b.shape[1]
+    da, db = to_dev(a), to_dev(b)
+    dc = to_dev(c) if c is not None else empty(m, n)
+    ws = workspace(8 << 20 * 1)
+    rc = L.pevd_dgemm(int(trans_a), int(trans_b), m, n, k, alpha, _p(da), a.shape[0], _p(db),
+                      b.shape[0], beta, _p(dc), m, _p(ws), ws.numel(), _stream())
+    _lib.check(rc, "dgemm")
+    return from_dev(dc)
+
+
+def panel_qr(panel):
+    """Householder panel QR (sbr.py:69-116) -> (R, Y, W, T); Q = I - W Y^T, Q^T P = R."""
+    L = _lib.load()
+    p = np.asarray(panel, dtype=np.float64)
+    m, k = p.shape
+    dp = to_dev(p)
+    dr, dy, dw, dt = empty(k, k), empty(m, k), empty(m, k), empty(k, k)
+    ws = workspace(L.pevd_panel_qr_workspace_bytes())
+    rc = L.pevd_panel_qr(m, k, _p(dp), m, _p(dr), _p(dy), m, _p(dw), m, _p(dt), _p(ws), _stream())
+    _lib.check(rc, "panel_qr")
+    return from_dev(dr), from_dev(dy), from_dev(dw), from_dev(dt)
+
+
+def sbr(a, b):
+    """Band reduction (sbr.py:155-188) -> (bands (b+1, n), Y staircase (n, n), Tall (R, b, b))."""
+    L = _lib.load()
+    a = np.asarray(a, dtype=np.float64)
+    n = a.shape[0]
+    da = to_dev(a)
+    torch = _torch()
+    bands = torch.empty((b + 1) * n, dtype=torch.float64, device="cuda")
+    rounds = max(1, -(-(n - b) // b))
+    tall = torch.zeros(rounds * b * b, dtype=torch.float64, device="cuda")
+    ws = workspace(L.pevd_sbr_workspace_bytes(n, b))
+    rc = L.pevd_sbr(n, b, _p(da), n, _p(bands), _p(tall), _p(ws), _stream())
+    _lib.check(rc, "sbr")
+    tall_h = tall.cpu().numpy().reshape(rounds, b, b).transpose(0, 2, 1)  # col-major blocks
+    return bands.cpu().numpy().reshape(b + 1, n), from_dev(da), tall_h
+
+
+def bc(bands, want_reflectors=True):
+    """Bulge chasing (bulge.py:299-309) -> (d, e, tau slots, V slots (nslots x vld))."""
+    L = _lib.load()
+    bands = np.ascontiguousarray(bands, dtype=np.float64)
+    b = bands.shape[0] - 1
+    n = bands.shape[1]
+    torch = _torch()
+    dbands = torch.from_numpy(bands.reshape(-1)).cuda()
+    d, e = empty(n), empty(max(n - 1, 1))
+    nref = L.pevd_bc_num_reflectors(n, b)
+    vld = ((b + 7) // 8) * 8
+    tau = torch.zeros(max(nref, 1), dtype=torch.float64, device="cuda") if want_reflectors else None
+    V = torch.zeros(max(nref, 1) * vld, dtype=torch.float64, device="cuda") if want_reflectors else None
+    ws = workspace(L.pevd_bc_workspace_bytes(n, b))
+    rc = L.pevd_bc(n, b, _p(dbands), _p(d), _p(e), _p(tau), _p(V), vld, _p(ws), _stream())
+    _lib.check(rc, "bc")
+    out_tau = tau.cpu().numpy()[:nref] if want_reflectors else None
+    out_v = V.cpu().numpy()[: nref * vld].reshape(nref, vld) if want_reflectors else None
+    return d.cpu().numpy()[:n], e.cpu().numpy()[: n - 1], out_tau, out_v
+
+
+def slot_offset(n: int, b: int, j: int) -> int:
+    """Fixed reflector slot layout of pevd_bc: slot(i, j) = offset(j) + i (include/pevd.h)."""
+    return j * (n - 2) - b * j * (j - 1) // 2
+
+
+def slots_to_reference(n: int, b: int, tau, V):
+    """Fixed slots -> the reference BulgeReflectorSet arrays (bulge.py:33-68): only recorded
+    reflectors (tau != 0), canonical order (chase step j outer, sweep i inner)."""
+    i_l, j_l, r_l, l_l, t_l, v_l = [], [], [], [], [], []
+    stride = ((b + 7) // 8) * 8
+    j = 0
+    while n - 2 - j * b > 0:
+        off = slot_offset(n, b, j)
+        for i in range(n - 2 - j * b):
+            t = tau[off + i]
+            if t != 0.0:
+                r0 = i + 1 + j * b
+                i_l.append(i); j_l.append(j); r_l.append(r0); l_l.append(min(b, n - r0))
+                t_l.append(t)
+                vv = np.zeros(stride)
+                vv[: V.shape[1]] = V[off + i][:stride]
+                v_l.append(vv)
+        j += 1
+    return dict(i=np.array(i_l, np.int64), j=np.array(j_l, np.int64),
+                row0=np.array(r_l, np.int64), len=np.array(l_l, np.int64),
+                tau=np.array(t_l), v=np.array(v_l).reshape(len(t_l), stride))
+
+
+def stedc(d, e):
+    """Tridiagonal divide and conquer (replaces tridiag_eig, tridiag.py:298-334) -> (lam, Q)."""
+    L = _lib.load()
+    d = np.asarray(d, dtype=np.float64)
+    n = d.shape[0]
+    dd = to_dev(d)
+    de = to_dev(np.asarray(e, dtype=np.float64) if n > 1 else np.zeros(1))
+    q = empty(n, n)
+    ws = workspace(L.pevd_stedc_workspace_bytes(n))
+    rc = L.pevd_stedc(n, _p(dd), _p(de), _p(q), n, _p(ws), _stream())
+    if rc == _lib.PEVD_ERR_CONVERGE:
+        raise RuntimeError(L.pevd_last_error().decode())
+    _lib.check(rc, "stedc")
+    return dd.cpu().numpy()[:n], from_dev(q)
+
+
+def sbr_back_form(n, b, ystair, tall):
+    """Q_s = prod (I - Y_x T_x Y_x^T) (backtrans.py:128-146, all columns)."""
+    L = _lib.load()
+    torch = _torch()
+    dy = to_dev(ystair)
+    rounds = tall.shape[0]
+    dt = torch.from_numpy(np.ascontiguousarray(np.asarray(tall).transpose(0, 2, 1)).reshape(-1)).cuda()
+    q = empty(n, n)
+    ws = workspace(L.pevd_sbr_back_workspace_bytes(n, b))
+    rc = L.pevd_sbr_back_form(n, b, _p(dy), _p(dt), _p(q), n, _p(ws), _stream())
+    _lib.check(rc, "sbr_back_form")
+    del rounds
+    return from_dev(q)
+
+
+def bc_back_right(n, b, tau, V, x):
+    """X <- X Q_b (reordered BC-Back, backtrans.py:277-310, transposed)."""
+    L = _lib.load()
+    torch = _torch()
+    x = np.asarray(x, dtype=np.float64)
+    vld = V.shape[1]
+    dt = torch.from_numpy(np.ascontiguousarray(tau)).cuda()
+    dv = torch.from_numpy(np.ascontiguousarray(V).reshape(-1)).cuda()
+    dx = to_dev(x)
+    rc = L.pevd_bc_back_right(n, b, _p(dt), _p(dv), vld, _p(dx), x.shape[0], x.shape[0], _stream())
+    _lib.check(rc, "bc_back_right")
+    return from_dev(dx)
+
+
+def bc_back_left(n, b, tau, V, x):
+    """X <- Q_b X (conventional BC-Back, backtrans.py:277-310)."""
+    L = _lib.load()
+    torch = _torch()
+    x = np.asarray(x, dtype=np.float64)
+    vld = V.shape[1]
+    dt = torch.from_numpy(np.ascontiguousarray(tau)).cuda()
+    dv = torch.from_numpy(np.ascontiguousarray(V).reshape(-1)).cuda()
+    dx = to_dev(x)
+    rc = L.pevd_bc_back_left(n, b, _p(dt), _p(dv), vld, _p(dx), x.shape[0], x.shape[1], _stream())
+    _lib.check(rc, "bc_back_left")
+    return from_dev(dx)
+
+
+def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None):
+    """Whole single-GPU EVD through pevd_syevd_device: (lam, Q or None, PevdStats)."""
+    L = _lib.load()
+    torch = _torch()
+    a = np.asarray(a, dtype=np.float64)
+    n = a.shape[0]
+    oc = _lib.ORDER_CODES[order]
+    bb = max(1, min(b, n - 1)) if n > 1 else 1
+    da = to_dev(a)
+    lam = empty(n)
+    q = empty(n, n) if want_vectors else None
+    ws = workspace(L.pevd_syevd_workspace_bytes(n, bb, int(want_vectors), oc))
+    st = _lib.PevdStats() if stats is None else stats
+    rc = L.pevd_syevd_device(n, bb, _p(da), n, _p(lam), _p(q), n, int(want_vectors), oc, _p(ws),
+                             ws.numel(), _stream(), ctypes.byref(st))
+    if rc == _lib.PEVD_ERR_CONVERGE:
+        raise RuntimeError(L.pevd_last_error().decode())
+    _lib.check(rc, "syevd")
+    return lam.cpu().numpy()[:n], (from_dev(q) if want_vectors else None), st
