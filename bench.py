@@ -1,0 +1,300 @@
+"""Benchmark: FP64 EVD TFLOP/s (4 n^3 / wall, eigenvectors) at n = 49152 on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--n 49152]
+
+One step = one full two-stage EVD with eigenvectors of a synthetic random symmetric matrix
+(A = (G + G^T)/2, G ~ N(0,1) from a seeded torch generator on the device).  `value` times the
+device-resident path (pevd_syevd_device, input already in HBM; A is 19.3 GB, far larger than the
+126 MB L2, so no L2 flush is needed); `e2e` times the C-ABI call with HOST buffers
+(pevd_syevd: pinned host A in, lambda and Q out, device allocation included).  Under torchrun
+(N > 1) every rank solves its own EVD (replicas; the blockwise multi-GPU EVD is not wired into
+the bench yet) and value = N * 4 n^3 / max-over-ranks time.
+
+--impl reference times the CPU oracle (oracle/: C + numpy restatement of the reference package,
+pinned bit-exact to it) on a bounded sample (n=1024 per step) with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 EVD TFLOPS + wall time (n=49152, with eigvecs) at 1/2/4/8 B200"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev, self.rows, self._stop = dev, [], threading.Event()
+        self._th = threading.Thread(target=self._loop, daemon=True)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.25)
+
+    def __enter__(self):
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def stage_flops(n: int):
+    """Algorithmic FP64 flops per stage; BC-Back as its BLAS2 count."""
+    return {"sbr": 4 * n ** 3 / 3, "sbr_back": 4 * n ** 3 / 3, "bc_back": 2 * n ** 3,
+            "final": 2 * n ** 3, "solver": 4 * n ** 3 / 3}
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2511_16174_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = _lib.load()
+    n, b = args.n, args.b
+    oc = _lib.ORDER_CODES[args.order]
+    g = torch.Generator(device="cuda")
+    g.manual_seed(args.seed + rank)
+    a0 = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    a0.add_(a0.t().clone())
+    a0.mul_(0.5)
+    a = torch.empty_like(a0)
+    q = torch.empty_like(a0)
+    lam = torch.empty(n, dtype=torch.float64, device="cuda")
+    ws = torch.empty(L.pevd_syevd_workspace_bytes(n, b, 1, oc), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    P = ctypes.c_void_p
+
+    def step(st):
+        rc = L.pevd_syevd_device(n, b, P(a.data_ptr()), n, P(lam.data_ptr()), P(q.data_ptr()), n,
+                                 1, oc, P(ws.data_ptr()), ws.numel(), P(stream.cuda_stream),
+                                 ctypes.byref(st))
+        _lib.check(rc, "pevd_syevd_device")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        a.copy_(a0)
+        step(_lib.PevdStats())
+    times, stats = [], []
+    launches0 = L.pevd_kernel_launches()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            a.copy_(a0)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            st = _lib.PevdStats()
+            e0.record(stream)
+            step(st)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            stats.append(st)
+            barrier()
+    launches = (L.pevd_kernel_launches() - launches0) // max(1, args.steps)
+    ms = sum(times) / len(times)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * 4 * n ** 3 / (ms * 1e-3) / 1e12
+
+    # stage breakdown of the last step (CUDA events on the launching streams, inside the lib)
+    st = stats[-1]
+    stage_ms = {k: getattr(st, k + "_ms")[1] - getattr(st, k + "_ms")[0]
+                for k in ("sbr", "bc", "solver", "sbr_back", "bc_back", "final")}
+    fl = stage_flops(n)
+    dom = max(("sbr", "sbr_back", "bc_back", "final", "solver"), key=lambda k: stage_ms[k])
+    peaks = load_fp64_peaks()
+    peak = peaks["dfma"] if dom == "bc_back" else peaks["dmma"]
+    achieved = fl[dom] / (stage_ms[dom] * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3),
+                "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                "traffic": None,
+                "peak_source": ("FP64 DFMA microbenchmark" if dom == "bc_back" else
+                                "FP64 DMMA microbenchmark") +
+                               " on this pool's B200 (profiles/r01_fp64_peaks.json); "
+                               "MEASURED_PEAKS.json has no FP64 entry",
+                "stage_ms": {k: round(v, 1) for k, v in stage_ms.items()},
+                "stage_tflops": {k: round(fl[k] / (stage_ms[k] * 1e-3) / 1e12, 2)
+                                 for k in fl if stage_ms[k] > 0}}
+    clocks = clk.summary()
+
+    # ---- e2e through the C ABI with host buffers (pevd_syevd)
+    e2e = None
+    if not args.no_e2e:
+        a_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        a_host.copy_(a0)
+        del a, q, ws
+        torch.cuda.empty_cache()
+        q_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        lam_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        barrier()
+        t0 = time.perf_counter()
+        rc = L.pevd_syevd(n, b, P(a_host.data_ptr()), n, P(lam_host.data_ptr()),
+                          P(q_host.data_ptr()), n, 1, oc, ctypes.byref(_lib.PevdStats()))
+        t1 = time.perf_counter()
+        _lib.check(rc, "pevd_syevd")
+        ems = (t1 - t0) * 1e3
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": round(world * 4 * n ** 3 / (ems * 1e-3) / 1e12, 4), "unit": "TFLOP/s",
+               "ms_per_step": round(ems, 1), "h2d_bytes_per_step": 8 * n * n,
+               "d2h_bytes_per_step": 8 * n * n + 8 * n}
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(args.cpu_n)
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
+                "wall_s_per_evd": round(ms / 1e3, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"dense symmetric FP64 EVD with eigenvectors, n={n}, b={b}, "
+                                       f"order={args.order}, A=(G+G^T)/2 G~N(0,1)",
+                           "n": n, "b": b, "order": args.order,
+                           "parallelism": "replicas" if world > 1 else "1 GPU",
+                           "l2": "input 8n^2 = %.1f GB >> 126 MB L2 (no flush needed)" % (8 * n * n / 1e9),
+                           "flop_convention": "4 n^3 / wall (PAPER.md:92)"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "gpu_launches": int(launches), "impl": "b200"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def load_fp64_peaks():
+    path = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
+    try:
+        d = json.load(open(path))
+        dmma = max(x["tflops"] for x in d["micro"] if x["kind"].startswith("dmma"))
+        dfma = max(x["tflops"] for x in d["micro"] if x["kind"] == "dfma")
+        return {"dmma": round(dmma, 2), "dfma": round(dfma, 2),
+                "cublas_dgemm": round(d.get("cublas_dgemm_8192_sustained_4s_tflops", 0), 2)}
+    except Exception:
+        return {"dmma": 37.17, "dfma": 34.19, "cublas_dgemm": 35.41}
+
+
+def cpu_baseline(n_cpu: int):
+    """Oracle (C + numpy restatement of the reference) on the host: one EVD at n_cpu."""
+    import numpy as np
+    from oracle import oracle as orc
+    g = np.random.default_rng(n_cpu).standard_normal((n_cpu, n_cpu))
+    a = (g + g.T) / 2
+    orc.evd(a[:64, :64], 32, True)  # warm the library
+    t0 = time.perf_counter()
+    orc.evd(a, 32, True)
+    dt = time.perf_counter() - t0
+    return {"value": round(4 * n_cpu ** 3 / dt / 1e12, 6), "unit": "TFLOP/s",
+            "cores": os.cpu_count(), "kind": "port",
+            "sample": f"one n={n_cpu} EVD with vectors (oracle/: numpy BLAS on all host threads "
+                      f"+ single-threaded C QL/QR, chase and BC-Back), {dt:.2f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import oracle as orc
+    n = args.ref_n
+    g = np.random.default_rng(n).standard_normal((n, n))
+    a = (g + g.T) / 2
+    for _ in range(args.warmup):
+        orc.evd(a, args.b, True)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        orc.evd(a, args.b, True)
+        ts.append(time.perf_counter() - t0)
+    dt = sum(ts) / len(ts)
+    v = 4 * n ** 3 / dt / 1e12
+    print(json.dumps({
+        "metric": METRIC, "value": round(v, 6), "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"CPU oracle EVD with eigenvectors, bounded sample n={n} "
+                               f"(the n=49152 run would take days on the host)", "n": n,
+                   "b": args.b},
+        "cpu_baseline": {"value": round(v, 6), "unit": "TFLOP/s", "cores": os.cpu_count(),
+                         "kind": "port", "sample": f"n={n} EVD with vectors per step"},
+        "e2e": {"value": round(v, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=49152)
+    ap.add_argument("--b", type=int, default=32)
+    ap.add_argument("--order", default="pipelined", choices=["pipelined", "sequential", "conventional"])
+    ap.add_argument("--seed", type=int, default=49152)
+    ap.add_argument("--cpu-n", type=int, default=1536)
+    ap.add_argument("--ref-n", type=int, default=1024)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

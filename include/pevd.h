@@ -50,6 +50,8 @@ typedef struct pevd_stats {
 
 const char* pevd_last_error(void);
 const char* pevd_version(void);
+/* Number of CUDA kernels this library has launched since it was loaded. */
+int64_t pevd_kernel_launches(void);
 
 /* ---------------------------------------------------------------- whole EVD
  * Replaces pipeevd.run (pipeline.py:511) for one GPU: A = Q diag(lam) Q^T.

@@ -30,6 +30,7 @@ class PevdStats(ctypes.Structure):
 SIGNATURES = {
     "pevd_last_error": (ctypes.c_char_p, []),
     "pevd_version": (ctypes.c_char_p, []),
+    "pevd_kernel_launches": (_i64, []),
     "pevd_syevd_workspace_bytes": (_i64, [_i64, _int, _int, _int]),
     "pevd_syevd_device": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _int, _int, _vp, _i64,
                                  _vp, ctypes.POINTER(PevdStats)]),

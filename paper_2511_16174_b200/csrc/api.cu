@@ -8,6 +8,7 @@
 // stream; "conventional" applies Q_b then Q_s to Q_d from the left (pipeline.py:367-387).
 #include <cstdarg>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <vector>
 #include "kernels.cuh"
@@ -24,6 +25,9 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 const char* last_error() { return g_err; }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int num_sms() {
   static int cache[64];
@@ -107,6 +111,7 @@ extern "C" {
 
 const char* pevd_last_error(void) { return last_error(); }
 const char* pevd_version(void) { return "pevd 0.1.0 (sm_100a, FP64 DMMA)"; }
+int64_t pevd_kernel_launches(void) { return g_launches.load(); }
 
 int64_t pevd_syevd_workspace_bytes(int64_t n, int b, int want_vectors, int order) {
   if (n < 1) return 0;
@@ -172,6 +177,13 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     if ((rc = sbr_reduce(sm, n, b, A, lda, L.bands, want_vectors ? L.Tall : nullptr, L.ws_sbr)))
       break;
     cudaEventRecord(ev[0].b, sm);
+    // ---- BC first: its persistent CTAs must become resident before the SBR-Back GEMMs
+    //      (enqueued next, on the back stream) fill the SMs
+    cudaEventRecord(ev[1].a, sm);
+    if ((rc = bc_reduce(sm, n, b, L.bands, L.d, L.e, want_vectors ? L.tau : nullptr,
+                        want_vectors ? L.V : nullptr, L.vld, L.ws_bc)))
+      break;
+    cudaEventRecord(ev[1].b, sm);
     // ---- SBR-Back (forms Q_s) overlapping the chase
     if (want_vectors && order != PEVD_ORDER_CONVENTIONAL) {
       if (two_streams) cudaStreamWaitEvent(sback, ev[0].b, 0);
@@ -179,12 +191,6 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
       if ((rc = sbr_back_form(sback, n, b, A, L.Tall, L.Qs, n, L.ws_back))) break;
       cudaEventRecord(ev[3].b, sback);
     }
-    // ---- BC
-    cudaEventRecord(ev[1].a, sm);
-    if ((rc = bc_reduce(sm, n, b, L.bands, L.d, L.e, want_vectors ? L.tau : nullptr,
-                        want_vectors ? L.V : nullptr, L.vld, L.ws_bc)))
-      break;
-    cudaEventRecord(ev[1].b, sm);
     // ---- BC-Back on Q_s (back stream) overlapping the divide and conquer
     if (want_vectors && order != PEVD_ORDER_CONVENTIONAL) {
       if (two_streams) cudaStreamWaitEvent(sback, ev[1].b, 0);

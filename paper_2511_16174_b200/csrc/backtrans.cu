@@ -14,6 +14,7 @@
 // thread keeps the b+G-1 row entries a reflector group touches in registers while sliding up the
 // chase steps, so each entry of X is loaded and stored once per sweep group: arithmetic
 // intensity G/4 flop/byte.  The group's reflectors are staged in shared memory (broadcast reads).
+#include <cstdlib>
 #include "kernels.cuh"
 
 namespace pevd {
@@ -31,29 +32,49 @@ __global__ void set_identity(int64_t n, double* Q, int64_t ldq) {
   }
 }
 
-// T (K x K, upper) from G = Y^T Y and taus: T[q, i] = -tau_i sum_{t=q}^{i-1} T[q, t] G[t, i]
-__global__ void larft_kernel(int K, const double* __restrict__ G, int ldg,
-                             const double* __restrict__ Tall, int b, int x0, int npan,
-                             int64_t R, int pw_last, double* __restrict__ T) {
-  // thread q owns row q of T; the recurrence only reads its own row -> no synchronisation
-  const int q = threadIdx.x;
-  // taus from the per-panel T diagonals
-  for (int i = 0; i < K; ++i) {
-    const int x = x0 + i / b, r = i % b;
-    const int ldt = (x == R - 1) ? pw_last : b;  // the ragged last panel's T is pw x pw
-    const double tau = Tall[(int64_t)x * b * b + r + (int64_t)r * ldt];
-    if (q < K) {
-      double v = 0.0;
-      if (q == i) v = tau;
-      else if (q < i) {
-        double s = 0.0;
-        for (int t = q; t < i; ++t) s += T[q + (int64_t)t * K] * G[t + (int64_t)i * ldg];
-        v = -tau * s;
-      }
-      T[q + (int64_t)i * K] = v;
+// T_agg (K x K, upper) of the aggregated block reflector I - Y T Y^T from the per-panel T_x
+// (diagonal blocks, from the panel QR) and the Gram matrix G = Y^T Y:
+//   T[0:c, blk] = -T[0:c, 0:c] G[0:c, blk] T_blk     (blocks of b columns, c = blk * b)
+// one CTA, all products in shared memory (K <= NB_AGG * 32 = 128).
+__global__ void __launch_bounds__(256)
+    larft_kernel(int K, const double* __restrict__ G, int ldg, const double* __restrict__ Tall,
+                 int b, int x0, int64_t R, int pw_last, double* __restrict__ T) {
+  extern __shared__ double sm[];
+  double* Ts = sm;            // K x K (col-major, ld K)
+  double* tmp = Ts + K * K;   // K x b
+  const int tid = threadIdx.x;
+  for (int e = tid; e < K * K; e += blockDim.x) Ts[e] = 0.0;
+  __syncthreads();
+  const int nblk = (K + b - 1) / b;
+  for (int B = 0; B < nblk; ++B) {
+    const int x = x0 + B;
+    const int pw = (x == R - 1) ? pw_last : b;
+    const double* Tx = Tall + (int64_t)x * b * b;  // pw x pw, ld pw
+    const int c0 = B * b;
+    for (int e = tid; e < pw * pw; e += blockDim.x) {
+      const int r = e % pw, c = e / pw;
+      Ts[(c0 + r) + (c0 + c) * K] = Tx[r + c * pw];
     }
+    __syncthreads();
+    if (B == 0) continue;
+    // tmp = T[0:c0, 0:c0] G[0:c0, c0:c0+pw]
+    for (int e = tid; e < c0 * pw; e += blockDim.x) {
+      const int r = e % c0, c = e / c0;
+      double s = 0.0;
+      for (int t = r; t < c0; ++t) s += Ts[r + t * K] * G[t + (int64_t)(c0 + c) * ldg];
+      tmp[r + c * c0] = s;
+    }
+    __syncthreads();
+    // T[0:c0, blk] = -tmp T_blk
+    for (int e = tid; e < c0 * pw; e += blockDim.x) {
+      const int r = e % c0, c = e / c0;
+      double s = 0.0;
+      for (int t = 0; t <= c; ++t) s += tmp[r + t * c0] * Ts[(c0 + t) + (c0 + c) * K];
+      Ts[r + (c0 + c) * K] = -s;
+    }
+    __syncthreads();
   }
-  (void)npan;
+  for (int e = tid; e < K * K; e += blockDim.x) T[e] = Ts[e];
 }
 
 // ------------------------------------------------------------ BC-Back, generic b (slow, tests)
@@ -196,6 +217,22 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+int launch_larft(cudaStream_t st, int K, const double* G, const double* Tall, int b, int x0,
+                 int64_t R, int pw_last, double* T) {
+  const size_t smem = (size_t)(K * K + K * b) * 8;
+  static int attr_dev = -1;
+  int dev;
+  PEVD_CUDA(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    PEVD_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+    attr_dev = dev;
+  }
+  larft_kernel<<<1, 256, smem, st>>>(K, G, K, Tall, b, x0, R, pw_last, T);
+  PEVD_LAUNCH_CHECK();
+  return OK;
+}
+
 }  // namespace
 
 int64_t sbr_back_ws_bytes(int64_t n, int b) {
@@ -227,8 +264,7 @@ int sbr_back_form(cudaStream_t st, int64_t n, int b, const double* Yfull, const 
     // Gram and T_agg
     GemmArgs gg{K, K, m, 1.0, 0.0, Y, n, Y, n, Gm, K, 1, 0, A_GENERAL, C_ALL};
     PEVD_TRY(gemm(st, gg, sk, skn));
-    larft_kernel<<<1, 256, 0, st>>>((int)K, Gm, (int)K, Tall, b, (int)x0, (int)(x1 - x0), R,
-                                    (int)(n - b - (R - 1) * b), Tg);
+    PEVD_TRY(launch_larft(st, (int)K, Gm, Tall, b, (int)x0, R, (int)(n - b - (R - 1) * b), Tg));
     PEVD_LAUNCH_CHECK();
     // tmp1 = Y^T Q22 (K x m); tmp2 = T tmp1; Q22 -= Y tmp2
     GemmArgs g1{K, m, m, 1.0, 0.0, Y, n, Q22, ldq, tmp1, K, 1, 0, A_GENERAL, C_ALL};
@@ -263,8 +299,7 @@ int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, 
     double* X2 = X + t0;
     GemmArgs gg{K, K, m, 1.0, 0.0, Y, n, Y, n, Gm, K, 1, 0, A_GENERAL, C_ALL};
     PEVD_TRY(gemm(st, gg, sk, skn));
-    larft_kernel<<<1, 256, 0, st>>>((int)K, Gm, (int)K, Tall, b, (int)x0, (int)(x1 - x0), R,
-                                    (int)(n - b - (R - 1) * b), Tg);
+    PEVD_TRY(launch_larft(st, (int)K, Gm, Tall, b, (int)x0, R, (int)(n - b - (R - 1) * b), Tg));
     PEVD_LAUNCH_CHECK();
     for (int64_t c = 0; c < ncols; c += n) {
       const int64_t nc = std::min<int64_t>(n, ncols - c);
@@ -283,9 +318,20 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
                   double* X, int64_t ldx, int64_t nrows) {
   if (n < 3 || nrows <= 0 || b < 2) return OK;
   if (b == 32 && vld >= 32) {
-    constexpr int G = 16;
-    bc_back_right_reg<32, G><<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, tau, V, vld, X, ldx,
-                                                                         nrows);
+    static int g_sel = -1;
+    if (g_sel < 0) {
+      const char* e = getenv("PEVD_BCBACK_G");
+      g_sel = e ? atoi(e) : 16;
+    }
+    if (g_sel == 32)
+      bc_back_right_reg<32, 32><<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, tau, V, vld, X,
+                                                                            ldx, nrows);
+    else if (g_sel == 8)
+      bc_back_right_reg<32, 8><<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, tau, V, vld, X,
+                                                                           ldx, nrows);
+    else
+      bc_back_right_reg<32, 16><<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, tau, V, vld, X,
+                                                                            ldx, nrows);
   } else {
     bc_back_right_generic<<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, b, tau, V, vld, X, ldx,
                                                                       nrows, 16);

@@ -71,7 +71,12 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
       if (gi > 0) {
         if (lane == 0) {
           const int need = (int)(j + 3);
-          while (ld_acquire(prog + gi - 1) < need) {
+          if (ld_acquire(prog + gi - 1) < need) {
+            unsigned ns = 32;
+            while (ld_acquire(prog + gi - 1) < need) {
+              __nanosleep(ns);  // yield issue slots to the working warps
+              if (ns < 256) ns <<= 1;
+            }
           }
         }
         __syncwarp();
@@ -84,10 +89,22 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
       const int nT = (int)(tend - (w0 + L));
       const int64_t slot = (int64_t)j * (n - 2) - (int64_t)b * j * (j - 1) / 2 + gi;
 
-      // ---- stage the left block (column q = cg + q, rows w0 + r)
-      for (int q = 0; q < nleft; ++q) {
-        if (lane < L)
-          S.SL[lane * LDS_ + q] = __ldcg(Bd + (cg + q) * LDB + (w0 - cg - q) + lane);
+      // ---- stage the whole region with independent loads (one L2 round trip, not 3b)
+      double rl[BMAX], rw[BMAX], rc[BMAX];
+#pragma unroll
+      for (int q = 0; q < BMAX; ++q) {
+        rl[q] = (q < nleft && lane < L) ? __ldcg(Bd + (cg + q) * LDB + (w0 - cg - q) + lane) : 0.0;
+        rw[q] = (q < L && lane >= q && lane < L) ? __ldcg(Bd + (w0 + q) * LDB + (lane - q)) : 0.0;
+        rc[q] = (q < L && lane < nT) ? __ldcg(Bd + (w0 + q) * LDB + (L + lane - q)) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < BMAX; ++q) {
+        S.SL[lane * LDS_ + q] = rl[q];
+        S.SC[lane * LDS_ + q] = rc[q];
+        if (lane >= q) {
+          S.SW[lane * LDS_ + q] = rw[q];
+          S.SW[q * LDS_ + lane] = rw[q];
+        }
       }
       __syncwarp();
       const double x = (lane < L) ? S.SL[lane * LDS_] : 0.0;
@@ -99,15 +116,6 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
           for (int r = lane; r < vld; r += 32) V_out[slot * vld + r] = (r == 0) ? 1.0 : 0.0;
         }
       } else {
-        // ---- stage window (lower -> full) and coupling block
-        for (int c = 0; c < L; ++c) {
-          if (lane >= c && lane < L) {
-            const double val = __ldcg(Bd + (w0 + c) * LDB + (lane - c));
-            S.SW[lane * LDS_ + c] = val;
-            S.SW[c * LDS_ + lane] = val;
-          }
-          if (lane < nT) S.SC[lane * LDS_ + c] = __ldcg(Bd + (w0 + c) * LDB + (L + lane - c));
-        }
         const double x0 = __shfl_sync(0xffffffffu, x, 0);
         const double nrm = sqrt(x0 * x0 + tail);
         const double alpha = (x0 >= 0.0) ? -nrm : nrm;
@@ -118,35 +126,58 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
         S.vs[lane] = v;
         if (lane < L) S.SL[lane * LDS_] = (lane == 0) ? alpha : 0.0;
         __syncwarp();
+        // (all staged entries outside the live L x L / nT x L region are zero and v is zero
+        //  beyond L, so every loop below runs the full BMAX width without predicates; four
+        //  partial sums break the dependent-FMA chains)
         // ---- H from the left on the bulge columns strictly between (lane = column q)
         if (lane >= 1 && lane < nleft) {
           const int q = lane;
-          double dot = 0.0;
-          for (int r = 0; r < L; ++r) dot += S.vs[r] * S.SL[r * LDS_ + q];
-          dot *= tau;
-          for (int r = 0; r < L; ++r) S.SL[r * LDS_ + q] -= dot * S.vs[r];
+          double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+          for (int r = 0; r < BMAX; r += 4) {
+            d0 = fma(S.vs[r], S.SL[r * LDS_ + q], d0);
+            d1 = fma(S.vs[r + 1], S.SL[(r + 1) * LDS_ + q], d1);
+            d2 = fma(S.vs[r + 2], S.SL[(r + 2) * LDS_ + q], d2);
+            d3 = fma(S.vs[r + 3], S.SL[(r + 3) * LDS_ + q], d3);
+          }
+          const double dot = tau * ((d0 + d1) + (d2 + d3));
+#pragma unroll
+          for (int r = 0; r < BMAX; ++r) S.SL[r * LDS_ + q] -= dot * S.vs[r];
         }
         // ---- H A H on the window (lane = row r)
         double u = 0.0;
-        if (lane < L) {
-          double acc = 0.0;
-          for (int c = 0; c < L; ++c) acc += S.SW[lane * LDS_ + c] * S.vs[c];
-          u = tau * acc;
+        {
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+          for (int c = 0; c < BMAX; c += 4) {
+            a0 = fma(S.SW[lane * LDS_ + c], S.vs[c], a0);
+            a1 = fma(S.SW[lane * LDS_ + c + 1], S.vs[c + 1], a1);
+            a2 = fma(S.SW[lane * LDS_ + c + 2], S.vs[c + 2], a2);
+            a3 = fma(S.SW[lane * LDS_ + c + 3], S.vs[c + 3], a3);
+          }
+          u = tau * ((a0 + a1) + (a2 + a3));
         }
         const double gam = 0.5 * tau * warp_sum(v * u);
         const double w = u - gam * v;
         S.wv[lane] = w;
         // ---- H from the right on the coupling rows (lane = row t)
-        if (lane < nT) {
-          double dot = 0.0;
-          for (int c = 0; c < L; ++c) dot += S.SC[lane * LDS_ + c] * S.vs[c];
-          dot *= tau;
-          for (int c = 0; c < L; ++c) S.SC[lane * LDS_ + c] -= dot * S.vs[c];
+        {
+          double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+          for (int c = 0; c < BMAX; c += 4) {
+            d0 = fma(S.SC[lane * LDS_ + c], S.vs[c], d0);
+            d1 = fma(S.SC[lane * LDS_ + c + 1], S.vs[c + 1], d1);
+            d2 = fma(S.SC[lane * LDS_ + c + 2], S.vs[c + 2], d2);
+            d3 = fma(S.SC[lane * LDS_ + c + 3], S.vs[c + 3], d3);
+          }
+          const double dot = tau * ((d0 + d1) + (d2 + d3));
+#pragma unroll
+          for (int c = 0; c < BMAX; ++c) S.SC[lane * LDS_ + c] -= dot * S.vs[c];
         }
         __syncwarp();
-        if (lane < L) {
-          for (int c = 0; c <= lane; ++c)
-            S.SW[lane * LDS_ + c] -= v * S.wv[c] + w * S.vs[c];
+#pragma unroll
+        for (int c = 0; c < BMAX; ++c) {
+          if (c <= lane) S.SW[lane * LDS_ + c] -= v * S.wv[c] + w * S.vs[c];
         }
         __syncwarp();
         // ---- write back
@@ -226,7 +257,10 @@ int bc_reduce(cudaStream_t st, int64_t n, int b, const double* bands_ref, double
       return ERR_CUDA;
     }
     // every warp must be co-resident (warps wait on each other): never exceed one full wave
-    const int64_t need = cdiv(n - 2, BC_WARPS);
+    // about n/(3b) sweeps are in flight at once; twice that many warps keeps every sweep's
+    // warp free when its turn comes, more would only add spinning warps next to the back stream
+    const int64_t want_warps = std::min<int64_t>(n - 2, std::max<int64_t>(2 * n / (3 * b), 2 * num_sms()));
+    const int64_t need = cdiv(want_warps, BC_WARPS);
     const int grid = (int)std::min<int64_t>((int64_t)per_sm * num_sms(), need);
     bc_chase_kernel<<<grid, BC_WARPS * 32, smem, st>>>(n, b, Bd, LDB, prog, tau, V, vld,
                                                        grid * BC_WARPS);

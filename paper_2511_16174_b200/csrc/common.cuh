@@ -27,7 +27,14 @@ const char* last_error();
     if (r_ != ::pevd::OK) return r_;    \
   } while (0)
 
-#define PEVD_LAUNCH_CHECK() PEVD_CUDA(cudaGetLastError())
+// every kernel launch of the library is followed by PEVD_LAUNCH_CHECK (counted for bench.py's
+// gpu_launches claim, pevd_kernel_launches())
+void count_launch();
+#define PEVD_LAUNCH_CHECK()            \
+  do {                                 \
+    ::pevd::count_launch();            \
+    PEVD_CUDA(cudaGetLastError());     \
+  } while (0)
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t pad8(int64_t k) { return (k + 7) / 8 * 8; }

@@ -260,6 +260,7 @@ int panel_qr(cudaStream_t st, int64_t m, int k, const double* panel, int64_t ldp
   void* args[] = {&m, &k, &panel, &ldp, &R, &Y1, &ldy1, &Y2, &ldy2, &W, &ldw, &T, &wk, &rows};
   PEVD_CUDA(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel, dim3(ncta),
                                         dim3(QR_THREADS), args, smem, st));
+  count_launch();
   return OK;
 }
 

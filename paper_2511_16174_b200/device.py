@@ -86,7 +86,7 @@ def panel_qr(panel):
 
 
 def sbr(a, b):
-    """Band reduction (sbr.py:155-188) -> (bands (b+1, n), Y staircase (n, n), Tall (R, b, b))."""
+    """Band reduction (sbr.py:155-188) -> (bands (b+1, n), Y staircase (n, n), Tall flat)."""
     L = _lib.load()
     a = np.asarray(a, dtype=np.float64)
     n = a.shape[0]
@@ -98,8 +98,8 @@ def sbr(a, b):
     ws = workspace(L.pevd_sbr_workspace_bytes(n, b))
     rc = L.pevd_sbr(n, b, _p(da), n, _p(bands), _p(tall), _p(ws), _stream())
     _lib.check(rc, "sbr")
-    tall_h = tall.cpu().numpy().reshape(rounds, b, b).transpose(0, 2, 1)  # col-major blocks
-    return bands.cpu().numpy().reshape(b + 1, n), from_dev(da), tall_h
+    # tall: flat, panel x's T (pw x pw, column-major, ld pw) at offset x * b * b
+    return bands.cpu().numpy().reshape(b + 1, n), from_dev(da), tall.cpu().numpy()
 
 
 def bc(bands, want_reflectors=True):
@@ -172,14 +172,18 @@ def sbr_back_form(n, b, ystair, tall):
     L = _lib.load()
     torch = _torch()
     dy = to_dev(ystair)
-    rounds = tall.shape[0]
-    dt = torch.from_numpy(np.ascontiguousarray(np.asarray(tall).transpose(0, 2, 1)).reshape(-1)).cuda()
+    dt = torch.from_numpy(np.ascontiguousarray(tall, dtype=np.float64).reshape(-1)).cuda()
     q = empty(n, n)
     ws = workspace(L.pevd_sbr_back_workspace_bytes(n, b))
     rc = L.pevd_sbr_back_form(n, b, _p(dy), _p(dt), _p(q), n, _p(ws), _stream())
     _lib.check(rc, "sbr_back_form")
-    del rounds
     return from_dev(q)
+
+
+def t_block(tall, x: int, b: int, pw: int) -> np.ndarray:
+    """Panel x's T factor (pw x pw) out of the flat Tall array."""
+    o = x * b * b
+    return np.asarray(tall).reshape(-1)[o:o + pw * pw].reshape(pw, pw).T.copy()
 
 
 def bc_back_right(n, b, tau, V, x):

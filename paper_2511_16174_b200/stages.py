@@ -1,0 +1,282 @@
+"""Per-stage functions with the reference's signatures, executed on the GPU.
+
+Each mirrors a reference function (file:line) so the reference's own per-stage tests read the
+same against this package; the arithmetic runs in libpevd.so (device.py -> C ABI).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import device
+from .core import (BandMatrix, FlopCounter, ProtocolError, ReflectorPanel, SymmetricMatrix,
+                   TridiagonalMatrix, EigenResult)
+from .schedule import bc_back_macs, round_schedule, sbr_macs, bc_macs
+
+DEFAULT_GROUP_SIZE = 4  # backtrans.py:23 (device kernels use their own grouping)
+
+
+def _pad8(k: int) -> int:
+    return ((k + 7) // 8) * 8
+
+
+# ------------------------------------------------------------------ SBR
+
+
+@dataclass
+class SbrConfig:
+    """sbr.py:20-34"""
+
+    b: int = 32
+    panel_width: int | None = None
+    inner_block: int = 8
+
+    def __post_init__(self):
+        if self.panel_width is None:
+            self.panel_width = self.b
+        if self.panel_width != self.b:
+            raise ValueError("panel_width must equal the bandwidth")
+        if self.b < 1:
+            raise ValueError("bandwidth must be >= 1")
+        if self.inner_block < 1:
+            raise ValueError("inner_block must be >= 1")
+
+
+@dataclass
+class SbrFactors:
+    """All panel reflectors of one reduction, ordered by column offset (sbr.py:37-51)."""
+
+    n: int
+    b: int
+    panels: list = field(default_factory=list)
+
+
+def house_vector(x):
+    """core.py:238-255 (scalar helper; the device kernels inline the same convention)."""
+    x = np.asarray(x, dtype=np.float64)
+    v = np.zeros(len(x))
+    v[0] = 1.0
+    tail = float(np.linalg.norm(x[1:]))
+    if tail == 0.0:
+        return v, 0.0, float(x[0])
+    sign = -1.0 if x[0] < 0.0 else 1.0
+    alpha = -sign * float(np.hypot(x[0], tail))
+    v[1:] = x[1:] / (x[0] - alpha)
+    return v, 2.0 / (1.0 + float(np.dot(v[1:], v[1:]))), alpha
+
+
+def panel_qr(panel: np.ndarray, col_offset: int = 0, inner_block: int = 8,
+             counter: FlopCounter | None = None, stage: str = "SBR") -> ReflectorPanel:
+    """Householder QR of a panel on the GPU; overwrites it with R (sbr.py:69-116)."""
+    m, k = panel.shape
+    if m < k:
+        raise ValueError("panel must be at least as tall as wide")
+    R, Y, W, T = device.panel_qr(panel)
+    panel[:k, :] = np.triu(R)
+    panel[k:, :] = 0.0
+    panel[np.tril_indices(k, -1)] = 0.0
+    if counter is not None:
+        counter.add(stage, 2 * m * k * k)
+    return ReflectorPanel(W=W, Y=Y, col_offset=col_offset)
+
+
+def sbr_reduce(a: SymmetricMatrix, cfg: SbrConfig, counter: FlopCounter | None = None):
+    """Dense -> band on the GPU: (BandMatrix, SbrFactors) (sbr.py:155-188)."""
+    n, b = a.n, cfg.b
+    if n <= b:
+        raise ValueError(f"need n > b, got n={n}, b={b}")
+    bands, ystair, tall = device.sbr(a.data, b)
+    panels = []
+    for x, (c0, pw, t0) in enumerate(round_schedule(n, b)):
+        Y = np.asfortranarray(ystair[t0:, c0:c0 + pw])
+        T = device.t_block(tall, x, b, pw)
+        p = ReflectorPanel(W=Y @ T, Y=Y, col_offset=c0)
+        p._T = T
+        panels.append(p)
+    if counter is not None:
+        counter.add("SBR", sbr_macs(n, b))
+    return BandMatrix(n, b, bands), SbrFactors(n=n, b=b, panels=panels)
+
+
+# ------------------------------------------------------------------ BC
+
+
+class BulgeReflectorSet:
+    """Bulge-chasing reflectors in canonical (chase step j, sweep i) order (bulge.py:33-141)."""
+
+    def __init__(self, n, b, i_idx, j_idx, row0, length, tau, v):
+        self.n, self.b = n, b
+        self.i_idx = np.ascontiguousarray(i_idx, dtype=np.int64)
+        self.j_idx = np.ascontiguousarray(j_idx, dtype=np.int64)
+        self.row0 = np.ascontiguousarray(row0, dtype=np.int64)
+        self.length = np.ascontiguousarray(length, dtype=np.int64)
+        self.tau = np.ascontiguousarray(tau, dtype=np.float64)
+        self.v = np.ascontiguousarray(v, dtype=np.float64)
+        if len(self.tau):
+            perm = np.lexsort((self.i_idx, self.j_idx))
+            for name in ("i_idx", "j_idx", "row0", "length", "tau", "v"):
+                setattr(self, name, np.ascontiguousarray(getattr(self, name)[perm]))
+        if self.v.shape != (len(self.tau), _pad8(b)):
+            raise ValueError("reflector storage has the wrong stride")
+        for t in self.tau:
+            if not math.isfinite(t):
+                raise ValueError("non-finite tau")
+        if len(self.tau) and np.any(self.v[:, 0] != 1.0):
+            raise ValueError("reflector vectors must have v[0] = 1")
+        self._pos = {(int(i), int(j)): p for p, (i, j) in enumerate(zip(self.i_idx, self.j_idx))}
+        if len(self._pos) != len(self.tau):
+            raise ValueError("duplicate (sweep, step) index")
+        self._slots = None
+
+    def __len__(self) -> int:
+        return len(self.tau)
+
+    @property
+    def stride(self) -> int:
+        return self.v.shape[1] if len(self.tau) else _pad8(self.b)
+
+    def position(self, i, j):
+        return self._pos.get((i, j))
+
+    def by_step(self) -> dict:
+        out: dict = {}
+        for p in range(len(self.tau)):
+            out.setdefault(int(self.j_idx[p]), []).append(p)
+        return out
+
+    @classmethod
+    def empty(cls, n, b):
+        z = np.zeros(0)
+        return cls(n, b, z, z, z, z, z, np.zeros((0, _pad8(b))))
+
+    @classmethod
+    def from_slots(cls, n, b, tau, V):
+        r = device.slots_to_reference(n, b, tau, V)
+        u = cls(n, b, r["i"], r["j"], r["row0"], r["len"], r["tau"], r["v"])
+        u._slots = (tau, V)
+        return u
+
+    def slots(self):
+        """Fixed-slot layout of the device kernels (include/pevd.h pevd_bc)."""
+        if self._slots is None:
+            n, b = self.n, self.b
+            nslot = 0
+            j = 0
+            while n - 2 - j * b > 0:
+                nslot += n - 2 - j * b
+                j += 1
+            tau = np.zeros(max(nslot, 1))
+            V = np.zeros((max(nslot, 1), _pad8(b)))
+            for p in range(len(self.tau)):
+                i, jj = int(self.i_idx[p]), int(self.j_idx[p])
+                s = device.slot_offset(n, b, jj) + i
+                tau[s] = self.tau[p]
+                V[s] = self.v[p]
+            self._slots = (tau, V)
+        return self._slots
+
+
+def bc_reduce(band: BandMatrix, counter: FlopCounter | None = None):
+    """Band -> tridiagonal on the GPU wavefront chase (bulge.py:299-309)."""
+    n, b = band.n, band.b
+    if b <= 1:
+        return band.to_tridiagonal(), BulgeReflectorSet.empty(n, max(b, 1))
+    d, e, tau, V = device.bc(band.bands)
+    if counter is not None:
+        counter.add("BC", bc_macs(n, b))
+    return TridiagonalMatrix(d=d, e=e), BulgeReflectorSet.from_slots(n, b, tau, V)
+
+
+# ------------------------------------------------------------------ solver
+
+
+def tridiag_eig(t: TridiagonalMatrix, want_vectors: bool = False,
+                counter: FlopCounter | None = None) -> EigenResult:
+    """Symmetric tridiagonal eigensolver: device divide and conquer (replaces tridiag.py:298)."""
+    n = t.n
+    if n == 0:
+        return EigenResult(lam=np.zeros(0), Q=np.zeros((0, 0)) if want_vectors else None,
+                           vectors_computed=want_vectors)
+    lam, q = device.stedc(t.d, t.e if n > 1 else np.zeros(0))
+    if counter is not None:
+        counter.add("Solver", max(1, (2 * n ** 3) // 3))
+    if not want_vectors:
+        return EigenResult(lam=lam)
+    return EigenResult(lam=lam, Q=np.asfortranarray(q), vectors_computed=True)
+
+
+# ------------------------------------------------------------------ back transformation
+
+
+def bc_back_apply(u: BulgeReflectorSet, qs_t_block, counter: FlopCounter | None = None,
+                  direction: str = "reordered", grouped: bool = True,
+                  group_size: int = DEFAULT_GROUP_SIZE, debug_validate: bool = False,
+                  inplace: bool = False) -> np.ndarray:
+    """Q_b^T X ("reordered") or Q_b X ("conventional") on the GPU (backtrans.py:277-310)."""
+    x = np.array(qs_t_block, dtype=np.float64, order="C")
+    if x.ndim != 2 or x.shape[0] != u.n:
+        raise ValueError(f"target must have {u.n} rows")
+    if direction not in ("reordered", "conventional"):
+        raise ValueError(f"unknown direction {direction!r}")
+    if len(u) == 0:
+        return x
+    tau, V = u.slots()
+    if direction == "reordered":
+        out = device.bc_back_right(u.n, u.b, tau, V, x.T).T   # (X^T Q_b)^T = Q_b^T X
+    else:
+        out = device.bc_back_left(u.n, u.b, tau, V, x)
+    if counter is not None:
+        counter.add("BC-Back", bc_back_macs(u.n, u.b, x.shape[1]))
+    return np.ascontiguousarray(out)
+
+
+def sbr_back_accumulate(factors: SbrFactors, cols, counter: FlopCounter | None = None):
+    """Columns [lo, hi) of Q_s (backtrans.py:128-146), formed on the GPU."""
+    n = factors.n
+    lo, hi = cols
+    if not 0 <= lo <= hi <= n:
+        raise ValueError("column range out of bounds")
+    qs = _form_qs(factors)
+    if counter is not None:
+        counter.add("SBR-Back", max(1, (2 * n ** 3) // 3))
+    return np.asfortranarray(qs[:, lo:hi])
+
+
+def sbr_back_rows(factors: SbrFactors, rows, counter: FlopCounter | None = None):
+    """Rows [lo, hi) of Q_s (backtrans.py:186-192)."""
+    n = factors.n
+    lo, hi = rows
+    if not 0 <= lo <= hi <= n:
+        raise ValueError("row range out of bounds")
+    qs = _form_qs(factors)
+    if counter is not None:
+        counter.add("SBR-Back", max(1, (2 * n ** 3) // 3))
+    return np.ascontiguousarray(qs[lo:hi, :])
+
+
+def _form_qs(factors: SbrFactors) -> np.ndarray:
+    n, b = factors.n, factors.b
+    ystair = np.zeros((n, n), order="F")
+    rounds = max(1, len(factors.panels))
+    tall = np.zeros(rounds * b * b)
+    for x, p in enumerate(factors.panels):
+        m, pw = p.Y.shape
+        t0 = n - m
+        ystair[t0:, p.col_offset:p.col_offset + pw] = p.Y
+        T = getattr(p, "_T", None)
+        if T is None:  # W = Y T  ->  T = argmin ||Y T - W|| (upper triangular)
+            T = np.triu(np.linalg.lstsq(p.Y, p.W, rcond=None)[0])
+        tall[x * b * b: x * b * b + pw * pw] = np.asarray(T).T.reshape(-1)
+    return device.sbr_back_form(n, b, ystair, tall)
+
+
+def final_gemm(q_sb_block, q_d, counter: FlopCounter | None = None) -> np.ndarray:
+    """One block of rows of Q = Q_sb Q_d on the DMMA GEMM (backtrans.py:317-322)."""
+    if q_sb_block.shape[1] != q_d.shape[0]:
+        raise ValueError("inner dimensions disagree")
+    out = device.dgemm(q_sb_block, q_d)
+    if counter is not None:
+        counter.add("FinalMultiply", q_sb_block.shape[0] * q_d.shape[1] * q_d.shape[0])
+    return out
