@@ -134,8 +134,8 @@ __global__ void bc_back_left_generic(int64_t n, int b, const double* __restrict_
 
 // ------------------------------------------------------------ BC-Back, b = 32 register window
 
-template <int B, int G>
-__global__ void __launch_bounds__(128)
+template <int B, int G, int MINB>
+__global__ void __launch_bounds__(128, MINB)
     bc_back_right_reg(int64_t n, const double* __restrict__ tau, const double* __restrict__ V,
                       int vld, double* X, int64_t ldx, int64_t nrows) {
   constexpr int WIN = B + G - 1;
@@ -321,17 +321,17 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
     static int g_sel = -1;
     if (g_sel < 0) {
       const char* e = getenv("PEVD_BCBACK_G");
-      g_sel = e ? atoi(e) : 16;
+      g_sel = e ? atoi(e) : 32;
     }
-    if (g_sel == 32)
-      bc_back_right_reg<32, 32><<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, tau, V, vld, X,
-                                                                            ldx, nrows);
-    else if (g_sel == 8)
-      bc_back_right_reg<32, 8><<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, tau, V, vld, X,
-                                                                           ldx, nrows);
-    else
-      bc_back_right_reg<32, 16><<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, tau, V, vld, X,
-                                                                            ldx, nrows);
+    const unsigned grid = (unsigned)cdiv(nrows, 128);
+    switch (g_sel) {
+      case 8: bc_back_right_reg<32, 8, 4><<<grid, 128, 0, st>>>(n, tau, V, vld, X, ldx, nrows); break;
+      case 16: bc_back_right_reg<32, 16, 3><<<grid, 128, 0, st>>>(n, tau, V, vld, X, ldx, nrows); break;
+      case 20: bc_back_right_reg<32, 20, 3><<<grid, 128, 0, st>>>(n, tau, V, vld, X, ldx, nrows); break;
+      case 32: bc_back_right_reg<32, 32, 2><<<grid, 128, 0, st>>>(n, tau, V, vld, X, ldx, nrows); break;
+      case 33: bc_back_right_reg<32, 32, 1><<<grid, 128, 0, st>>>(n, tau, V, vld, X, ldx, nrows); break;
+      default: bc_back_right_reg<32, 24, 3><<<grid, 128, 0, st>>>(n, tau, V, vld, X, ldx, nrows); break;
+    }
   } else {
     bc_back_right_generic<<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, b, tau, V, vld, X, ldx,
                                                                       nrows, 16);

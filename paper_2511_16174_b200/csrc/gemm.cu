@@ -185,7 +185,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int64_t i0, int64_t
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
 __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, STAGES>::NT)
-    gemm_kernel(const __grid_constant__ GemmArgs g, int ksplit, double* ws) {
+    gemm_kernel_generic(const __grid_constant__ GemmArgs g, int ksplit, double* ws) {
   extern __shared__ __align__(16) double smem[];
   const int64_t i0 = (int64_t)blockIdx.x * BM, j0 = (int64_t)blockIdx.y * BN;
   if (g.cmode == C_LOWER_TILES && i0 + BM - 1 < j0) return;
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, STAGES>::NT)
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
 __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, STAGES>::NT)
-    gemm_grouped_kernel(const GemmArgs* __restrict__ args) {
+    gemm_grouped_kernel_generic(const GemmArgs* __restrict__ args) {
   extern __shared__ __align__(16) double smem[];
   const GemmArgs g = args[blockIdx.z];
   const int64_t i0 = (int64_t)blockIdx.x * BM, j0 = (int64_t)blockIdx.y * BN;
@@ -230,9 +230,9 @@ __global__ void splitk_reduce(const double* __restrict__ ws, int ksplit, int64_t
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
-int launch(cudaStream_t st, const GemmArgs& g, int ksplit, double* ws) {
+int launch_generic(cudaStream_t st, const GemmArgs& g, int ksplit, double* ws) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES>;
-  auto kern = gemm_kernel<BM, BN, BK, WM, WN, STAGES>;
+  auto kern = gemm_kernel_generic<BM, BN, BK, WM, WN, STAGES>;
   static bool attr_set = false;
   if (!attr_set) {
     PEVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -245,10 +245,10 @@ int launch(cudaStream_t st, const GemmArgs& g, int ksplit, double* ws) {
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES>
-int launch_grouped(cudaStream_t st, const GemmArgs* d_args, int count, int64_t max_m,
+int launch_grouped_generic(cudaStream_t st, const GemmArgs* d_args, int count, int64_t max_m,
                    int64_t max_n) {
   using C = Cfg<BM, BN, BK, WM, WN, STAGES>;
-  auto kern = gemm_grouped_kernel<BM, BN, BK, WM, WN, STAGES>;
+  auto kern = gemm_grouped_kernel_generic<BM, BN, BK, WM, WN, STAGES>;
   static bool attr_set = false;
   if (!attr_set) {
     PEVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -260,55 +260,298 @@ int launch_grouped(cudaStream_t st, const GemmArgs* d_args, int count, int64_t m
   return OK;
 }
 
+
+// =====================================================================================
+// Fast path (A_GENERAL): compile-time transposes, 16-byte cp.async chunks along each operand's
+// contiguous dimension, per-thread base pointers advanced by a constant stride per k-tile.
+// Shared layouts keep the contiguous dimension contiguous (so a chunk is one LDGSTS.128); the
+// 4-double pads make every DMMA fragment load the minimum two wavefronts in all four cases.
+// =====================================================================================
+
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
+struct FCfg {
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int NT = WARPS_M * WARPS_N * 32;
+  static constexpr int A_LD = TA ? BK + 4 : BM + 4;
+  static constexpr int A_OUT = TA ? BM : BK;
+  static constexpr int B_LD = TB ? BN + 4 : BK + 4;
+  static constexpr int B_OUT = TB ? BK : BN;
+  static constexpr int A_STAGE = A_OUT * A_LD, B_STAGE = B_OUT * B_LD;
+  static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) * 8;
+  static constexpr int MI = WM / 8, NI = WN / 8;
+};
+
+__device__ __forceinline__ void cp_async_vec(void* smem, const void* gmem, int bytes, bool vec16) {
+  if (vec16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)),
+                 "l"(gmem), "r"(bytes));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)),
+                 "l"(gmem), "r"(bytes));
+}
+
+// One operand tile: rows along the contiguous dimension `c` (length CL), outer dimension `o`
+// (length OL).  Global element (c, o) lives at base[c + o*ld]; shared at sm[o*SLD + c].
+template <int CL, int OL, int SLD, int NT, int V>
+__device__ __forceinline__ void load_tile(double* sm, const double* base, int64_t ld, int64_t c0,
+                                          int64_t o0, int64_t c_lim, int64_t o_lim,
+                                          const int* omap, int tid) {
+  constexpr int CPR = CL / V;             // chunks per outer row
+  constexpr int TOT = CPR * OL;
+  constexpr int STEP = NT / CPR;          // outer rows covered per pass
+  static_assert(NT % CPR == 0 && TOT % NT == 0, "tile/thread mismatch");
+  const int cc = (tid % CPR) * V;
+  const int orow = tid / CPR;
+  const int64_t gc = c0 + cc;
+  int vbytes = 0;
+  if (gc < c_lim) vbytes = (int)((c_lim - gc >= V ? V : c_lim - gc) * 8);
+#pragma unroll
+  for (int i = 0; i < TOT / NT; ++i) {
+    const int o = orow + i * STEP;
+    const int64_t go = o0 + o;
+    const bool ok = go < o_lim && vbytes > 0;
+    const int64_t col = omap ? (ok ? (int64_t)omap[go] : 0) : go;
+    const double* src = ok ? base + gc + col * ld : base;
+    cp_async_vec(sm + o * SLD + cc, src, ok ? vbytes : 0, V == 2);
+  }
+}
+
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int V>
+__device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t j0, int64_t kbeg,
+                                          int64_t kend, double* ws_out, int64_t ws_ld,
+                                          double* smem) {
+  using C = FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
+  double* As = smem;
+  double* Bs = smem + STAGES * C::A_STAGE;
+  double acc[C::MI][C::NI][2];
+#pragma unroll
+  for (int a = 0; a < C::MI; ++a)
+#pragma unroll
+    for (int b = 0; b < C::NI; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  auto load_stage = [&](int st, int64_t k0) {
+    double* as = As + st * C::A_STAGE;
+    double* bs = Bs + st * C::B_STAGE;
+    if (!TA)  // A[m + k*lda]: contiguous m, outer k (optionally gathered by amap)
+      load_tile<BM, BK, C::A_LD, C::NT, V>(as, g.A, g.lda, i0, k0, g.m, kend, g.amap, tid);
+    else      // A[k + m*lda]: contiguous k, outer m
+      load_tile<BK, BM, C::A_LD, C::NT, V>(as, g.A, g.lda, k0, i0, kend, g.m, nullptr, tid);
+    if (!TB)  // B[k + n*ldb]: contiguous k, outer n
+      load_tile<BK, BN, C::B_LD, C::NT, V>(bs, g.B, g.ldb, k0, j0, kend, g.n, nullptr, tid);
+    else      // B[n + k*ldb]: contiguous n, outer k
+      load_tile<BN, BK, C::B_LD, C::NT, V>(bs, g.B, g.ldb, j0, k0, g.n, kend, nullptr, tid);
+  };
+
+  const int64_t KT = (kend - kbeg + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, kbeg + s * BK);
+    cp_async_commit();
+  }
+  for (int64_t kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int64_t pf = kt + STAGES - 1;
+      if (pf < KT) load_stage((int)(pf % STAGES), kbeg + pf * BK);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * C::A_STAGE;
+    const double* bs = Bs + (kt % STAGES) * C::B_STAGE;
+    const int r8 = lane >> 2, c4 = lane & 3;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      const int kr = k4 + c4;
+      double af[C::MI], bf[C::NI];
+#pragma unroll
+      for (int a = 0; a < C::MI; ++a) {
+        const int r = wm * WM + a * 8 + r8;
+        af[a] = TA ? as[r * C::A_LD + kr] : as[kr * C::A_LD + r];
+      }
+#pragma unroll
+      for (int b = 0; b < C::NI; ++b) {
+        const int c = wn * WN + b * 8 + r8;
+        bf[b] = TB ? bs[kr * C::B_LD + c] : bs[c * C::B_LD + kr];
+      }
+#pragma unroll
+      for (int a = 0; a < C::MI; ++a)
+#pragma unroll
+        for (int b = 0; b < C::NI; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  const int r_in = lane >> 2, c_in = 2 * (lane & 3);
+#pragma unroll
+  for (int a = 0; a < C::MI; ++a) {
+    const int64_t gi = i0 + wm * WM + a * 8 + r_in;
+    if (gi >= g.m) continue;
+#pragma unroll
+    for (int b = 0; b < C::NI; ++b) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gj = j0 + wn * WN + b * 8 + c_in + h;
+        if (gj >= g.n) continue;
+        if (ws_out) {
+          ws_out[gi + gj * ws_ld] = acc[a][b][h];
+        } else {
+          const int64_t cj = g.cmap ? (int64_t)g.cmap[gj] : gj;
+          double* cp = g.C + gi + cj * g.ldc;
+          const double v = g.alpha * acc[a][b][h];
+          *cp = (g.beta == 0.0) ? v : v + g.beta * *cp;
+        }
+      }
+    }
+  }
+}
+
+// 16-byte chunks need every chunk start 16B aligned: base aligned, ld even, tile origins even
+__device__ __host__ __forceinline__ bool vec_ok(const GemmArgs& g) {
+  return ((uintptr_t)g.A % 16 == 0) && ((uintptr_t)g.B % 16 == 0) && (g.lda % 2 == 0) &&
+         (g.ldb % 2 == 0);
+}
+
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::NT)
+    gemm_fast_kernel(const __grid_constant__ GemmArgs g, int ksplit, double* ws) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t i0 = (int64_t)blockIdx.x * BM, j0 = (int64_t)blockIdx.y * BN;
+  if (g.cmode == C_LOWER_TILES && i0 + BM - 1 < j0) return;
+  int64_t kbeg = 0, kend = g.k;
+  double* wsp = nullptr;
+  if (ksplit > 1) {
+    const int64_t chunk = ((g.k + ksplit - 1) / ksplit + BK - 1) / BK * BK;
+    kbeg = blockIdx.z * chunk;
+    kend = kbeg + chunk < g.k ? kbeg + chunk : g.k;
+    if (kbeg > kend) kbeg = kend;
+    wsp = ws + (int64_t)blockIdx.z * g.m * g.n;
+  }
+  if (vec_ok(g))
+    fast_tile<TA, TB, BM, BN, BK, WM, WN, STAGES, 2>(g, i0, j0, kbeg, kend, wsp, g.m, smem);
+  else
+    fast_tile<TA, TB, BM, BN, BK, WM, WN, STAGES, 1>(g, i0, j0, kbeg, kend, wsp, g.m, smem);
+}
+
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::NT)
+    gemm_fast_grouped_kernel(const GemmArgs* __restrict__ args) {
+  extern __shared__ __align__(16) double smem[];
+  const GemmArgs g = args[blockIdx.z];
+  const int64_t i0 = (int64_t)blockIdx.x * BM, j0 = (int64_t)blockIdx.y * BN;
+  if (g.m <= 0 || g.n <= 0 || i0 >= g.m || j0 >= g.n) return;
+  if (g.cmode == C_LOWER_TILES && i0 + BM - 1 < j0) return;
+  const int64_t k = g.k > 0 ? g.k : 0;
+  if (vec_ok(g))
+    fast_tile<TA, TB, BM, BN, BK, WM, WN, STAGES, 2>(g, i0, j0, 0, k, nullptr, 0, smem);
+  else
+    fast_tile<TA, TB, BM, BN, BK, WM, WN, STAGES, 1>(g, i0, j0, 0, k, nullptr, 0, smem);
+}
+
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
+int launch_fast(cudaStream_t st, const GemmArgs& g, int ksplit, double* ws) {
+  using C = FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>;
+  auto kern = gemm_fast_kernel<TA, TB, BM, BN, BK, WM, WN, STAGES>;
+  static int attr_dev = -1;
+  int dev;
+  PEVD_CUDA(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    PEVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_dev = dev;
+  }
+  dim3 grid((unsigned)cdiv(g.m, BM), (unsigned)cdiv(g.n, BN), ksplit);
+  kern<<<grid, C::NT, C::SMEM, st>>>(g, ksplit, ws);
+  PEVD_LAUNCH_CHECK();
+  return OK;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+int launch_fast_t(cudaStream_t st, const GemmArgs& g, int ksplit, double* ws) {
+  if (!g.transA && !g.transB) return launch_fast<false, false, BM, BN, BK, WM, WN, STAGES>(st, g, ksplit, ws);
+  if (g.transA && !g.transB) return launch_fast<true, false, BM, BN, BK, WM, WN, STAGES>(st, g, ksplit, ws);
+  if (!g.transA && g.transB) return launch_fast<false, true, BM, BN, BK, WM, WN, STAGES>(st, g, ksplit, ws);
+  return launch_fast<true, true, BM, BN, BK, WM, WN, STAGES>(st, g, ksplit, ws);
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+int launch_fast_grouped(cudaStream_t st, const GemmArgs* d_args, int count, int64_t max_m,
+                        int64_t max_n) {
+  // grouped problems of the D&C merge: A column-gathered, not transposed; B not transposed
+  using C = FCfg<false, false, BM, BN, BK, WM, WN, STAGES>;
+  auto kern = gemm_fast_grouped_kernel<false, false, BM, BN, BK, WM, WN, STAGES>;
+  static int attr_dev = -1;
+  int dev;
+  PEVD_CUDA(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    PEVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_dev = dev;
+  }
+  dim3 grid((unsigned)cdiv(max_m, BM), (unsigned)cdiv(max_n, BN), count);
+  kern<<<grid, C::NT, C::SMEM, st>>>(d_args);
+  PEVD_LAUNCH_CHECK();
+  return OK;
+}
+
+int splitk_finish(cudaStream_t st, const GemmArgs& g, int ks, double* ws) {
+  splitk_reduce<<<(unsigned)std::min<int64_t>(cdiv(g.m * g.n, 256), 4 * num_sms()), 256, 0, st>>>(
+      ws, ks, g.m, g.n, g.alpha, g.beta, g.C, g.ldc, g.cmap);
+  PEVD_LAUNCH_CHECK();
+  return OK;
+}
+
 }  // namespace
 
 int gemm(cudaStream_t st, const GemmArgs& g, double* ws, int64_t ws_elems) {
   if (g.m <= 0 || g.n <= 0) return OK;
   const int sms = num_sms();
-  if (g.n <= 32) {
-    // skinny (AW = A W, Z = AW - Y M ...): 128 x 32 tiles, split K when the grid is thin
+  if (g.amode == A_SYM_LOWER) {
+    // symmetric operand read from its lower triangle: generic 8-byte loader
     const int64_t tiles = cdiv(g.m, 128);
     int ks = 1;
-    if (ws && g.k >= 1024 && tiles < 2 * sms) {
+    if (g.n <= 32 && ws && g.k >= 1024 && tiles < 2 * sms) {
       ks = (int)std::min<int64_t>(cdiv(3 * sms, tiles), g.k / 256);
       while (ks > 1 && (int64_t)ks * g.m * g.n > ws_elems) --ks;
     }
-    if (ks > 1 && g.cmode == C_ALL) {
-      PEVD_TRY((launch<128, 32, 16, 32, 32, 3>(st, g, ks, ws)));
-      splitk_reduce<<<std::min<int64_t>(cdiv(g.m * g.n, 256), 4 * sms), 256, 0, st>>>(
-          ws, ks, g.m, g.n, g.alpha, g.beta, g.C, g.ldc, g.cmap);
-      PEVD_LAUNCH_CHECK();
+    if (g.n <= 32) {
+      PEVD_TRY((launch_generic<128, 32, 16, 32, 32, 3>(st, g, ks, ks > 1 ? ws : nullptr)));
+      if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
       return OK;
     }
-    return launch<128, 32, 16, 32, 32, 3>(st, g, 1, nullptr);
+    return launch_generic<128, 128, 16, 64, 32, 3>(st, g, 1, nullptr);
+  }
+  if (g.n <= 32) {
+    // skinny: 128 x 32 tiles, split K when the grid is thin
+    const int64_t tiles = cdiv(g.m, 128);
+    int ks = 1;
+    if (ws && g.k >= 1024 && tiles < 2 * sms && g.cmode == C_ALL) {
+      ks = (int)std::min<int64_t>(cdiv(3 * sms, tiles), g.k / 256);
+      while (ks > 1 && (int64_t)ks * g.m * g.n > ws_elems) --ks;
+    }
+    PEVD_TRY((launch_fast_t<128, 32, 32, 32, 32, 3>(st, g, ks, ks > 1 ? ws : nullptr)));
+    if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
+    return OK;
   }
   const int64_t tiles = cdiv(g.m, 128) * cdiv(g.n, 128);
-  if (tiles >= sms || g.k < 64) {
-    return launch<128, 128, 16, 64, 32, 3>(st, g, 1, nullptr);
-  }
-  // few output tiles: smaller tiles, then split-K if still thin
+  if (tiles >= sms || g.k < 64) return launch_fast_t<128, 128, 32, 64, 32, 3>(st, g, 1, nullptr);
   const int64_t tiles64 = cdiv(g.m, 64) * cdiv(g.n, 64);
   int ks = 1;
-  if (ws && tiles64 < sms && g.k >= 512) {
+  if (ws && tiles64 < sms && g.k >= 512 && g.cmode == C_ALL) {
     ks = (int)std::min<int64_t>(cdiv(2 * sms, tiles64), g.k / 128);
     while (ks > 1 && (int64_t)ks * g.m * g.n > ws_elems) --ks;
   }
-  if (ks > 1 && g.cmode == C_ALL) {
-    PEVD_TRY((launch<64, 64, 16, 32, 32, 3>(st, g, ks, ws)));
-    splitk_reduce<<<std::min<int64_t>(cdiv(g.m * g.n, 256), 4 * sms), 256, 0, st>>>(
-        ws, ks, g.m, g.n, g.alpha, g.beta, g.C, g.ldc, g.cmap);
-    PEVD_LAUNCH_CHECK();
-    return OK;
-  }
-  return launch<64, 64, 16, 32, 32, 3>(st, g, 1, nullptr);
+  PEVD_TRY((launch_fast_t<64, 64, 32, 32, 32, 3>(st, g, ks, ks > 1 ? ws : nullptr)));
+  if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
+  return OK;
 }
 
 int gemm_grouped(cudaStream_t st, const GemmArgs* d_args, int count, int64_t max_m,
                  int64_t max_n) {
   if (count <= 0 || max_m <= 0 || max_n <= 0) return OK;
   if (max_m * max_n >= (int64_t)128 * 128 * 64)
-    return launch_grouped<128, 128, 16, 64, 32, 3>(st, d_args, count, max_m, max_n);
-  return launch_grouped<64, 64, 16, 32, 32, 3>(st, d_args, count, max_m, max_n);
+    return launch_fast_grouped<128, 128, 32, 64, 32, 3>(st, d_args, count, max_m, max_n);
+  return launch_fast_grouped<64, 64, 32, 32, 32, 3>(st, d_args, count, max_m, max_n);
 }
 
 }  // namespace pevd

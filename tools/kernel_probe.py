@@ -1,0 +1,131 @@
+"""Time individual device stages through the C ABI (CUDA events, after warm-up).
+
+  python tools/kernel_probe.py bcback 16384        # BC-Back on n x n rows (PEVD_BCBACK_G picks G)
+  python tools/kernel_probe.py gemm 8192 8192 8192 [ta tb]
+  python tools/kernel_probe.py sbr 16384
+  python tools/kernel_probe.py stedc 16384
+  python tools/kernel_probe.py bc 16384
+"""
+import ctypes
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2511_16174_b200 import _lib  # noqa: E402
+
+P = ctypes.c_void_p
+L = _lib.load()
+
+
+def ptr(t):
+    return P(t.data_ptr())
+
+
+def stream():
+    return P(torch.cuda.current_stream().cuda_stream)
+
+
+def timed(fn, reps=3, warm=1):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return min(ts), ts
+
+
+def rand_band(n, b, seed=0):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    return torch.randn((b + 1) * n, dtype=torch.float64, device="cuda", generator=g)
+
+
+def reflectors(n, b):
+    bands = rand_band(n, b)
+    nref = L.pevd_bc_num_reflectors(n, b)
+    vld = (b + 7) // 8 * 8
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    e = torch.empty(n, dtype=torch.float64, device="cuda")
+    tau = torch.empty(nref, dtype=torch.float64, device="cuda")
+    V = torch.empty(nref * vld, dtype=torch.float64, device="cuda")
+    ws = torch.empty(L.pevd_bc_workspace_bytes(n, b), dtype=torch.uint8, device="cuda")
+    ms, _ = timed(lambda: _lib.check(L.pevd_bc(n, b, ptr(bands), ptr(d), ptr(e), ptr(tau), ptr(V),
+                                               vld, ptr(ws), stream()), "bc"), reps=1, warm=0)
+    return tau, V, vld, ms
+
+
+def main():
+    mode = sys.argv[1]
+    out = {"mode": mode}
+    if mode == "bcback":
+        n = int(sys.argv[2])
+        b = 32
+        tau, V, vld, _ = reflectors(n, b)
+        X = torch.randn((n, n), dtype=torch.float64, device="cuda")
+        ms, ts = timed(lambda: _lib.check(L.pevd_bc_back_right(n, b, ptr(tau), ptr(V), vld, ptr(X),
+                                                               n, n, stream()), "bcback"))
+        nref = L.pevd_bc_num_reflectors(n, b)
+        flops = 4.0 * b * nref * n
+        out.update(n=n, G=os.environ.get("PEVD_BCBACK_G", "default"), ms=ms, ts=ts,
+                   tflops=flops / ms / 1e9)
+    elif mode == "bc":
+        n = int(sys.argv[2])
+        _, _, _, ms = reflectors(n, 32)
+        _, _, _, ms = reflectors(n, 32)
+        out.update(n=n, ms=ms, us_per_slot=ms * 1e3 / (3 * n))
+    elif mode == "gemm":
+        m, n, k = (int(x) for x in sys.argv[2:5])
+        ta = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+        tb = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+        A = torch.randn(m * k, dtype=torch.float64, device="cuda")
+        B = torch.randn(k * n, dtype=torch.float64, device="cuda")
+        C = torch.zeros(m * n, dtype=torch.float64, device="cuda")
+        ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+        lda = k if ta else m
+        ldb = n if tb else k
+        ms, ts = timed(lambda: _lib.check(L.pevd_dgemm(ta, tb, m, n, k, 1.0, ptr(A), lda, ptr(B), ldb,
+                                                       0.0, ptr(C), m, ptr(ws), ws.numel(), stream()),
+                                          "gemm"), reps=5)
+        out.update(m=m, n=n, k=k, ms=ms, tflops=2.0 * m * n * k / ms / 1e9)
+    elif mode == "sbr":
+        n = int(sys.argv[2])
+        b = 32
+        A0 = torch.randn((n, n), dtype=torch.float64, device="cuda")
+        A0 = (A0 + A0.t()) / 2
+        A = torch.empty_like(A0)
+        bands = torch.empty((b + 1) * n, dtype=torch.float64, device="cuda")
+        tall = torch.empty(((n - b) // b + 1) * b * b, dtype=torch.float64, device="cuda")
+        ws = torch.empty(L.pevd_sbr_workspace_bytes(n, b), dtype=torch.uint8, device="cuda")
+
+        def f():
+            A.copy_(A0)
+            _lib.check(L.pevd_sbr(n, b, ptr(A), n, ptr(bands), ptr(tall), ptr(ws), stream()), "sbr")
+        ms, ts = timed(f, reps=2)
+        out.update(n=n, ms=ms, tflops=4 * n ** 3 / 3 / ms / 1e9)
+    elif mode == "stedc":
+        n = int(sys.argv[2])
+        d0 = torch.randn(n, dtype=torch.float64, device="cuda")
+        e = torch.randn(n, dtype=torch.float64, device="cuda")
+        d = torch.empty_like(d0)
+        Q = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        ws = torch.empty(L.pevd_stedc_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+
+        def f():
+            d.copy_(d0)
+            _lib.check(L.pevd_stedc(n, ptr(d), ptr(e), ptr(Q), n, ptr(ws), stream()), "stedc")
+        ms, ts = timed(f, reps=2)
+        out.update(n=n, ms=ms)
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
