@@ -59,7 +59,7 @@ struct Carve {
 
 struct Layout {
   double *bands, *Tall, *d, *e, *tau, *V, *Qs, *Qd;
-  void *ws_sbr, *ws_bc, *ws_dc, *ws_back;
+  void *ws_sbr, *ws_bc, *ws_dc, *ws_back, *ws_bcb;
   int vld;
   int64_t total;
 };
@@ -84,6 +84,7 @@ Layout plan_layout(void* base, int64_t n, int b, int want_vectors, int order) {
   L.ws_bc = c.take(bc_ws_bytes(n, b));
   L.ws_dc = c.take(stedc_ws_bytes(n));
   L.ws_back = c.take(sbr_back_ws_bytes(n, b));
+  L.ws_bcb = c.take(bc_back_ws_bytes(n));
   L.total = c.off;
   return L;
 }
@@ -195,7 +196,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     if (want_vectors && order != PEVD_ORDER_CONVENTIONAL) {
       if (two_streams) cudaStreamWaitEvent(sback, ev[1].b, 0);
       cudaEventRecord(ev[4].a, sback);
-      if ((rc = bc_back_right(sback, n, b, L.tau, L.V, L.vld, L.Qs, n, n))) break;
+      if ((rc = bc_back_right(sback, n, b, L.tau, L.V, L.vld, L.Qs, n, n, L.ws_bcb))) break;
       cudaEventRecord(ev[4].b, sback);
     }
     // ---- D&C
@@ -365,9 +366,11 @@ int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, const double* Tal
   return sbr_back_apply_left((cudaStream_t)stream, n, b, Ystair, Tall, X, ldx, ncols, workspace);
 }
 
+int64_t pevd_bc_back_workspace_bytes(int64_t nrows) { return bc_back_ws_bytes(nrows); }
+
 int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
-                       int64_t ldx, int64_t nrows, void* stream) {
-  return bc_back_right((cudaStream_t)stream, n, b, tau, V, vld, X, ldx, nrows);
+                       int64_t ldx, int64_t nrows, void* workspace, void* stream) {
+  return bc_back_right((cudaStream_t)stream, n, b, tau, V, vld, X, ldx, nrows, workspace);
 }
 
 int pevd_bc_back_left(int64_t n, int b, const double* tau, const double* V, int vld, double* X,

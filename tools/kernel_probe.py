@@ -71,8 +71,9 @@ def main():
         b = 32
         tau, V, vld, _ = reflectors(n, b)
         X = torch.randn((n, n), dtype=torch.float64, device="cuda")
+        ws = torch.empty(L.pevd_bc_back_workspace_bytes(n), dtype=torch.uint8, device="cuda")
         ms, ts = timed(lambda: _lib.check(L.pevd_bc_back_right(n, b, ptr(tau), ptr(V), vld, ptr(X),
-                                                               n, n, stream()), "bcback"))
+                                                               n, n, ptr(ws), stream()), "bcback"))
         nref = L.pevd_bc_num_reflectors(n, b)
         flops = 4.0 * b * nref * n
         out.update(n=n, G=os.environ.get("PEVD_BCBACK_G", "default"), ms=ms, ts=ts,
