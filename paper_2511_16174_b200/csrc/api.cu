@@ -84,7 +84,7 @@ Layout plan_layout(void* base, int64_t n, int b, int want_vectors, int order) {
   L.ws_bc = c.take(bc_ws_bytes(n, b));
   L.ws_dc = c.take(stedc_ws_bytes(n));
   L.ws_back = c.take(sbr_back_ws_bytes(n, b));
-  L.ws_bcb = c.take(bc_back_ws_bytes(n));
+  L.ws_bcb = c.take(bc_back_ws_bytes(n, n));
   L.total = c.off;
   return L;
 }
@@ -366,7 +366,7 @@ int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, const double* Tal
   return sbr_back_apply_left((cudaStream_t)stream, n, b, Ystair, Tall, X, ldx, ncols, workspace);
 }
 
-int64_t pevd_bc_back_workspace_bytes(int64_t nrows) { return bc_back_ws_bytes(nrows); }
+int64_t pevd_bc_back_workspace_bytes(int64_t n, int64_t nrows) { return bc_back_ws_bytes(n, nrows); }
 
 int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
                        int64_t ldx, int64_t nrows, void* workspace, void* stream) {

@@ -15,6 +15,7 @@
 // chase steps, so each entry of X is loaded and stored once per sweep group: arithmetic
 // intensity G/4 flop/byte.  The group's reflectors are staged in shared memory (broadcast reads).
 #include <cstdlib>
+#include <vector>
 #include "kernels.cuh"
 
 namespace pevd {
@@ -392,6 +393,247 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
   }
 }
 
+// ------------------------------------------------------------ BC-Back, b = 32, DMMA compact WY
+// A warp owns 8 rows of X and a 96-column window (Q4_SG = 64 sweeps + b) kept as 12 DMMA
+// accumulator tiles (lane l holds X[l/4][8c + 2(l%4) + h]).  The 64 reflectors of a tile
+// (sweeps i0..i0+63 at chase step j) are applied as 8 blocks of 8 with the compact WY form
+// (forward T, LAPACK larft):  X_slice <- X_slice (I - V T V^T),  slice = window columns
+// [8s, 8s+40):
+//   P  = X_slice V        10 DMMA   (A operand = the accumulator tiles themselves)
+//   P2 = P (-T)            2 DMMA
+//   X_slice += P2 V^T     10 DMMA
+// The accumulator layout gives lane l the columns {2(l%4), 2(l%4)+1} of each 8-column tile; by
+// reading the k-index of every B operand through that permutation (k-slot l%4 of k-step h is
+// column/reflector 2(l%4)+h) the C fragments ARE the A fragments: no shuffles, no conversion.
+// The T factors of all blocks are computed up front (wy_tfactor_kernel); each step's V and -T
+// are prefetched into registers during the previous step and staged double-buffered.
+constexpr int WY_ROWS = 64;  // 8 warps x 8 rows
+constexpr int WY_THREADS = 256;
+constexpr int WY_VP = 48;    // padded reflector row: v[idx] at idx + 8, idx in [-8, 40)
+constexpr int WY_PF = (Q4_SG * 32 + Q4_SG * 8) / WY_THREADS;  // prefetched doubles per thread
+
+struct WySmem {
+  double vp[2][Q4_SG][WY_VP];
+  double T[2][Q4_SG / 8][8][8];  // -T per block, [buf][block][s][t]
+  int unit;
+};
+
+// -T of every block of 8 consecutive sweeps at every chase step.  Block (j, q) covers sweeps
+// 8q..8q+7 and lives at Tf + 64 * (tofs[j] + q).
+__global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
+                                  const double* __restrict__ V, int vld,
+                                  const int64_t* __restrict__ tofs, int64_t jcount,
+                                  double* __restrict__ Tf) {
+  constexpr int B = 32;
+  const int64_t total = tofs[jcount];
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    // locate j by binary search on tofs
+    int64_t lo = 0, hi = jcount;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (tofs[mid] <= id) lo = mid; else hi = mid;
+    }
+    const int64_t j = lo, q = id - tofs[j];
+    const int64_t off = bc_slot_offset_dev(n, B, j);
+    const int64_t nsw_j = n - 2 - j * B;
+    double tv[8];
+    const double* v[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int64_t i = 8 * q + s;
+      const bool ok = i < nsw_j;
+      tv[s] = ok ? tau[off + i] : 0.0;
+      v[s] = V + (ok ? (off + i) : off) * vld;
+    }
+    double T[8][8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) T[s][t] = 0.0;
+      if (tv[t] == 0.0) continue;
+      T[t][t] = tv[t];
+      // g_u = v_u^T v_t for u < t (v_u starts t - u rows above v_t)
+      double g[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        g[u] = 0.0;
+        if (u < t && tv[u] != 0.0) {
+          const int d = t - u;
+          double acc = 0.0;
+          for (int r = 0; r < B - d; ++r) acc = fma(v[u][r + d], v[t][r], acc);
+          g[u] = acc;
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        if (s < t) {
+          double acc = 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (u >= s && u < t) acc = fma(T[s][u], g[u], acc);
+          T[s][t] = -tv[t] * acc;
+        }
+      }
+    }
+    double* out = Tf + id * 64;
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) out[s * 8 + t] = -T[s][t];
+  }
+}
+
+__global__ void __launch_bounds__(WY_THREADS, 2)
+    bc_back_wy_kernel(int64_t n, const double* __restrict__ V, int vld,
+                      const double* __restrict__ Tf, const int64_t* __restrict__ tofs, double* X,
+                      int64_t ldx, int64_t nrows, int* counter, int* progress, int64_t nunits,
+                      int nrb) {
+  extern __shared__ __align__(16) unsigned char wyraw[];
+  WySmem& S = *reinterpret_cast<WySmem*>(wyraw);
+  constexpr int B = 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int qd = lane & 3, r8 = lane >> 2;
+  const int64_t nsw = n - 2;
+  for (int e = tid; e < 2 * Q4_SG * WY_VP; e += WY_THREADS) (&S.vp[0][0][0])[e] = 0.0;
+  __syncthreads();
+  // prefetch registers: element e = tid + p * WY_THREADS; e < 2048: V(t = e/32, r = e%32),
+  // else -T (block = (e-2048)/64, entry (e-2048)%64)
+  auto fetch = [&](int64_t i0, int64_t j, double* pf) {
+    const int64_t off = bc_slot_offset_dev(n, B, j);
+    const int64_t nsw_j = n - 2 - j * B;
+    const int64_t tb = tofs[j] + i0 / 8;
+#pragma unroll
+    for (int p = 0; p < WY_PF; ++p) {
+      const int e = tid + p * WY_THREADS;
+      if (e < Q4_SG * B) {
+        const int t = e >> 5, r = e & 31;
+        const int64_t i = i0 + t;
+        pf[p] = (i < nsw_j) ? __ldg(V + (off + i) * vld + r) : 0.0;
+      } else {
+        const int e2 = e - Q4_SG * B;
+        const int blk = e2 >> 6;
+        pf[p] = (i0 + 8 * blk < nsw_j) ? __ldg(Tf + (tb + blk) * 64 + (e2 & 63)) : 0.0;
+      }
+    }
+  };
+  auto stage = [&](int buf, const double* pf) {
+#pragma unroll
+    for (int p = 0; p < WY_PF; ++p) {
+      const int e = tid + p * WY_THREADS;
+      if (e < Q4_SG * B) S.vp[buf][e >> 5][(e & 31) + 8] = pf[p];
+      else (&S.T[buf][0][0][0])[e - Q4_SG * B] = pf[p];
+    }
+  };
+  (void)nsw;
+  for (;;) {
+    if (tid == 0) S.unit = atomicAdd(counter, 1);
+    __syncthreads();
+    const int64_t u = S.unit;
+    __syncthreads();
+    if (u >= nunits) break;
+    const int64_t k = u / nrb;
+    const int rb = (int)(u % nrb);
+    if (tid == 0 && ld_acquire(progress + rb) < (int)k) {
+      unsigned ns = 64;
+      while (ld_acquire(progress + rb) < (int)k) {
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+      }
+    }
+    const int64_t row = (int64_t)rb * WY_ROWS + warp * 8 + r8;
+    const bool active = row < nrows;
+    double* x = X + (active ? row : 0);
+    const int64_t i0 = k * Q4_SG;
+    const int64_t jmax = (n - 3 - i0) / B;
+    int64_t ws = i0 + 1 + jmax * B;
+    double pf[WY_PF];
+    fetch(i0, jmax, pf);
+    __syncthreads();  // progress acquired by tid 0 before anyone reads X
+    double w[12][2];
+#pragma unroll
+    for (int c = 0; c < 12; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t col = ws + 8 * c + 2 * qd + h;
+        w[c][h] = (active && col < n) ? __ldcg(x + col * ldx) : 0.0;
+      }
+    int buf = 0;
+    stage(buf, pf);
+    __syncthreads();
+    for (int64_t j = jmax; j >= 0; --j) {
+      // prefetch the next step: its new window columns [ws - 32, ws) and its V / -T
+      double nx[4][2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          nx[c][h] = (j > 0 && active) ? __ldcg(x + (ws - B + 8 * c + 2 * qd + h) * ldx) : 0.0;
+      if (j > 0) fetch(i0, j - 1, pf);
+      // ---- apply the 8 blocks of this step
+#pragma unroll
+      for (int blk = 0; blk < Q4_SG / 8; ++blk) {
+        const int tb = blk * 8;
+        double p0 = 0.0, p1 = 0.0, e0 = 0.0, e1 = 0.0;
+        const double* vrow = &S.vp[buf][tb + r8][8 + 2 * qd - r8];
+#pragma unroll
+        for (int cc = 0; cc < 5; ++cc) {
+          dmma884(p0, p1, w[blk + cc][0], vrow[8 * cc]);
+          dmma884(e0, e1, w[blk + cc][1], vrow[8 * cc + 1]);
+        }
+        p0 += e0;
+        p1 += e1;
+        double q0 = 0.0, q1 = 0.0;
+        dmma884(q0, q1, p0, S.T[buf][blk][2 * qd][r8]);
+        dmma884(q0, q1, p1, S.T[buf][blk][2 * qd + 1][r8]);
+#pragma unroll
+        for (int cc = 0; cc < 5; ++cc) {
+          const double va = S.vp[buf][tb + 2 * qd][8 + 8 * cc + r8 - 2 * qd];
+          const double vb = S.vp[buf][tb + 2 * qd + 1][8 + 8 * cc + r8 - 2 * qd - 1];
+          dmma884(w[blk + cc][0], w[blk + cc][1], q0, va);
+          dmma884(w[blk + cc][0], w[blk + cc][1], q1, vb);
+        }
+      }
+      // ---- slide: tiles 8..11 are final for this group; shift by b = 32 (4 tiles)
+#pragma unroll
+      for (int c = 8; c < 12; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t col = ws + 8 * c + 2 * qd + h;
+          if (active && col < n) x[col * ldx] = w[c][h];
+        }
+      if (j > 0) {
+#pragma unroll
+        for (int c = 11; c >= 4; --c) {
+          w[c][0] = w[c - 4][0];
+          w[c][1] = w[c - 4][1];
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          w[c][0] = nx[c][0];
+          w[c][1] = nx[c][1];
+        }
+        ws -= B;
+        stage(buf ^ 1, pf);  // the other buffer: nobody reads it during this step
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t col = ws + 8 * c + 2 * qd + h;
+            if (active && col < n) x[col * ldx] = w[c][h];
+          }
+      }
+      buf ^= 1;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      __threadfence();
+      st_release(progress + rb, (int)(k + 1));
+    }
+  }
+}
+
 }  // namespace
 
 int64_t sbr_back_ws_bytes(int64_t n, int b) {
@@ -473,7 +715,13 @@ int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, 
   return OK;
 }
 
-int64_t bc_back_ws_bytes(int64_t nrows) { return (cdiv(nrows, Q4_ROWS) + 64) * 4; }
+int64_t bc_back_ws_bytes(int64_t n, int64_t nrows) {
+  // counters + T-factor offsets + the -T factors of every block of 8 sweeps (64 doubles each)
+  const int64_t jcount = n >= 3 ? (n - 3) / 32 + 1 : 1;
+  int64_t nblk = 0;
+  for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(std::max<int64_t>(n - 2 - j * 32, 0), 8);
+  return ((nrows / 32 + 64) * 4 + 255) / 256 * 256 + (jcount + 2) * 8 + nblk * 64 * 8 + 256;
+}
 
 int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                   double* X, int64_t ldx, int64_t nrows, void* ws) {
@@ -481,34 +729,54 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("PEVD_BCBACK");
-    mode = (e && e[0] == 'q') ? 0 : 1;  // register-window kernel by default
+    mode = (e && e[0] == 'q') ? 0 : (e && e[0] == 'r') ? 1 : 2;  // DMMA compact WY by default
   }
-  if (b == 32 && vld >= 32 && mode == 0 && ws) {
-    const int nrb = (int)cdiv(nrows, Q4_ROWS);
+  if (b == 32 && vld >= 32 && mode != 1 && ws) {
+    // mode 0: 4-lane DFMA kernel, mode 2 (default): DMMA compact-WY kernel
+    const bool wy = mode == 2;
+    const int rows_per = wy ? WY_ROWS : Q4_ROWS;
+    const int nrb = (int)cdiv(nrows, rows_per);
     const int64_t ngroups = cdiv(n - 2, Q4_SG);
     const int64_t nunits = ngroups * nrb;
     int* counter = (int*)ws;
     int* progress = counter + 32;
+    const int64_t jcount = (n - 3) / 32 + 1;
+    int64_t* tofs = (int64_t*)((char*)ws + ((nrows / 32 + 64) * 4 + 255) / 256 * 256);
+    double* Tf = (double*)(tofs + jcount + 2);
     PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
-    const size_t smem = sizeof(Q4Smem);
-    static int attr_dev = -1;
+    if (wy) {
+      std::vector<int64_t> h(jcount + 1);
+      h[0] = 0;
+      for (int64_t j = 0; j < jcount; ++j) h[j + 1] = h[j] + cdiv(n - 2 - j * 32, 8);
+      PEVD_CUDA(cudaMemcpyAsync(tofs, h.data(), (jcount + 1) * 8, cudaMemcpyHostToDevice, st));
+      PEVD_CUDA(cudaStreamSynchronize(st));  // h is pageable and goes out of scope
+      wy_tfactor_kernel<<<(unsigned)std::min<int64_t>(cdiv(h[jcount], 128), 16384), 128, 0, st>>>(
+          n, tau, V, vld, tofs, jcount, Tf);
+      PEVD_LAUNCH_CHECK();
+    }
+    const void* kfn = wy ? (const void*)bc_back_wy_kernel : (const void*)bc_back_q4_kernel;
+    const size_t smem = wy ? sizeof(WySmem) : sizeof(Q4Smem);
+    const int nthr = wy ? WY_THREADS : Q4_THREADS;
+    static int attr_dev[2] = {-1, -1};
     int dev;
     PEVD_CUDA(cudaGetDevice(&dev));
-    if (attr_dev != dev) {
-      PEVD_CUDA(cudaFuncSetAttribute(bc_back_q4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-      attr_dev = dev;
+    if (attr_dev[wy] != dev) {
+      PEVD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_dev[wy] = dev;
     }
     int per_sm = 0;
-    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bc_back_q4_kernel, Q4_THREADS,
-                                                            smem));
+    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nthr, smem));
     if (per_sm < 1) {
       set_error("bc_back: persistent kernel cannot be resident");
       return ERR_CUDA;
     }
     const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
-    bc_back_q4_kernel<<<(unsigned)grid, Q4_THREADS, smem, st>>>(n, tau, V, vld, X, ldx, nrows,
-                                                                counter, progress, nunits, nrb);
+    if (wy)
+      bc_back_wy_kernel<<<(unsigned)grid, nthr, smem, st>>>(n, V, vld, Tf, tofs, X, ldx, nrows,
+                                                            counter, progress, nunits, nrb);
+    else
+      bc_back_q4_kernel<<<(unsigned)grid, nthr, smem, st>>>(n, tau, V, vld, X, ldx, nrows, counter,
+                                                            progress, nunits, nrb);
     PEVD_LAUNCH_CHECK();
     return OK;
   }

@@ -268,12 +268,14 @@ int launch_grouped_generic(cudaStream_t st, const GemmArgs* d_args, int count, i
 // 4-double pads make every DMMA fragment load the minimum two wavefronts in all four cases.
 // =====================================================================================
 
-template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, bool SYM = false>
 struct FCfg {
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int NT = WARPS_M * WARPS_N * 32;
-  static constexpr int A_LD = TA ? BK + 4 : BM + 4;
-  static constexpr int A_OUT = TA ? BM : BK;
+  static constexpr int A_LD0 = BM + 4, A_LD1 = BK + 4;   // m-contiguous / k-contiguous layouts
+  static constexpr int A_LD = TA ? A_LD1 : A_LD0;
+  static constexpr int A_OUT = SYM ? (BK * A_LD0 > BM * A_LD1 ? BK : (BM * A_LD1 + A_LD0 - 1) / A_LD0)
+                                   : (TA ? BM : BK);
   static constexpr int B_LD = TB ? BN + 4 : BK + 4;
   static constexpr int B_OUT = TB ? BK : BN;
   static constexpr int A_STAGE = A_OUT * A_LD, B_STAGE = B_OUT * B_LD;
@@ -316,11 +318,12 @@ __device__ __forceinline__ void load_tile(double* sm, const double* base, int64_
   }
 }
 
-template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int V>
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int V,
+          bool SYM = false>
 __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t j0, int64_t kbeg,
                                           int64_t kend, double* ws_out, int64_t ws_ld,
                                           double* smem) {
-  using C = FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>;
+  using C = FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES, SYM>;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
@@ -332,10 +335,28 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
 #pragma unroll
     for (int b = 0; b < C::NI; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
+  // symmetric-lower A (A_SYM_LOWER): per k-tile, tiles on/below the diagonal are read as stored
+  // (m-contiguous), tiles above it from their mirror below the diagonal (k-contiguous layout),
+  // and the few tiles crossing the diagonal element by element.
+  auto sym_mode = [&](int64_t k0) { return (k0 + BK - 1 <= i0) ? 0 : (k0 >= i0 + BM ? 1 : 2); };
   auto load_stage = [&](int st, int64_t k0) {
     double* as = As + st * C::A_STAGE;
     double* bs = Bs + st * C::B_STAGE;
-    if (!TA)  // A[m + k*lda]: contiguous m, outer k (optionally gathered by amap)
+    if (SYM) {
+      const int md = sym_mode(k0);
+      if (md == 0)
+        load_tile<BM, BK, C::A_LD0, C::NT, V>(as, g.A, g.lda, i0, k0, g.m, kend, nullptr, tid);
+      else if (md == 1)
+        load_tile<BK, BM, C::A_LD1, C::NT, V>(as, g.A, g.lda, k0, i0, kend, g.m, nullptr, tid);
+      else
+        for (int idx = tid; idx < BM * BK; idx += C::NT) {
+          const int i = idx % BM, kk = idx / BM;
+          const int64_t gi = i0 + i, gk = k0 + kk;
+          const bool ok = gi < g.m && gk < kend;
+          const double* src = (gi >= gk) ? g.A + gi + gk * g.lda : g.A + gk + gi * g.lda;
+          cp_async8(as + kk * C::A_LD0 + i, ok ? src : g.A, ok);
+        }
+    } else if (!TA)  // A[m + k*lda]: contiguous m, outer k (optionally gathered by amap)
       load_tile<BM, BK, C::A_LD, C::NT, V>(as, g.A, g.lda, i0, k0, g.m, kend, g.amap, tid);
     else      // A[k + m*lda]: contiguous k, outer m
       load_tile<BK, BM, C::A_LD, C::NT, V>(as, g.A, g.lda, k0, i0, kend, g.m, nullptr, tid);
@@ -362,6 +383,7 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
     const double* as = As + (kt % STAGES) * C::A_STAGE;
     const double* bs = Bs + (kt % STAGES) * C::B_STAGE;
     const int r8 = lane >> 2, c4 = lane & 3;
+    const bool a_kc = SYM ? (sym_mode(kbeg + kt * BK) == 1) : TA;  // k-contiguous A layout
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
       const int kr = k4 + c4;
@@ -369,7 +391,7 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
 #pragma unroll
       for (int a = 0; a < C::MI; ++a) {
         const int r = wm * WM + a * 8 + r8;
-        af[a] = TA ? as[r * C::A_LD + kr] : as[kr * C::A_LD + r];
+        af[a] = a_kc ? as[r * C::A_LD1 + kr] : as[kr * C::A_LD0 + r];
       }
 #pragma unroll
       for (int b = 0; b < C::NI; ++b) {
@@ -414,8 +436,8 @@ __device__ __host__ __forceinline__ bool vec_ok(const GemmArgs& g) {
          (g.ldb % 2 == 0);
 }
 
-template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::NT)
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, bool SYM>
+__global__ void __launch_bounds__(FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES, SYM>::NT)
     gemm_fast_kernel(const __grid_constant__ GemmArgs g, int ksplit, double* ws) {
   extern __shared__ __align__(16) double smem[];
   const int64_t i0 = (int64_t)blockIdx.x * BM, j0 = (int64_t)blockIdx.y * BN;
@@ -430,9 +452,9 @@ __global__ void __launch_bounds__(FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::NT)
     wsp = ws + (int64_t)blockIdx.z * g.m * g.n;
   }
   if (vec_ok(g))
-    fast_tile<TA, TB, BM, BN, BK, WM, WN, STAGES, 2>(g, i0, j0, kbeg, kend, wsp, g.m, smem);
+    fast_tile<TA, TB, BM, BN, BK, WM, WN, STAGES, 2, SYM>(g, i0, j0, kbeg, kend, wsp, g.m, smem);
   else
-    fast_tile<TA, TB, BM, BN, BK, WM, WN, STAGES, 1>(g, i0, j0, kbeg, kend, wsp, g.m, smem);
+    fast_tile<TA, TB, BM, BN, BK, WM, WN, STAGES, 1, SYM>(g, i0, j0, kbeg, kend, wsp, g.m, smem);
 }
 
 template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
@@ -450,10 +472,10 @@ __global__ void __launch_bounds__(FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>::NT)
     fast_tile<TA, TB, BM, BN, BK, WM, WN, STAGES, 1>(g, i0, j0, 0, k, nullptr, 0, smem);
 }
 
-template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES>
+template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, bool SYM = false>
 int launch_fast(cudaStream_t st, const GemmArgs& g, int ksplit, double* ws) {
-  using C = FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES>;
-  auto kern = gemm_fast_kernel<TA, TB, BM, BN, BK, WM, WN, STAGES>;
+  using C = FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES, SYM>;
+  auto kern = gemm_fast_kernel<TA, TB, BM, BN, BK, WM, WN, STAGES, SYM>;
   static int attr_dev = -1;
   int dev;
   PEVD_CUDA(cudaGetDevice(&dev));
@@ -507,15 +529,16 @@ int gemm(cudaStream_t st, const GemmArgs& g, double* ws, int64_t ws_elems) {
   if (g.m <= 0 || g.n <= 0) return OK;
   const int sms = num_sms();
   if (g.amode == A_SYM_LOWER) {
-    // symmetric operand read from its lower triangle: generic 8-byte loader
-    const int64_t tiles = cdiv(g.m, 128);
+    // symmetric operand read from its lower triangle (A W of the band reduction): N is small
+    const int64_t tiles = cdiv(g.m, 128) * cdiv(g.n, 32);
     int ks = 1;
-    if (g.n <= 32 && ws && g.k >= 1024 && tiles < 2 * sms) {
+    if (ws && g.k >= 1024 && tiles < 2 * sms) {
       ks = (int)std::min<int64_t>(cdiv(3 * sms, tiles), g.k / 256);
       while (ks > 1 && (int64_t)ks * g.m * g.n > ws_elems) --ks;
     }
     if (g.n <= 32) {
-      PEVD_TRY((launch_generic<128, 32, 16, 32, 32, 3>(st, g, ks, ks > 1 ? ws : nullptr)));
+      if (g.transB) PEVD_TRY((launch_fast<false, true, 128, 32, 32, 32, 32, 3, true>(st, g, ks, ks > 1 ? ws : nullptr)));
+      else PEVD_TRY((launch_fast<false, false, 128, 32, 32, 32, 32, 3, true>(st, g, ks, ks > 1 ? ws : nullptr)));
       if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
       return OK;
     }

@@ -56,7 +56,7 @@ int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, 
                         double* X, int64_t ldx, int64_t ncols, void* ws);
 // Right-apply the bulge reflectors to the rows of X (nrows x n, col-major ldx):
 // X <- X Q_b  (== (Q_b^T X^T)^T, the reordered BC-Back, backtrans.py:277-310).
-int64_t bc_back_ws_bytes(int64_t nrows);
+int64_t bc_back_ws_bytes(int64_t n, int64_t nrows);
 int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                   double* X, int64_t ldx, int64_t nrows, void* ws);
 // Left-apply Q_b to X (n x ncols): X <- Q_b X (conventional BC-Back).

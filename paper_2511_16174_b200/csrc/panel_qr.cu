@@ -84,10 +84,18 @@ __global__ void __launch_bounds__(QR_THREADS)
       if (vi < KMAX) {
         const int c = vi;
         if (j < k && c >= j && c < k) {
-          for (int lr = grp; lr < nr; lr += 4) {
+          double s1 = 0.0;
+          int lr = grp;
+          for (; lr + 4 < nr; lr += 8) {
+            const int64_t r = r0 + lr;
+            if (r > j) s += P[lr * LDP + j] * P[lr * LDP + c];
+            if (r + 4 > j) s1 += P[(lr + 4) * LDP + j] * P[(lr + 4) * LDP + c];
+          }
+          for (; lr < nr; lr += 4) {
             const int64_t r = r0 + lr;
             if (r > j) s += P[lr * LDP + j] * P[lr * LDP + c];
           }
+          s += s1;
         }
       } else {
         const int q = vi - KMAX;
@@ -121,9 +129,17 @@ __global__ void __launch_bounds__(QR_THREADS)
     // ---- deterministic reduction of all CTA partials (identical in every CTA)
     {
       const int vi = tid % NVAL, grp = tid / NVAL;
-      double s = 0.0;
-      for (unsigned p = grp; p < ncta; p += 4) s += __ldcg(part + (int64_t)p * NVAL + vi);
-      red[grp * NVAL + vi] = s;
+      // independent loads, four accumulators: the L2 round trips overlap instead of chaining
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      unsigned p = grp;
+      for (; p + 12 < ncta; p += 16) {
+        s0 += __ldcg(part + (int64_t)p * NVAL + vi);
+        s1 += __ldcg(part + (int64_t)(p + 4) * NVAL + vi);
+        s2 += __ldcg(part + (int64_t)(p + 8) * NVAL + vi);
+        s3 += __ldcg(part + (int64_t)(p + 12) * NVAL + vi);
+      }
+      for (; p < ncta; p += 4) s0 += __ldcg(part + (int64_t)p * NVAL + vi);
+      red[grp * NVAL + vi] = (s0 + s1) + (s2 + s3);
     }
     __syncthreads();
     if (tid < NVAL) hv[tid] = red[tid] + red[NVAL + tid] + red[2 * NVAL + tid] + red[3 * NVAL + tid];

@@ -63,68 +63,163 @@ int64_t sbr_num_rounds(int64_t n, int b) {
 }
 
 static constexpr int64_t SPLITK_ELEMS = 4 << 20;
+static constexpr int NBB = 4;  // panels per double-blocked trailing update (rank 2 * NBB * b)
 
 int64_t sbr_ws_bytes(int64_t n, int b) {
-  // YZY (n x 3b) + W (n x b) + M, R, coupling tmp (b x b each) + split-K + QR
-  return (n * 3 * b + n * b + 3 * (int64_t)b * b + SPLITK_ELEMS) * 8 + panel_qr_ws_bytes() + 1024;
+  // YZY (n x 3*NBB*b) + W (n x b) + M, R, coupling (b x b) + tZ, tY (NBB*b x b) + split-K + QR
+  const int64_t K = (int64_t)NBB * b;
+  return (n * 3 * K + n * b + 3 * (int64_t)b * b + 2 * K * b + SPLITK_ELEMS) * 8 +
+         panel_qr_ws_bytes() + 1024;
 }
 
+namespace {
+
+struct SbrWs {
+  double *YZY, *Wb, *Mb, *Rb, *Cp, *tZ, *tY, *sk;
+  void* qrws;
+  int64_t ldz;
+};
+
+// the single-panel round (used for the ragged last round, sbr.py:175-182 coupling)
+int sbr_single_round(cudaStream_t st, int64_t n, int b, double* A, int64_t lda, double* bands,
+                     double* Tall, const SbrWs& W, int64_t x) {
+  const int64_t c0 = x * b;
+  const int64_t pw = std::min<int64_t>(b, n - b - c0);
+  const int64_t t0 = c0 + b;
+  const int64_t m = n - t0;
+  const int64_t ldz = W.ldz;
+  double* panel = A + t0 + c0 * lda;
+  double* A22 = A + t0 + t0 * lda;
+  double* Tx = Tall ? Tall + x * (int64_t)b * b : nullptr;
+  double* Yz = W.YZY;
+  double* Zz = W.YZY + pw * ldz;
+  double* Y3 = W.YZY + 2 * pw * ldz;
+  PEVD_TRY(panel_qr(st, m, (int)pw, panel, lda, W.Rb, panel, lda, Yz, ldz, W.Wb, n, Tx, W.qrws));
+  band_cols_from_panel<<<1, 256, 0, st>>>(n, b, c0, (int)pw, A, lda, W.Rb, bands);
+  PEVD_LAUNCH_CHECK();
+  PEVD_CUDA(cudaMemcpy2DAsync(Y3, ldz * 8, Yz, ldz * 8, m * 8, pw, cudaMemcpyDeviceToDevice, st));
+  if (pw < b) {
+    const int64_t nc = b - pw;
+    double* cpl = A + t0 + (c0 + pw) * lda;
+    GemmArgs g1{pw, nc, m, 1.0, 0.0, W.Wb, n, cpl, lda, W.Cp, pw, 1, 0, A_GENERAL, C_ALL};
+    PEVD_TRY(gemm(st, g1, W.sk, SPLITK_ELEMS));
+    GemmArgs g2{m, nc, pw, -1.0, 1.0, Yz, ldz, W.Cp, pw, cpl, lda, 0, 0, A_GENERAL, C_ALL};
+    PEVD_TRY(gemm(st, g2, W.sk, SPLITK_ELEMS));
+  }
+  GemmArgs g_aw{m, pw, m, 1.0, 0.0, A22, lda, W.Wb, n, Zz, ldz, 0, 0, A_SYM_LOWER, C_ALL};
+  PEVD_TRY(gemm(st, g_aw, W.sk, SPLITK_ELEMS));
+  GemmArgs g_m{pw, pw, m, 1.0, 0.0, W.Wb, n, Zz, ldz, W.Mb, pw, 1, 0, A_GENERAL, C_ALL};
+  PEVD_TRY(gemm(st, g_m, W.sk, SPLITK_ELEMS));
+  GemmArgs g_z{m, pw, pw, -0.5, 1.0, Yz, ldz, W.Mb, pw, Zz, ldz, 0, 0, A_GENERAL, C_ALL};
+  PEVD_TRY(gemm(st, g_z, W.sk, SPLITK_ELEMS));
+  GemmArgs g_u{m, m, 2 * pw, -1.0, 1.0, Yz, ldz, Zz, ldz, A22, lda, 0, 1, A_GENERAL, C_LOWER_TILES};
+  PEVD_TRY(gemm(st, g_u, nullptr, 0));
+  return OK;
+}
+
+}  // namespace
+
+// Double-blocked band reduction.  A block of nbl <= NBB full panels (c0, t0 = c0 + b, m0 = n - t0)
+// keeps Y_p and Z_p (block-relative rows [0, m0), zero above their own start) in [Y | Z | Y];
+// for panel i of the block:
+//   1. its columns (rows from the panel's diagonal block down) receive the pending updates of
+//      panels 0..i-1:  C -= Y_p Z_p^T + Z_p Y_p^T            (two skinny GEMMs)
+//   2. panel QR; its band columns are now final
+//   3. AW_i = A_blockstart[t_i:, t_i:] W_i  - Y_p (Z_p^T W_i) - Z_p (Y_p^T W_i)
+//   4. Z_i = AW_i - 1/2 Y_i (W_i^T AW_i)
+// then one rank-2*nbl*b update of the remaining trailing matrix (lower tiles):
+//   A[t0+(nbl-1)b:, same] -= [Y Z][Z Y]^T.
 int sbr_reduce(cudaStream_t st, int64_t n, int b, double* A, int64_t lda, double* bands_ref,
                double* Tall, void* ws) {
   if (b < 1 || n < 2 || b >= n) {
     set_error("sbr_reduce: need 1 <= b < n (n=%lld, b=%d)", (long long)n, b);
     return ERR_VALUE;
   }
-  double* YZY = (double*)ws;
-  const int64_t ldz = n;
-  double* Wb = YZY + n * 3 * b;
-  double* Mb = Wb + n * b;
-  double* Rb = Mb + (int64_t)b * b;
-  double* Cp = Rb + (int64_t)b * b;
-  double* sk = Cp + (int64_t)b * b;
-  void* qrws = (void*)(sk + SPLITK_ELEMS);
-
-  int64_t x = 0;
+  const int64_t Kmax = (int64_t)NBB * b;
+  SbrWs W;
+  W.ldz = n;
+  W.YZY = (double*)ws;
+  W.Wb = W.YZY + n * 3 * Kmax;
+  W.Mb = W.Wb + n * b;
+  W.Rb = W.Mb + (int64_t)b * b;
+  W.Cp = W.Rb + (int64_t)b * b;
+  W.tZ = W.Cp + (int64_t)b * b;
+  W.tY = W.tZ + Kmax * b;
+  W.sk = W.tY + Kmax * b;
+  W.qrws = (void*)(W.sk + SPLITK_ELEMS);
+  const int64_t ldz = W.ldz;
+  const int64_t R = sbr_num_rounds(n, b);
   int64_t c_end = 0;
-  for (int64_t c0 = 0; c0 < n - b; c0 += b, ++x) {
-    const int64_t pw = std::min<int64_t>(b, n - b - c0);
-    const int64_t t0 = c0 + b;
-    const int64_t m = n - t0;
-    double* panel = A + t0 + c0 * lda;
-    double* A22 = A + t0 + t0 * lda;
-    double* Tx = Tall ? Tall + x * (int64_t)b * b : nullptr;
-    double* Yz = YZY;  // [Y | Z | Y], ld = n
-    double* Zz = YZY + pw * ldz;
-    double* Y3 = YZY + 2 * pw * ldz;
-    // 1. panel QR (Y overwrites the panel in A; R kept aside for the band)
-    PEVD_TRY(panel_qr(st, m, (int)pw, panel, lda, Rb, panel, lda, Yz, ldz, Wb, n, Tx, qrws));
-    // 2. band columns of this panel are final
-    band_cols_from_panel<<<1, 256, 0, st>>>(n, b, c0, (int)pw, A, lda, Rb, bands_ref);
-    PEVD_LAUNCH_CHECK();
-    PEVD_CUDA(cudaMemcpy2DAsync(Y3, ldz * 8, Yz, ldz * 8, m * 8, pw, cudaMemcpyDeviceToDevice, st));
-    // ragged final round: coupling columns [c0+pw, t0) rows [t0, n) get Q^T from the left
-    if (pw < b) {
-      const int64_t nc = b - pw;
-      double* cpl = A + t0 + (c0 + pw) * lda;
-      GemmArgs g1{pw, nc, m, 1.0, 0.0, Wb, n, cpl, lda, Cp, pw, 1, 0, A_GENERAL, C_ALL};
-      PEVD_TRY(gemm(st, g1, sk, SPLITK_ELEMS));
-      GemmArgs g2{m, nc, pw, -1.0, 1.0, Yz, ldz, Cp, pw, cpl, lda, 0, 0, A_GENERAL, C_ALL};
-      PEVD_TRY(gemm(st, g2, sk, SPLITK_ELEMS));
+  for (int64_t x = 0; x < R;) {
+    const int64_t c0 = x * b;
+    const int64_t pw0 = std::min<int64_t>(b, n - b - c0);
+    if (pw0 < b) {  // ragged last round
+      PEVD_TRY(sbr_single_round(st, n, b, A, lda, bands_ref, Tall, W, x));
+      c_end = c0 + pw0;
+      ++x;
+      continue;
     }
-    // 3. AW = A22 W  (symmetric, lower storage) -> Z slot
-    GemmArgs g_aw{m, pw, m, 1.0, 0.0, A22, lda, Wb, n, Zz, ldz, 0, 0, A_SYM_LOWER, C_ALL};
-    PEVD_TRY(gemm(st, g_aw, sk, SPLITK_ELEMS));
-    // 4. M = W^T AW
-    GemmArgs g_m{pw, pw, m, 1.0, 0.0, Wb, n, Zz, ldz, Mb, pw, 1, 0, A_GENERAL, C_ALL};
-    PEVD_TRY(gemm(st, g_m, sk, SPLITK_ELEMS));
-    // 5. Z = AW - 1/2 Y M
-    GemmArgs g_z{m, pw, pw, -0.5, 1.0, Yz, ldz, Mb, pw, Zz, ldz, 0, 0, A_GENERAL, C_ALL};
-    PEVD_TRY(gemm(st, g_z, sk, SPLITK_ELEMS));
-    // 6. A22 -= [Y Z] [Z Y]^T   (lower tiles)
-    GemmArgs g_u{m, m, 2 * pw, -1.0, 1.0, Yz, ldz, Zz, ldz, A22, lda, 0, 1, A_GENERAL,
+    int nbl = 1;
+    while (nbl < NBB && x + nbl < R && (n - b - (x + nbl) * b) >= b) ++nbl;
+    const int64_t t0 = c0 + b, m0 = n - t0;
+    const int64_t K = (int64_t)nbl * b;
+    double* Yb = W.YZY;            // [0, K)
+    double* Zb = W.YZY + K * ldz;  // [K, 2K)
+    double* Y3 = W.YZY + 2 * K * ldz;
+    // rows above each panel's start must read as zero
+    PEVD_CUDA(cudaMemset2DAsync(W.YZY, ldz * 8, 0, (size_t)K * 8, (size_t)(3 * K), st));
+    for (int i = 0; i < nbl; ++i) {
+      const int64_t ci = c0 + (int64_t)i * b, ti = t0 + (int64_t)i * b, mi = n - ti;
+      const int64_t ri = (int64_t)i * b;
+      if (i >= 1) {
+        // 1. pending updates on the panel columns, rows [ci, n) = block rows [ri - b, m0)
+        double* Cpan = A + ci + ci * lda;
+        const int64_t mc = mi + b;
+        GemmArgs g1{mc, b, ri, -1.0, 1.0, Yb + (ri - b), ldz, Zb + (ri - b), ldz, Cpan, lda,
+                    0, 1, A_GENERAL, C_ALL};
+        PEVD_TRY(gemm(st, g1, W.sk, SPLITK_ELEMS));
+        GemmArgs g2{mc, b, ri, -1.0, 1.0, Zb + (ri - b), ldz, Yb + (ri - b), ldz, Cpan, lda,
+                    0, 1, A_GENERAL, C_ALL};
+        PEVD_TRY(gemm(st, g2, W.sk, SPLITK_ELEMS));
+      }
+      // 2. panel QR (explicit Y into the staircase and into the block buffer)
+      double* panel = A + ti + ci * lda;
+      double* Tx = Tall ? Tall + (x + i) * (int64_t)b * b : nullptr;
+      double* Yi = Yb + ri + ri * ldz;
+      double* Zi = Zb + ri + ri * ldz;
+      PEVD_TRY(panel_qr(st, mi, b, panel, lda, W.Rb, panel, lda, Yi, ldz, W.Wb, n, Tx, W.qrws));
+      band_cols_from_panel<<<1, 256, 0, st>>>(n, b, ci, b, A, lda, W.Rb, bands_ref);
+      PEVD_LAUNCH_CHECK();
+      // 3. AW_i into the Z slot
+      GemmArgs g_aw{mi, b, mi, 1.0, 0.0, A + ti + ti * lda, lda, W.Wb, n, Zi, ldz, 0, 0,
+                    A_SYM_LOWER, C_ALL};
+      PEVD_TRY(gemm(st, g_aw, W.sk, SPLITK_ELEMS));
+      if (i >= 1) {
+        GemmArgs gz{ri, b, mi, 1.0, 0.0, Zb + ri, ldz, W.Wb, n, W.tZ, ri, 1, 0, A_GENERAL, C_ALL};
+        PEVD_TRY(gemm(st, gz, W.sk, SPLITK_ELEMS));
+        GemmArgs gy{ri, b, mi, 1.0, 0.0, Yb + ri, ldz, W.Wb, n, W.tY, ri, 1, 0, A_GENERAL, C_ALL};
+        PEVD_TRY(gemm(st, gy, W.sk, SPLITK_ELEMS));
+        GemmArgs c1{mi, b, ri, -1.0, 1.0, Yb + ri, ldz, W.tZ, ri, Zi, ldz, 0, 0, A_GENERAL, C_ALL};
+        PEVD_TRY(gemm(st, c1, W.sk, SPLITK_ELEMS));
+        GemmArgs c2{mi, b, ri, -1.0, 1.0, Zb + ri, ldz, W.tY, ri, Zi, ldz, 0, 0, A_GENERAL, C_ALL};
+        PEVD_TRY(gemm(st, c2, W.sk, SPLITK_ELEMS));
+      }
+      // 4. Z_i = AW_i - 1/2 Y_i (W_i^T AW_i)
+      GemmArgs g_m{b, b, mi, 1.0, 0.0, W.Wb, n, Zi, ldz, W.Mb, b, 1, 0, A_GENERAL, C_ALL};
+      PEVD_TRY(gemm(st, g_m, W.sk, SPLITK_ELEMS));
+      GemmArgs g_z{mi, b, b, -0.5, 1.0, Yi, ldz, W.Mb, b, Zi, ldz, 0, 0, A_GENERAL, C_ALL};
+      PEVD_TRY(gemm(st, g_z, W.sk, SPLITK_ELEMS));
+    }
+    // copy of Y for the [Z Y] operand, then the block's rank-2K trailing update (lower tiles)
+    PEVD_CUDA(cudaMemcpy2DAsync(Y3, ldz * 8, Yb, ldz * 8, m0 * 8, K, cudaMemcpyDeviceToDevice, st));
+    const int64_t ru = (int64_t)(nbl - 1) * b;
+    const int64_t mu = m0 - ru;
+    double* Cu = A + (t0 + ru) + (t0 + ru) * lda;
+    GemmArgs g_u{mu, mu, 2 * K, -1.0, 1.0, Yb + ru, ldz, Zb + ru, ldz, Cu, lda, 0, 1, A_GENERAL,
                  C_LOWER_TILES};
     PEVD_TRY(gemm(st, g_u, nullptr, 0));
-    c_end = c0 + pw;
+    c_end = c0 + K;
+    x += nbl;
   }
   {
     const int64_t total = (int64_t)(b + 1) * (n - c_end);

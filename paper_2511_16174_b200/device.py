@@ -195,7 +195,7 @@ def bc_back_right(n, b, tau, V, x):
     dt = torch.from_numpy(np.ascontiguousarray(tau)).cuda()
     dv = torch.from_numpy(np.ascontiguousarray(V).reshape(-1)).cuda()
     dx = to_dev(x)
-    ws = workspace(L.pevd_bc_back_workspace_bytes(x.shape[0]))
+    ws = workspace(L.pevd_bc_back_workspace_bytes(n, x.shape[0]))
     rc = L.pevd_bc_back_right(n, b, _p(dt), _p(dv), vld, _p(dx), x.shape[0], x.shape[0], _p(ws),
                               _stream())
     _lib.check(rc, "bc_back_right")

@@ -71,7 +71,7 @@ def main():
         b = 32
         tau, V, vld, _ = reflectors(n, b)
         X = torch.randn((n, n), dtype=torch.float64, device="cuda")
-        ws = torch.empty(L.pevd_bc_back_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+        ws = torch.empty(L.pevd_bc_back_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
         ms, ts = timed(lambda: _lib.check(L.pevd_bc_back_right(n, b, ptr(tau), ptr(V), vld, ptr(X),
                                                                n, n, ptr(ws), stream()), "bcback"))
         nref = L.pevd_bc_num_reflectors(n, b)
