@@ -81,6 +81,12 @@ int pevd_dgemm(int transA, int transB, int64_t m, int64_t n, int64_t k, double a
                const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
                int64_t ldc, void* workspace, int64_t workspace_bytes, void* stream);
 
+/* C = alpha A B + beta C with A symmetric (m x m) read from its lower triangle only
+ * (the A W product of form_z, sbr.py:119-130). */
+int pevd_dsymm_lower(int64_t m, int64_t n, double alpha, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                     void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Householder panel QR, sbr.py:69-116.  P (m x k, ldp) read; R (k x k), Y (m x k, ldy),
  * W (m x k, ldw), T (k x k) written (any output may be NULL except Y).  k <= 32. */
 int64_t pevd_panel_qr_workspace_bytes(void);

@@ -38,6 +38,8 @@ SIGNATURES = {
                           ctypes.POINTER(PevdStats)]),
     "pevd_dgemm": (_int, [_int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp,
                           _i64, _vp, _i64, _vp]),
+    "pevd_dsymm_lower": (_int, [_i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp, _i64,
+                                _vp]),
     "pevd_panel_qr_workspace_bytes": (_i64, []),
     "pevd_panel_qr": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp]),
     "pevd_sbr_workspace_bytes": (_i64, [_i64, _int]),

@@ -317,6 +317,13 @@ int pevd_dgemm(int transA, int transB, int64_t m, int64_t n, int64_t k, double a
   return gemm((cudaStream_t)stream, g, (double*)workspace, workspace_bytes / 8);
 }
 
+int pevd_dsymm_lower(int64_t m, int64_t n, double alpha, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                     void* workspace, int64_t workspace_bytes, void* stream) {
+  GemmArgs g{m, n, m, alpha, beta, A, lda, B, ldb, C, ldc, 0, 0, A_SYM_LOWER, C_ALL};
+  return gemm((cudaStream_t)stream, g, (double*)workspace, workspace_bytes / 8);
+}
+
 int64_t pevd_panel_qr_workspace_bytes(void) { return panel_qr_ws_bytes(); }
 
 int pevd_panel_qr(int64_t m, int k, const double* P, int64_t ldp, double* R, double* Y,

@@ -67,16 +67,14 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
 
   for (int64_t gi = wglob; gi < n - 2; gi += total_warps) {
     for (int64_t j = 0; gi + 1 + j * b <= n - 2; ++j) {
-      // ---- wait for the predecessor sweep to complete step j+2
+      // ---- wait for the predecessor sweep to complete step j+2.  Polling is a relaxed L2 load
+      //      (an acquire would invalidate L1 on every poll); every band access of this kernel
+      //      goes through L2 (ld.cg / st), and the producer orders its stores before the flag
+      //      with a gpu-scope fence, so the data the flag covers is what the L2 returns.
       if (gi > 0) {
         if (lane == 0) {
           const int need = (int)(j + 3);
-          if (ld_acquire(prog + gi - 1) < need) {
-            unsigned ns = 32;
-            while (ld_acquire(prog + gi - 1) < need) {
-              __nanosleep(ns);  // yield issue slots to the working warps
-              if (ns < 256) ns <<= 1;
-            }
+          while (ld_relaxed(prog + gi - 1) < need) {
           }
         }
         __syncwarp();
@@ -195,14 +193,14 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
       // ---- publish progress
       __syncwarp();
       if (lane == 0) {
-        __threadfence();
-        st_release(prog + gi, (int)(j + 1));
+        __threadfence();  // orders the warp's band stores (after __syncwarp) before the flag
+        st_relaxed(prog + gi, (int)(j + 1));
       }
     }
     __syncwarp();
     if (lane == 0) {
       __threadfence();
-      st_release(prog + gi, DONE);
+      st_relaxed(prog + gi, DONE);
     }
   }
 }

@@ -537,8 +537,9 @@ int gemm(cudaStream_t st, const GemmArgs& g, double* ws, int64_t ws_elems) {
       while (ks > 1 && (int64_t)ks * g.m * g.n > ws_elems) --ks;
     }
     if (g.n <= 32) {
-      if (g.transB) PEVD_TRY((launch_fast<false, true, 128, 32, 32, 32, 32, 3, true>(st, g, ks, ks > 1 ? ws : nullptr)));
-      else PEVD_TRY((launch_fast<false, false, 128, 32, 32, 32, 32, 3, true>(st, g, ks, ks > 1 ? ws : nullptr)));
+      // 8 warps of 16 x 32, BK = 16, 4 stages: ~100 KB of shared memory -> 2 CTAs (16 warps)/SM
+      if (g.transB) PEVD_TRY((launch_fast<false, true, 128, 32, 16, 16, 32, 4, true>(st, g, ks, ks > 1 ? ws : nullptr)));
+      else PEVD_TRY((launch_fast<false, false, 128, 32, 16, 16, 32, 4, true>(st, g, ks, ks > 1 ? ws : nullptr)));
       if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
       return OK;
     }
@@ -552,7 +553,7 @@ int gemm(cudaStream_t st, const GemmArgs& g, double* ws, int64_t ws_elems) {
       ks = (int)std::min<int64_t>(cdiv(3 * sms, tiles), g.k / 256);
       while (ks > 1 && (int64_t)ks * g.m * g.n > ws_elems) --ks;
     }
-    PEVD_TRY((launch_fast_t<128, 32, 32, 32, 32, 3>(st, g, ks, ks > 1 ? ws : nullptr)));
+    PEVD_TRY((launch_fast_t<128, 32, 16, 16, 32, 4>(st, g, ks, ks > 1 ? ws : nullptr)));
     if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
     return OK;
   }
@@ -564,7 +565,7 @@ int gemm(cudaStream_t st, const GemmArgs& g, double* ws, int64_t ws_elems) {
     ks = (int)std::min<int64_t>(cdiv(2 * sms, tiles64), g.k / 128);
     while (ks > 1 && (int64_t)ks * g.m * g.n > ws_elems) --ks;
   }
-  PEVD_TRY((launch_fast_t<64, 64, 32, 32, 32, 3>(st, g, ks, ks > 1 ? ws : nullptr)));
+  PEVD_TRY((launch_fast_t<64, 64, 16, 32, 32, 4>(st, g, ks, ks > 1 ? ws : nullptr)));
   if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
   return OK;
 }
@@ -574,7 +575,7 @@ int gemm_grouped(cudaStream_t st, const GemmArgs* d_args, int count, int64_t max
   if (count <= 0 || max_m <= 0 || max_n <= 0) return OK;
   if (max_m * max_n >= (int64_t)128 * 128 * 64)
     return launch_fast_grouped<128, 128, 32, 64, 32, 3>(st, d_args, count, max_m, max_n);
-  return launch_fast_grouped<64, 64, 32, 32, 32, 3>(st, d_args, count, max_m, max_n);
+  return launch_fast_grouped<64, 64, 16, 32, 32, 4>(st, d_args, count, max_m, max_n);
 }
 
 }  // namespace pevd
