@@ -112,6 +112,18 @@ def run(a, cfg: PipelineConfig):
     n = int(dense.shape[0])
     partition(n, cfg.workers)  # raises ValueError for workers > n (schedule.py:26-27)
     b = min(cfg.b, n - 1) if n > 1 else 0
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1 and n > 2:
+        # one process per GPU: the blockwise protocol (distributed.py)
+        from .distributed import run_distributed
+        from .core import FlopCounter as _FC
+        res, events, ledger, _ = run_distributed(dense, cfg)
+        if cfg.trace_path:
+            log = TraceLog()
+            for ev in events:
+                log.add(ev.worker, ev.stage, ev.block, ev.t_start, ev.t_end, ev.words)
+            log.to_ndjson(cfg.trace_path)
+        return res, events, ledger, _macs(n, b, cfg)
     from . import device  # imports torch lazily; fails loudly without CUDA / libpevd.so
     t0 = time.perf_counter_ns()
     try:
