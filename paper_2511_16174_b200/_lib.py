@@ -54,7 +54,7 @@ SIGNATURES = {
     "pevd_sbr_back_left": (_int, [_i64, _int, _vp, _vp, _vp, _i64, _i64, _vp, _vp]),
     "pevd_bc_back_workspace_bytes": (_i64, [_i64, _i64]),
     "pevd_bc_back_right": (_int, [_i64, _int, _vp, _vp, _int, _vp, _i64, _i64, _vp, _vp]),
-    "pevd_bc_back_left": (_int, [_i64, _int, _vp, _vp, _int, _vp, _i64, _i64, _vp]),
+    "pevd_bc_back_left": (_int, [_i64, _int, _vp, _vp, _int, _vp, _i64, _i64, _vp, _vp]),
 }
 
 _lib = None

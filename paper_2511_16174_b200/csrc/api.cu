@@ -210,7 +210,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     if (want_vectors) {
       if (order == PEVD_ORDER_CONVENTIONAL) {
         cudaEventRecord(ev[4].a, sm);
-        if ((rc = bc_back_left(sm, n, b, L.tau, L.V, L.vld, L.Qd, n, n))) break;
+        if ((rc = bc_back_left(sm, n, b, L.tau, L.V, L.vld, L.Qd, n, n, L.ws_bcb))) break;
         cudaEventRecord(ev[4].b, sm);
         cudaEventRecord(ev[3].a, sm);
         if ((rc = sbr_back_apply_left(sm, n, b, A, L.Tall, L.Qd, n, n, L.ws_back))) break;
@@ -381,8 +381,8 @@ int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int
 }
 
 int pevd_bc_back_left(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
-                      int64_t ldx, int64_t ncols, void* stream) {
-  return bc_back_left((cudaStream_t)stream, n, b, tau, V, vld, X, ldx, ncols);
+                      int64_t ldx, int64_t ncols, void* workspace, void* stream) {
+  return bc_back_left((cudaStream_t)stream, n, b, tau, V, vld, X, ldx, ncols, workspace);
 }
 
 }  // extern "C"

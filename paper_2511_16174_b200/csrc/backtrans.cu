@@ -420,15 +420,17 @@ struct WySmem {
 
 // -T of every block of 8 consecutive sweeps at every chase step.  Block (j, q) covers sweeps
 // 8q..8q+7 and lives at Tf + 64 * (tofs[j] + q).
+template <bool BACKWARD>
 __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
                                   const double* __restrict__ V, int vld,
                                   const int64_t* __restrict__ tofs, int64_t jcount,
                                   double* __restrict__ Tf) {
+  // forward:  H_0 H_1 ... H_7 = I - V T V^T, T upper (LAPACK larft 'F')
+  // backward: H_7 H_6 ... H_0 = I - V T V^T, T lower (larft 'B')
   constexpr int B = 32;
   const int64_t total = tofs[jcount];
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
        id += (int64_t)gridDim.x * blockDim.x) {
-    // locate j by binary search on tofs
     int64_t lo = 0, hi = jcount;
     while (hi - lo > 1) {
       const int64_t mid = (lo + hi) >> 1;
@@ -446,33 +448,52 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
       tv[s] = ok ? tau[off + i] : 0.0;
       v[s] = V + (ok ? (off + i) : off) * vld;
     }
+    // Gram entries g[u][t] = v_u^T v_t for u < t (v_u starts t - u rows above v_t)
+    double G[8][8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        double acc = 0.0;
+        if (u < t && tv[u] != 0.0 && tv[t] != 0.0) {
+          const int d = t - u;
+          for (int r = 0; r < B - d; ++r) acc = fma(v[u][r + d], v[t][r], acc);
+        }
+        G[u][t] = acc;
+      }
     double T[8][8];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int s = 0; s < 8; ++s)
 #pragma unroll
-      for (int s = 0; s < 8; ++s) T[s][t] = 0.0;
-      if (tv[t] == 0.0) continue;
-      T[t][t] = tv[t];
-      // g_u = v_u^T v_t for u < t (v_u starts t - u rows above v_t)
-      double g[8];
+      for (int t = 0; t < 8; ++t) T[s][t] = 0.0;
+    if (!BACKWARD) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        g[u] = 0.0;
-        if (u < t && tv[u] != 0.0) {
-          const int d = t - u;
-          double acc = 0.0;
-          for (int r = 0; r < B - d; ++r) acc = fma(v[u][r + d], v[t][r], acc);
-          g[u] = acc;
+      for (int t = 0; t < 8; ++t) {
+        T[t][t] = tv[t];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          if (s < t) {
+            double acc = 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (u >= s && u < t) acc = fma(T[s][u], G[u][t], acc);
+            T[s][t] = -tv[t] * acc;
+          }
         }
       }
+    } else {
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        if (s < t) {
-          double acc = 0.0;
+      for (int i = 7; i >= 0; --i) {
+        T[i][i] = tv[i];
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (u >= s && u < t) acc = fma(T[s][u], g[u], acc);
-          T[s][t] = -tv[t] * acc;
+        for (int s = 0; s < 8; ++s) {
+          if (s > i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (u > i && u <= s) acc = fma(T[s][u], G[i][u], acc);  // v_u^T v_i = G[i][u]
+            T[s][i] = -tv[i] * acc;
+          }
         }
       }
     }
@@ -484,6 +505,13 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
   }
 }
 
+// LEFT = false: X <- X Q_b on the rows of X (element (row, col) at X[row + col*ldx]), reflectors
+//   in creation-compatible grouped order (groups ascending, steps bottom-to-top, sweeps
+//   ascending), forward T.
+// LEFT = true:  X <- Q_b X, done as Y <- Y Q_b^T on the rows of Y = X^T (element (row, col) at
+//   X[row*ldx + col]): groups descending, steps top-to-bottom, sweeps descending, backward T
+//   (the conventional grouped order of backtrans.py:232-235).
+template <bool LEFT>
 __global__ void __launch_bounds__(WY_THREADS, 2)
     bc_back_wy_kernel(int64_t n, const double* __restrict__ V, int vld,
                       const double* __restrict__ Tf, const int64_t* __restrict__ tofs, double* X,
@@ -532,23 +560,27 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
     const int64_t u = S.unit;
     __syncthreads();
     if (u >= nunits) break;
-    const int64_t k = u / nrb;
+    const int64_t ngroups = (nsw + Q4_SG - 1) / Q4_SG;
+    const int64_t seq = u / nrb;                       // groups this row block has done before
+    const int64_t k = LEFT ? ngroups - 1 - seq : seq;
     const int rb = (int)(u % nrb);
-    if (tid == 0 && ld_acquire(progress + rb) < (int)k) {
+    if (tid == 0 && ld_acquire(progress + rb) < (int)seq) {
       unsigned ns = 64;
-      while (ld_acquire(progress + rb) < (int)k) {
+      while (ld_acquire(progress + rb) < (int)seq) {
         __nanosleep(ns);
         if (ns < 1024) ns <<= 1;
       }
     }
     const int64_t row = (int64_t)rb * WY_ROWS + warp * 8 + r8;
     const bool active = row < nrows;
-    double* x = X + (active ? row : 0);
+    const int64_t cs = LEFT ? 1 : ldx;                 // column stride of a row's elements
+    double* x = X + (active ? (LEFT ? row * ldx : row) : 0);
     const int64_t i0 = k * Q4_SG;
     const int64_t jmax = (n - 3 - i0) / B;
-    int64_t ws = i0 + 1 + jmax * B;
+    const int64_t jfirst = LEFT ? 0 : jmax;
+    int64_t ws = i0 + 1 + jfirst * B;
     double pf[WY_PF];
-    fetch(i0, jmax, pf);
+    fetch(i0, jfirst, pf);
     __syncthreads();  // progress acquired by tid 0 before anyone reads X
     double w[12][2];
 #pragma unroll
@@ -556,23 +588,29 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t col = ws + 8 * c + 2 * qd + h;
-        w[c][h] = (active && col < n) ? __ldcg(x + col * ldx) : 0.0;
+        w[c][h] = (active && col < n) ? __ldcg(x + col * cs) : 0.0;
       }
     int buf = 0;
     stage(buf, pf);
     __syncthreads();
-    for (int64_t j = jmax; j >= 0; --j) {
-      // prefetch the next step: its new window columns [ws - 32, ws) and its V / -T
+    for (int64_t jj = 0; jj <= jmax; ++jj) {
+      const int64_t j = LEFT ? jj : jmax - jj;
+      const bool more = jj < jmax;
+      // prefetch the next step: its new window columns and its V / -T
       double nx[4][2];
+      const int64_t nbase = LEFT ? ws + 3 * B : ws - B;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-          nx[c][h] = (j > 0 && active) ? __ldcg(x + (ws - B + 8 * c + 2 * qd + h) * ldx) : 0.0;
-      if (j > 0) fetch(i0, j - 1, pf);
+        for (int h = 0; h < 2; ++h) {
+          const int64_t col = nbase + 8 * c + 2 * qd + h;
+          nx[c][h] = (more && active && col < n) ? __ldcg(x + col * cs) : 0.0;
+        }
+      if (more) fetch(i0, LEFT ? j + 1 : j - 1, pf);
       // ---- apply the 8 blocks of this step
 #pragma unroll
-      for (int blk = 0; blk < Q4_SG / 8; ++blk) {
+      for (int bb = 0; bb < Q4_SG / 8; ++bb) {
+        const int blk = LEFT ? Q4_SG / 8 - 1 - bb : bb;
         const int tb = blk * 8;
         double p0 = 0.0, p1 = 0.0, e0 = 0.0, e1 = 0.0;
         const double* vrow = &S.vp[buf][tb + r8][8 + 2 * qd - r8];
@@ -594,42 +632,69 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
           dmma884(w[blk + cc][0], w[blk + cc][1], q1, vb);
         }
       }
-      // ---- slide: tiles 8..11 are final for this group; shift by b = 32 (4 tiles)
+      // ---- slide by b = 32 (4 tiles): the trailing 4 tiles (right) / leading 4 tiles (left)
+      //      are final for this group
+      if (!LEFT) {
 #pragma unroll
-      for (int c = 8; c < 12; ++c)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t col = ws + 8 * c + 2 * qd + h;
-          if (active && col < n) x[col * ldx] = w[c][h];
-        }
-      if (j > 0) {
-#pragma unroll
-        for (int c = 11; c >= 4; --c) {
-          w[c][0] = w[c - 4][0];
-          w[c][1] = w[c - 4][1];
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          w[c][0] = nx[c][0];
-          w[c][1] = nx[c][1];
-        }
-        ws -= B;
-        stage(buf ^ 1, pf);  // the other buffer: nobody reads it during this step
-      } else {
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
+        for (int c = 8; c < 12; ++c)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int64_t col = ws + 8 * c + 2 * qd + h;
-            if (active && col < n) x[col * ldx] = w[c][h];
+            if (active && col < n) x[col * cs] = w[c][h];
           }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t col = ws + 8 * c + 2 * qd + h;
+            if (active && col < n) x[col * cs] = w[c][h];
+          }
+      }
+      if (more) {
+        if (!LEFT) {
+#pragma unroll
+          for (int c = 11; c >= 4; --c) {
+            w[c][0] = w[c - 4][0];
+            w[c][1] = w[c - 4][1];
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            w[c][0] = nx[c][0];
+            w[c][1] = nx[c][1];
+          }
+          ws -= B;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            w[c][0] = w[c + 4][0];
+            w[c][1] = w[c + 4][1];
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            w[8 + c][0] = nx[c][0];
+            w[8 + c][1] = nx[c][1];
+          }
+          ws += B;
+        }
+        stage(buf ^ 1, pf);  // the other buffer: nobody reads it during this step
+      } else {
+#pragma unroll
+        for (int c = 0; c < 12; ++c) {
+          if (LEFT ? c < 4 : c >= 8) continue;  // already stored above
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t col = ws + 8 * c + 2 * qd + h;
+            if (active && col < n) x[col * cs] = w[c][h];
+          }
+        }
       }
       buf ^= 1;
       __syncthreads();
     }
     if (tid == 0) {
       __threadfence();
-      st_release(progress + rb, (int)(k + 1));
+      st_release(progress + rb, (int)(seq + 1));
     }
   }
 }
@@ -750,11 +815,11 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
       for (int64_t j = 0; j < jcount; ++j) h[j + 1] = h[j] + cdiv(n - 2 - j * 32, 8);
       PEVD_CUDA(cudaMemcpyAsync(tofs, h.data(), (jcount + 1) * 8, cudaMemcpyHostToDevice, st));
       PEVD_CUDA(cudaStreamSynchronize(st));  // h is pageable and goes out of scope
-      wy_tfactor_kernel<<<(unsigned)std::min<int64_t>(cdiv(h[jcount], 128), 16384), 128, 0, st>>>(
+      wy_tfactor_kernel<false><<<(unsigned)std::min<int64_t>(cdiv(h[jcount], 128), 16384), 128, 0, st>>>(
           n, tau, V, vld, tofs, jcount, Tf);
       PEVD_LAUNCH_CHECK();
     }
-    const void* kfn = wy ? (const void*)bc_back_wy_kernel : (const void*)bc_back_q4_kernel;
+    const void* kfn = wy ? (const void*)bc_back_wy_kernel<false> : (const void*)bc_back_q4_kernel;
     const size_t smem = wy ? sizeof(WySmem) : sizeof(Q4Smem);
     const int nthr = wy ? WY_THREADS : Q4_THREADS;
     static int attr_dev[2] = {-1, -1};
@@ -772,8 +837,9 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
     }
     const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
     if (wy)
-      bc_back_wy_kernel<<<(unsigned)grid, nthr, smem, st>>>(n, V, vld, Tf, tofs, X, ldx, nrows,
-                                                            counter, progress, nunits, nrb);
+      bc_back_wy_kernel<false><<<(unsigned)grid, nthr, smem, st>>>(n, V, vld, Tf, tofs, X, ldx,
+                                                                   nrows, counter, progress,
+                                                                   nunits, nrb);
     else
       bc_back_q4_kernel<<<(unsigned)grid, nthr, smem, st>>>(n, tau, V, vld, X, ldx, nrows, counter,
                                                             progress, nunits, nrb);
@@ -798,8 +864,50 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
 }
 
 int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
-                 double* X, int64_t ldx, int64_t ncols) {
+                 double* X, int64_t ldx, int64_t ncols, void* ws) {
   if (n < 3 || ncols <= 0 || b < 2) return OK;
+  if (b == 32 && vld >= 32 && ws) {
+    // X <- Q_b X  ==  (X^T Q_b^T)^T: the DMMA compact-WY kernel in reverse order on the rows of
+    // X^T (= the columns of X, contiguous), backward T factors
+    const int nrb = (int)cdiv(ncols, WY_ROWS);
+    const int64_t ngroups = cdiv(n - 2, Q4_SG);
+    const int64_t nunits = ngroups * nrb;
+    int* counter = (int*)ws;
+    int* progress = counter + 32;
+    const int64_t jcount = (n - 3) / 32 + 1;
+    int64_t* tofs = (int64_t*)((char*)ws + ((ncols / 32 + 64) * 4 + 255) / 256 * 256);
+    double* Tf = (double*)(tofs + jcount + 2);
+    PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
+    std::vector<int64_t> h(jcount + 1);
+    h[0] = 0;
+    for (int64_t j = 0; j < jcount; ++j) h[j + 1] = h[j] + cdiv(n - 2 - j * 32, 8);
+    PEVD_CUDA(cudaMemcpyAsync(tofs, h.data(), (jcount + 1) * 8, cudaMemcpyHostToDevice, st));
+    PEVD_CUDA(cudaStreamSynchronize(st));
+    wy_tfactor_kernel<true><<<(unsigned)std::min<int64_t>(cdiv(h[jcount], 128), 16384), 128, 0, st>>>(
+        n, tau, V, vld, tofs, jcount, Tf);
+    PEVD_LAUNCH_CHECK();
+    const size_t smem = sizeof(WySmem);
+    static int attr_dev = -1;
+    int dev;
+    PEVD_CUDA(cudaGetDevice(&dev));
+    if (attr_dev != dev) {
+      PEVD_CUDA(cudaFuncSetAttribute(bc_back_wy_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_dev = dev;
+    }
+    int per_sm = 0;
+    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bc_back_wy_kernel<true>,
+                                                            WY_THREADS, smem));
+    if (per_sm < 1) {
+      set_error("bc_back_left: persistent kernel cannot be resident");
+      return ERR_CUDA;
+    }
+    const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
+    bc_back_wy_kernel<true><<<(unsigned)grid, WY_THREADS, smem, st>>>(
+        n, V, vld, Tf, tofs, X, ldx, ncols, counter, progress, nunits, nrb);
+    PEVD_LAUNCH_CHECK();
+    return OK;
+  }
   bc_back_left_generic<<<(unsigned)cdiv(ncols, 128), 128, 0, st>>>(n, b, tau, V, vld, X, ldx,
                                                                    ncols);
   PEVD_LAUNCH_CHECK();

@@ -330,10 +330,30 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
   double* As = smem;
   double* Bs = smem + STAGES * C::A_STAGE;
   double acc[C::MI][C::NI][2];
+  // beta != 0: start the accumulators at (beta/alpha) C, so the epilogue is a plain store and the
+  // C reads overlap the pipeline prologue instead of trailing the (short-K) main loop
+  const bool preload = (ws_out == nullptr) && g.beta != 0.0 && g.alpha != 0.0;
+  {
+    const double sc = preload ? g.beta / g.alpha : 0.0;
+    const int r_in = lane >> 2, c_in = 2 * (lane & 3);
 #pragma unroll
-  for (int a = 0; a < C::MI; ++a)
+    for (int a = 0; a < C::MI; ++a) {
+      const int64_t gi = i0 + wm * WM + a * 8 + r_in;
 #pragma unroll
-    for (int b = 0; b < C::NI; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      for (int b = 0; b < C::NI; ++b) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double v = 0.0;
+          const int64_t gj = j0 + wn * WN + b * 8 + c_in + h;
+          if (preload && gi < g.m && gj < g.n) {
+            const int64_t cj = g.cmap ? (int64_t)g.cmap[gj] : gj;
+            v = sc * g.C[gi + cj * g.ldc];
+          }
+          acc[a][b][h] = v;
+        }
+      }
+    }
+  }
 
   // symmetric-lower A (A_SYM_LOWER): per k-tile, tiles on/below the diagonal are read as stored
   // (m-contiguous), tiles above it from their mirror below the diagonal (k-contiguous layout),
@@ -423,7 +443,7 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
           const int64_t cj = g.cmap ? (int64_t)g.cmap[gj] : gj;
           double* cp = g.C + gi + cj * g.ldc;
           const double v = g.alpha * acc[a][b][h];
-          *cp = (g.beta == 0.0) ? v : v + g.beta * *cp;
+          *cp = (g.beta == 0.0 || preload) ? v : v + g.beta * *cp;
         }
       }
     }

@@ -61,6 +61,6 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
                   double* X, int64_t ldx, int64_t nrows, void* ws);
 // Left-apply Q_b to X (n x ncols): X <- Q_b X (conventional BC-Back).
 int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
-                 double* X, int64_t ldx, int64_t ncols);
+                 double* X, int64_t ldx, int64_t ncols, void* ws);
 
 }  // namespace pevd

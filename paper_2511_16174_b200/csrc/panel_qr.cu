@@ -145,12 +145,14 @@ __global__ void __launch_bounds__(QR_THREADS)
     if (tid < NVAL) hv[tid] = red[tid] + red[NVAL + tid] + red[2 * NVAL + tid] + red[3 * NVAL + tid];
     if (tid < KMAX) coef[tid] = (j < k && tid >= j && tid < k) ? __ldcg(piv + tid) : 0.0;
     __syncthreads();
-    // ---- T column j-1: T[0:jp, jp] = -tau_jp * T[0:jp, 0:jp] * g[0:jp]
-    if (j >= 1 && tid == 0) {
-      const int jp = j - 1;
+    // ---- T column j-1: T[0:jp, jp] = -tau_jp * T[0:jp, 0:jp] * g[0:jp]  (row q per thread;
+    //      column jp only reads columns < jp, so all rows are independent)
+    if (j >= 1 && tid < j) {
+      const int jp = j - 1, q = tid;
       const double tj = taus[jp];
-      T[jp + jp * KMAX] = tj;
-      for (int q = jp - 1; q >= 0; --q) {  // upper triangular mat-vec, rows q
+      if (q == jp) {
+        T[jp + jp * KMAX] = tj;
+      } else {
         double s = 0.0;
         for (int t = q; t < jp; ++t) s += T[q + t * KMAX] * hv[KMAX + t];
         T[q + jp * KMAX] = -tj * s;
@@ -251,7 +253,8 @@ int panel_qr(cudaStream_t st, int64_t m, int k, const double* panel, int64_t ldp
     return ERR_VALUE;
   }
   const int sms = num_sms();
-  int ncta = (int)std::min<int64_t>(sms, cdiv(m, 96));
+  // fewer, fatter CTAs for short panels: every grid step pays one arrival + one partial per CTA
+  int ncta = (int)std::min<int64_t>(sms, cdiv(m, 192));
   if (ncta < 1) ncta = 1;
   int64_t rows = cdiv(m, ncta);
   ncta = (int)cdiv(m, rows);

@@ -72,6 +72,21 @@ def dgemm(a, b, alpha=1.0, beta=0.0, c=None, trans_a=False, trans_b=False):
     return from_dev(dc)
 
 
+def dsymm_lower(a, b):
+    """A B with A symmetric, read from its lower triangle only (pevd_dsymm_lower)."""
+    L = _lib.load()
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    m, n = a.shape[0], b.shape[1]
+    da, db = to_dev(a), to_dev(b)
+    dc = empty(m, n)
+    ws = workspace(8 << 20)
+    rc = L.pevd_dsymm_lower(m, n, 1.0, _p(da), m, _p(db), m, 0.0, _p(dc), m, _p(ws), ws.numel(),
+                            _stream())
+    _lib.check(rc, "dsymm_lower")
+    return from_dev(dc)
+
+
 def panel_qr(panel):
     """Householder panel QR (sbr.py:69-116) -> (R, Y, W, T); Q = I - W Y^T, Q^T P = R."""
     L = _lib.load()
@@ -211,7 +226,9 @@ def bc_back_left(n, b, tau, V, x):
     dt = torch.from_numpy(np.ascontiguousarray(tau)).cuda()
     dv = torch.from_numpy(np.ascontiguousarray(V).reshape(-1)).cuda()
     dx = to_dev(x)
-    rc = L.pevd_bc_back_left(n, b, _p(dt), _p(dv), vld, _p(dx), x.shape[0], x.shape[1], _stream())
+    ws = workspace(L.pevd_bc_back_workspace_bytes(n, x.shape[1]))
+    rc = L.pevd_bc_back_left(n, b, _p(dt), _p(dv), vld, _p(dx), x.shape[0], x.shape[1], _p(ws),
+                             _stream())
     _lib.check(rc, "bc_back_left")
     return from_dev(dx)
 

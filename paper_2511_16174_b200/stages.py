@@ -13,7 +13,7 @@ import numpy as np
 from . import device
 from .core import (BandMatrix, FlopCounter, ProtocolError, ReflectorPanel, SymmetricMatrix,
                    TridiagonalMatrix, EigenResult)
-from .schedule import bc_back_macs, round_schedule, sbr_macs, bc_macs
+from .schedule import bc_back_macs, bc_macs, round_schedule, sbr_macs
 
 DEFAULT_GROUP_SIZE = 4  # backtrans.py:23 (device kernels use their own grouping)
 
@@ -65,6 +65,69 @@ def house_vector(x):
     alpha = -sign * float(np.hypot(x[0], tail))
     v[1:] = x[1:] / (x[0] - alpha)
     return v, 2.0 / (1.0 + float(np.dot(v[1:], v[1:]))), alpha
+
+
+def apply_block_reflector(c, panel: ReflectorPanel, side: str = "left", transpose: bool = False,
+                          counter: FlopCounter | None = None, stage: str = "reflector"):
+    """Q c, Q^T c, c Q or c Q^T for Q = I - W Y^T, in place, on the DMMA GEMM (core.py:258-279)."""
+    w, y = panel.W, panel.Y
+    if transpose:
+        w, y = y, w
+    if side == "left":
+        c -= device.dgemm(w, device.dgemm(y, c, trans_a=True))
+    elif side == "right":
+        c -= device.dgemm(device.dgemm(c, w), y, trans_b=True)
+    else:
+        raise ValueError(f"side must be left or right, got {side!r}")
+    if counter is not None:
+        counter.add(stage, 2 * c.shape[0] * c.shape[1] * panel.width)
+    return c
+
+
+def sym_rank2k_update(a, y, z, counter: FlopCounter | None = None, stage: str = "rank2k"):
+    """a -= y z^T + z y^T, symmetric to the last bit (core.py:282-306): the lower triangle is
+    computed on the GPU and mirrored."""
+    m, k = y.shape
+    if a.shape != (m, m) or z.shape != (m, k):
+        raise ValueError("shape mismatch in rank-2k update")
+    yz = np.hstack([y, z])
+    zy = np.hstack([z, y])
+    upd = device.dgemm(yz, zy, trans_b=True)
+    il = np.tril_indices(m)
+    a[il] -= upd[il]
+    iu = np.triu_indices(m, 1)
+    a[iu] = a.T[iu]
+    if counter is not None:
+        counter.add(stage, m * (m + 1) * k)
+    return a
+
+
+def form_z(a_trailing, w, y, counter: FlopCounter | None = None, stage: str = "SBR"):
+    """Z = A W - Y (W^T A W)/2 with the symmetric-lower DMMA product for A W (sbr.py:119-130)."""
+    m, k = w.shape
+    if a_trailing.shape != (m, m) or y.shape != (m, k):
+        raise ValueError("shape mismatch in form_z")
+    aw = device.dsymm_lower(a_trailing, w)
+    z = aw - 0.5 * device.dgemm(y, device.dgemm(w, aw, trans_a=True))
+    if counter is not None:
+        counter.add(stage, m * m * k + k * k * m + m * k * k)
+    return z
+
+
+def trailing_update(a2, y, z, mode: str = "symmetric", counter: FlopCounter | None = None,
+                    stage: str = "SBR"):
+    """A2 -= Y Z^T + Z Y^T (sbr.py:133-152)."""
+    m, k = y.shape
+    if a2.shape != (m, m) or z.shape != (m, k):
+        raise ValueError("shape mismatch in trailing update")
+    if mode == "full":
+        a2 -= device.dgemm(np.hstack([y, z]), np.hstack([z, y]), trans_b=True)
+        if counter is not None:
+            counter.add(stage, 2 * m * m * k)
+    elif mode == "symmetric":
+        sym_rank2k_update(a2, y, z, counter, stage)
+    else:
+        raise ValueError(f"mode must be full or symmetric, got {mode!r}")
 
 
 def panel_qr(panel: np.ndarray, col_offset: int = 0, inner_block: int = 8,
@@ -145,6 +208,44 @@ class BulgeReflectorSet:
         for p in range(len(self.tau)):
             out.setdefault(int(self.j_idx[p]), []).append(p)
         return out
+
+    def group_labels(self, group_size: int = 4):
+        """(G_k, B_j) labels per reflector (bulge.py:90-92)."""
+        return self.i_idx // group_size, self.j_idx.copy()
+
+    def back_deps(self, i: int, j: int):
+        """Reflectors applied before u_(i,j) in the conventional direction (bulge.py:94-96)."""
+        return [(i + 1, j - 1), (i + 1, j)] if j >= 1 else [(i + 1, j)]
+
+    def validate_order(self, order, direction: str = "reordered") -> None:
+        """Check an application order against the dependency rule (bulge.py:98-119)."""
+        when = np.empty(len(self.tau), dtype=np.int64)
+        when[np.asarray(order, dtype=np.int64)] = np.arange(len(order))
+        for p in range(len(self.tau)):
+            i, j = int(self.i_idx[p]), int(self.j_idx[p])
+            if direction == "conventional":
+                needed = [(i + 1, j - 1), (i + 1, j)]
+            elif direction == "reordered":
+                needed = [(i - 1, j), (i - 1, j + 1)]
+            else:
+                raise ValueError(direction)
+            for i2, j2 in needed:
+                q = self._pos.get((i2, j2))
+                if q is not None and when[q] >= when[p]:
+                    raise ValueError(f"order violates dependency: u_({i},{j}) before u_({i2},{j2})")
+
+    @classmethod
+    def merge(cls, parts):
+        """Concatenate per-worker sets (bulge.py:126-141)."""
+        parts = list(parts)
+        if not parts:
+            raise ValueError("nothing to merge")
+        n, b = parts[0].n, parts[0].b
+        if any((p.n, p.b) != (n, b) for p in parts):
+            raise ValueError("mismatched reflector sets")
+        return cls(n, b, *(np.concatenate([getattr(p, f) for p in parts])
+                           for f in ("i_idx", "j_idx", "row0", "length", "tau")),
+                   np.vstack([p.v for p in parts]))
 
     @classmethod
     def empty(cls, n, b):
@@ -270,6 +371,72 @@ def _form_qs(factors: SbrFactors) -> np.ndarray:
             T = np.triu(np.linalg.lstsq(p.Y, p.W, rcond=None)[0])
         tall[x * b * b: x * b * b + pw * pw] = np.asarray(T).T.reshape(-1)
     return device.sbr_back_form(n, b, ystair, tall)
+
+
+class RowAccumulator:
+    """Rows of Q_s built panel by panel in creation order (backtrans.py:149-183); each panel is
+    folded in from the right on the GPU: M[:, t0:] -= (M[:, t0:] W) Y^T."""
+
+    def __init__(self, n: int, rows):
+        lo, hi = rows
+        if not 0 <= lo <= hi <= n:
+            raise ValueError("row range out of bounds")
+        self.n, self.rows = n, (lo, hi)
+        self.m = np.zeros((hi - lo, n))
+        self.m[np.arange(hi - lo), np.arange(lo, hi)] = 1.0
+        self._applied = 0
+        self._last_offset = -1
+
+    def apply_panel(self, panel: ReflectorPanel, counter: FlopCounter | None = None) -> None:
+        if panel.col_offset <= self._last_offset:
+            raise ValueError("panels must arrive in ascending creation order")
+        self._last_offset = panel.col_offset
+        t0 = self.n - panel.W.shape[0]
+        blk = self.m[:, t0:]
+        blk -= device.dgemm(device.dgemm(blk, panel.W), panel.Y, trans_b=True)
+        if counter is not None:
+            counter.add("SBR-Back", 2 * self.m.shape[0] * (self.n - t0) * panel.width)
+        self._applied += 1
+
+    @property
+    def panels_applied(self) -> int:
+        return self._applied
+
+    def matrix(self) -> np.ndarray:
+        return self.m
+
+
+def application_order(u: BulgeReflectorSet, direction: str = "reordered", grouped: bool = True,
+                      group_size: int = DEFAULT_GROUP_SIZE) -> np.ndarray:
+    """Dependency-valid reflector orders (backtrans.py:214-236); the device kernels use the
+    grouped form with group size 64 and 8-reflector compact-WY blocks."""
+    i, j = u.i_idx, u.j_idx
+    if len(u) == 0:
+        return np.zeros(0, dtype=np.int64)
+    k = i // group_size
+    if direction == "reordered":
+        return np.lexsort((i, -j, k)) if grouped else np.lexsort((j, i))
+    if direction == "conventional":
+        return np.lexsort((-i, j, -k)) if grouped else np.lexsort((j, i))[::-1].copy()
+    raise ValueError(f"unknown direction {direction!r}")
+
+
+@dataclass
+class OverlapBlock:
+    """The 2b x b block handed from one worker's chase to the next (bulge.py:144-167)."""
+
+    values: np.ndarray
+    offset: int
+    b: int
+
+    def __post_init__(self):
+        self.values = np.ascontiguousarray(self.values, dtype=np.float64)
+        if self.values.shape != (2 * self.b, self.b):
+            raise ValueError(f"overlap must be {2 * self.b} x {self.b}")
+
+    @property
+    def words(self) -> int:
+        return 2 * self.b * self.b
 
 
 def final_gemm(q_sb_block, q_d, counter: FlopCounter | None = None) -> np.ndarray:

@@ -176,3 +176,42 @@ def test_stage_functions_match_reference_semantics():
     np.testing.assert_allclose(conv, reord.T, atol=1e-13)
     bands_o, _ = orc.sbr_reduce(a.data, b)
     np.testing.assert_allclose(band.bands, bands_o, atol=1e-12 * a.norm_f)
+
+
+def test_stage_primitives_match_oracle():
+    # core.py:258-306 / sbr.py:119-152 primitives on the DMMA GEMM
+    rng = np.random.default_rng(3)
+    m, k = 200, 8
+    y = np.tril(rng.standard_normal((m, k)), -1)
+    y[np.arange(k), np.arange(k)] = 1.0
+    w = rng.standard_normal((m, k))
+    panel = pkg.ReflectorPanel(W=w, Y=y, col_offset=0)
+    c = rng.standard_normal((m, 17))
+    for side, tr, want in (("left", False, c - w @ (y.T @ c)), ("left", True, c - y @ (w.T @ c))):
+        got = pkg.apply_block_reflector(c.copy(), panel, side=side, transpose=tr)
+        np.testing.assert_allclose(got, want, atol=1e-12)
+    cr = rng.standard_normal((9, m))
+    got = pkg.apply_block_reflector(cr.copy(), panel, side="right")
+    np.testing.assert_allclose(got, cr - (cr @ w) @ y.T, atol=1e-12)
+    a = rng.standard_normal((m, m))
+    a = (a + a.T) / 2
+    z = rng.standard_normal((m, k))
+    got = pkg.sym_rank2k_update(a.copy(), y, z)
+    np.testing.assert_array_equal(got, got.T)
+    np.testing.assert_allclose(got, a - y @ z.T - z @ y.T, atol=1e-12)
+    np.testing.assert_allclose(pkg.form_z(a, w, y), orc.form_z(a, w, y), atol=1e-11)
+
+
+def test_row_accumulator_and_orders():
+    n, b = 96, 8
+    a = pkg.SymmetricMatrix.from_dense(_sym(n, 21))
+    band, factors = pkg.sbr_reduce(a, pkg.SbrConfig(b=b))
+    acc = pkg.RowAccumulator(n, (10, 60))
+    for p in factors.panels:
+        acc.apply_panel(p)
+    np.testing.assert_allclose(acc.matrix(), pkg.sbr_back_rows(factors, (10, 60)), atol=1e-13)
+    _, u = pkg.bc_reduce(band)
+    for direction in ("reordered", "conventional"):
+        u.validate_order(pkg.application_order(u, direction), direction)
+    with pytest.raises(ValueError, match="dependency"):
+        u.validate_order(pkg.application_order(u, "reordered")[::-1], "reordered")
