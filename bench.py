@@ -80,10 +80,13 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def stage_flops(n: int):
-    """Algorithmic FP64 flops per stage; BC-Back as its BLAS2 count."""
-    return {"sbr": 4 * n ** 3 / 3, "sbr_back": 4 * n ** 3 / 3, "bc_back": 2 * n ** 3,
-            "final": 2 * n ** 3, "solver": 4 * n ** 3 / 3}
+def stage_flops(n: int, order: str = "conventional"):
+    """Algorithmic FP64 flops per stage; BC-Back as its BLAS2 count.
+    SBR-Back forms Q_s ((4/3) n^3, pipelined/sequential) or applies it to Q_d from the left
+    (2 n^3, conventional, which has no final GEMM)."""
+    conv = order == "conventional"
+    return {"sbr": 4 * n ** 3 / 3, "sbr_back": (2 if conv else 4 / 3) * n ** 3,
+            "bc_back": 2 * n ** 3, "final": 0 if conv else 2 * n ** 3, "solver": 4 * n ** 3 / 3}
 
 
 def run_b200(args):
@@ -232,21 +235,20 @@ def run_b200_single(args):
     st = stats[-1]
     stage_ms = {k: getattr(st, k + "_ms")[1] - getattr(st, k + "_ms")[0]
                 for k in ("sbr", "bc", "solver", "sbr_back", "bc_back", "final")}
-    fl = stage_flops(n)
+    fl = stage_flops(n, args.order)
     dom = max(("sbr", "sbr_back", "bc_back", "final", "solver"), key=lambda k: stage_ms[k])
     peaks = load_fp64_peaks()
-    peak = peaks["dfma"] if dom == "bc_back" else peaks["dmma"]
+    peak = peaks["dmma"]  # every GEMM-like stage (BC-Back included) runs on DMMA
     achieved = fl[dom] / (stage_ms[dom] * 1e-3) / 1e12
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3),
                 "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
                 "traffic": None,
-                "peak_source": ("FP64 DFMA microbenchmark" if dom == "bc_back" else
-                                "FP64 DMMA microbenchmark") +
+                "peak_source": "FP64 DMMA (mma.sync m8n8k4) microbenchmark"
                                " on this pool's B200 (profiles/r01_fp64_peaks.json); "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "stage_ms": {k: round(v, 1) for k, v in stage_ms.items()},
                 "stage_tflops": {k: round(fl[k] / (stage_ms[k] * 1e-3) / 1e12, 2)
-                                 for k in fl if stage_ms[k] > 0}}
+                                 for k in fl if stage_ms[k] > 0 and fl[k] > 0}}
     clocks = clk.summary()
 
     # ---- e2e through the C ABI with host buffers (pevd_syevd)
@@ -362,7 +364,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=49152)
     ap.add_argument("--b", type=int, default=32)
-    ap.add_argument("--order", default="pipelined", choices=["pipelined", "sequential", "conventional"])
+    ap.add_argument("--order", default="conventional", choices=["pipelined", "sequential", "conventional"])
     ap.add_argument("--seed", type=int, default=49152)
     ap.add_argument("--cpu-n", type=int, default=1536)
     ap.add_argument("--ref-n", type=int, default=1024)

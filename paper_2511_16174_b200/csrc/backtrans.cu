@@ -4,8 +4,9 @@
 // SBR-Back: Q_s = H_0 H_1 ... H_{R-1}, H_x = I - Y_x T_x Y_x^T, accumulated backwards from the
 // identity (the cheap direction: each step only touches the trailing (n-t0)^2 block).  NB
 // consecutive panels are aggregated into one compact-WY block (Y_agg = the panels' columns of the
-// explicit-Y staircase left in A by the band reduction, T_agg rebuilt from Y_agg^T Y_agg and the
-// panel taus, LAPACK larft recurrence) so the three DMMA GEMMs per block are compute-bound.
+// explicit-Y staircase left in A by the band reduction, T_agg merged from the panel T's and
+// Y_agg^T Y_agg by the recursive larft recurrence, all groups batched up front) so the three
+// DMMA GEMMs per block are compute-bound.
 //
 // BC-Back (reordered, backtrans.py:277-310): X <- X Q_b for a block of rows of X (X = Q_s, so the
 // result is Q_s Q_b).  Rows are independent, so one thread owns one row; reflectors are applied in
@@ -22,7 +23,21 @@ namespace pevd {
 
 namespace {
 
-constexpr int NB_AGG = 8;  // panels per aggregated SBR-Back block
+constexpr int NB_AGG_MAX = 16;  // workspace bound on the panels per aggregated SBR-Back block
+
+// panels per aggregated SBR-Back block (K = nb * b reflectors per compact-WY GEMM pass);
+// PEVD_NBAGG overrides the default for tuning probes
+int nb_agg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PEVD_NBAGG");
+    v = e ? atoi(e) : 16;
+    if (v < 1) v = 1;
+    if (v > NB_AGG_MAX) v = NB_AGG_MAX;
+    while (v & (v - 1)) v &= v - 1;  // the recursive T merge pairs sibling blocks
+  }
+  return v;
+}
 
 __global__ void set_identity(int64_t n, double* Q, int64_t ldq) {
   const int64_t total = n * n;
@@ -30,49 +45,6 @@ __global__ void set_identity(int64_t n, double* Q, int64_t ldq) {
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % n, j = idx / n;
     Q[i + j * ldq] = (i == j) ? 1.0 : 0.0;
-  }
-}
-
-// T_agg (K x K, upper) of the aggregated block reflector I - Y T Y^T from the per-panel T_x
-// (diagonal blocks, from the panel QR) and the Gram matrix G = Y^T Y:
-//   T[0:c, blk] = -T[0:c, 0:c] G[0:c, blk] T_blk     (blocks of b columns, c = blk * b)
-// one CTA, all products in shared memory (K <= NB_AGG * 32 = 128).
-__global__ void __launch_bounds__(256)
-    larft_kernel(int K, const double* __restrict__ G, int ldg, const double* __restrict__ Tall,
-                 int b, int x0, int64_t R, int pw_last, double* T) {
-  // T lives in global memory (L2-resident, K <= 256); the per-block product in shared memory
-  extern __shared__ double tmp[];  // (K - b) x b
-  const int tid = threadIdx.x;
-  for (int e = tid; e < K * K; e += blockDim.x) T[e] = 0.0;
-  __syncthreads();
-  const int nblk = (K + b - 1) / b;
-  for (int B = 0; B < nblk; ++B) {
-    const int x = x0 + B;
-    const int pw = (x == R - 1) ? pw_last : b;
-    const double* Tx = Tall + (int64_t)x * b * b;  // pw x pw, ld pw
-    const int c0 = B * b;
-    for (int e = tid; e < pw * pw; e += blockDim.x) {
-      const int r = e % pw, c = e / pw;
-      T[(c0 + r) + (c0 + c) * K] = Tx[r + c * pw];
-    }
-    __syncthreads();
-    if (B == 0) continue;
-    // tmp = T[0:c0, 0:c0] G[0:c0, c0:c0+pw]
-    for (int e = tid; e < c0 * pw; e += blockDim.x) {
-      const int r = e % c0, c = e / c0;
-      double s = 0.0;
-      for (int t = r; t < c0; ++t) s += T[r + t * K] * G[t + (int64_t)(c0 + c) * ldg];
-      tmp[r + c * c0] = s;
-    }
-    __syncthreads();
-    // T[0:c0, blk] = -tmp T_blk
-    for (int e = tid; e < c0 * pw; e += blockDim.x) {
-      const int r = e % c0, c = e / c0;
-      double s = 0.0;
-      for (int t = 0; t <= c; ++t) s += tmp[r + t * c0] * T[(c0 + t) + (c0 + c) * K];
-      T[r + (c0 + c) * K] = -s;
-    }
-    __syncthreads();
   }
 }
 
@@ -236,23 +208,6 @@ __global__ void __launch_bounds__(128, MINB)
   }
 }
 
-int launch_larft(cudaStream_t st, int K, const double* G, const double* Tall, int b, int x0,
-                 int64_t R, int pw_last, double* T) {
-  const size_t smem = (size_t)(K * b) * 8;
-  static int attr_dev = -1;
-  int dev;
-  PEVD_CUDA(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    PEVD_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
-    attr_dev = dev;
-  }
-  larft_kernel<<<1, 256, smem, st>>>(K, G, K, Tall, b, x0, R, pw_last, T);
-  PEVD_LAUNCH_CHECK();
-  return OK;
-}
-
-
 // ------------------------------------------------------------ BC-Back, b = 32, 4 lanes per row
 // Lane (row r = lane/4, quarter q = lane%4) owns window positions p = 4m + q, m < Q4_WM: a
 // 96-wide window (Q4_SG = 64 sweeps + b - 1) costs 24 doubles per lane.  Reflector t touches
@@ -409,12 +364,24 @@ __global__ void __launch_bounds__(Q4_THREADS, 2)
 // are prefetched into registers during the previous step and staged double-buffered.
 constexpr int WY_ROWS = 64;  // 8 warps x 8 rows
 constexpr int WY_THREADS = 256;
-constexpr int WY_VP = 48;    // padded reflector row: v[idx] at idx + 8, idx in [-8, 40)
+// Shared-memory layouts, each conflict-free for its DMMA fragment pattern (a 64-bit warp access
+// is served per half-warp: lanes (r8 in 0..3, qd in 0..3) must hit 16 distinct 8-byte banks).
+// Both store reflector t (local index, shifted by its offset t % 8 inside its block of 8) at
+// window position p = (t % 8) + idx, zero outside [t % 8, t % 8 + 32):
+//  * va[h][t][s]:  P = X V operand, element p = 2 s + h  (lane reads t = tb + r8, s = 4 cc + qd:
+//                  address 20 r8 + qd -> pitch 20 = 4 mod 16)
+//  * vu[t][p]:     X += P2 V^T operand (lane reads t = tb + 2 qd + hh, p = 8 cc + r8:
+//                  address 84 qd + r8 -> pitch 42, 2 * 42 = 4 mod 16)
+//  * T[blk][s][t]: -T, pitch 10 (lane reads s = 2 qd + hh, t = r8: 20 qd + r8)
+constexpr int WY_PA = 20;
+constexpr int WY_PB = 42;
+constexpr int WY_TP = 10;
 constexpr int WY_PF = (Q4_SG * 32 + Q4_SG * 8) / WY_THREADS;  // prefetched doubles per thread
 
 struct WySmem {
-  double vp[2][Q4_SG][WY_VP];
-  double T[2][Q4_SG / 8][8][8];  // -T per block, [buf][block][s][t]
+  double va[2][2][Q4_SG][WY_PA];  // [buf][h][t][s]
+  double vu[2][Q4_SG][WY_PB];     // [buf][t][p]
+  double T[2][Q4_SG / 8][8][WY_TP];  // -T per block, [buf][block][s][t]
   int unit;
 };
 
@@ -523,7 +490,8 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qd = lane & 3, r8 = lane >> 2;
   const int64_t nsw = n - 2;
-  for (int e = tid; e < 2 * Q4_SG * WY_VP; e += WY_THREADS) (&S.vp[0][0][0])[e] = 0.0;
+  // zero everything once: the positions outside each reflector's support are never written
+  for (int e = tid; e < (int)(sizeof(WySmem) / 8) - 1; e += WY_THREADS) (&S.va[0][0][0][0])[e] = 0.0;
   __syncthreads();
   // prefetch registers: element e = tid + p * WY_THREADS; e < 2048: V(t = e/32, r = e%32),
   // else -T (block = (e-2048)/64, entry (e-2048)%64)
@@ -549,8 +517,14 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
 #pragma unroll
     for (int p = 0; p < WY_PF; ++p) {
       const int e = tid + p * WY_THREADS;
-      if (e < Q4_SG * B) S.vp[buf][e >> 5][(e & 31) + 8] = pf[p];
-      else (&S.T[buf][0][0][0])[e - Q4_SG * B] = pf[p];
+      if (e < Q4_SG * B) {
+        const int t = e >> 5, pos = (e & 31) + (t & 7);
+        S.va[buf][pos & 1][t][pos >> 1] = pf[p];
+        S.vu[buf][t][pos] = pf[p];
+      } else {
+        const int e2 = e - Q4_SG * B;
+        S.T[buf][e2 >> 6][(e2 >> 3) & 7][e2 & 7] = pf[p];
+      }
     }
   };
   (void)nsw;
@@ -613,11 +587,12 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
         const int blk = LEFT ? Q4_SG / 8 - 1 - bb : bb;
         const int tb = blk * 8;
         double p0 = 0.0, p1 = 0.0, e0 = 0.0, e1 = 0.0;
-        const double* vrow = &S.vp[buf][tb + r8][8 + 2 * qd - r8];
+        const double* v0 = &S.va[buf][0][tb + r8][qd];
+        const double* v1 = &S.va[buf][1][tb + r8][qd];
 #pragma unroll
         for (int cc = 0; cc < 5; ++cc) {
-          dmma884(p0, p1, w[blk + cc][0], vrow[8 * cc]);
-          dmma884(e0, e1, w[blk + cc][1], vrow[8 * cc + 1]);
+          dmma884(p0, p1, w[blk + cc][0], v0[4 * cc]);
+          dmma884(e0, e1, w[blk + cc][1], v1[4 * cc]);
         }
         p0 += e0;
         p1 += e1;
@@ -626,8 +601,8 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
         dmma884(q0, q1, p1, S.T[buf][blk][2 * qd + 1][r8]);
 #pragma unroll
         for (int cc = 0; cc < 5; ++cc) {
-          const double va = S.vp[buf][tb + 2 * qd][8 + 8 * cc + r8 - 2 * qd];
-          const double vb = S.vp[buf][tb + 2 * qd + 1][8 + 8 * cc + r8 - 2 * qd - 1];
+          const double va = S.vu[buf][tb + 2 * qd][8 * cc + r8];
+          const double vb = S.vu[buf][tb + 2 * qd + 1][8 * cc + r8];
           dmma884(w[blk + cc][0], w[blk + cc][1], q0, va);
           dmma884(w[blk + cc][0], w[blk + cc][1], q1, vb);
         }
@@ -701,80 +676,207 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
 
 }  // namespace
 
+// ---------------------------------------------------------------- SBR-Back (compact WY)
+// Panels are aggregated NB = nb_agg() at a time (K = NB b reflectors):
+//   H_x0 ... H_x0+NB-1 = I - Y T Y^T,  Y = the strided staircase view A[t0:, c0:c0+K]
+// The aggregated T factors of ALL groups are built up front (sbr_back_prepare), batched over the
+// groups: G = Y^T Y per group, then the recursive larft merge (LAPACK dlarft, recursive form)
+//   T12 = -T11 (G12 T22)  for pairs of sibling blocks of s = b, 2b, 4b, ... columns,
+// each level two grouped DMMA GEMM launches over every (group, pair).  Every group is padded to
+// K = NB b columns (absent panels: zero T blocks, zero Gram), so all groups share one layout:
+// T of group g at Tagg + g K^2 (ld K).  The prep depends only on the SBR output, so the
+// orchestrator runs it on a side stream under the bulge chase / divide and conquer.
+struct SbrBackWs {
+  double *tmp1, *tmp2, *sk, *Tagg, *G, *Tmp;
+  GemmArgs* dargs;
+  int64_t ngroups, K, skn;
+  int NB;
+};
+
+static int64_t sbr_back_ngroups(int64_t n, int b, int NB) {
+  return (b < 1 || n <= b) ? 0 : cdiv(sbr_num_rounds(n, b), NB);
+}
+
+static SbrBackWs sbr_back_carve(int64_t n, int b, void* ws, int NB) {
+  SbrBackWs W;
+  W.NB = NB;
+  W.K = (int64_t)NB * b;
+  W.ngroups = sbr_back_ngroups(n, b, NB);
+  const int64_t Km = (int64_t)NB_AGG_MAX * b;
+  const int64_t gmax = sbr_back_ngroups(n, b, 1);  // bound for any NB >= 1
+  W.tmp1 = (double*)ws;
+  W.tmp2 = W.tmp1 + Km * n;
+  W.skn = 4 << 20;
+  W.sk = W.tmp2 + Km * n;
+  // groups * K^2 <= cdiv(R, NB) * NB^2 b^2 <= (R + NB) * NB * b^2
+  const int64_t tsz = (gmax + NB_AGG_MAX) * (int64_t)NB_AGG_MAX * b * b;
+  W.Tagg = W.sk + W.skn;
+  W.G = W.Tagg + tsz;
+  W.Tmp = W.G + tsz;
+  W.dargs = (GemmArgs*)(W.Tmp + tsz);
+  return W;
+}
+
+__global__ void tagg_init_kernel(int64_t ngroups, int NB, int b, int64_t R, int pw_last,
+                                 const double* __restrict__ Tall, double* __restrict__ Tagg,
+                                 double* __restrict__ G) {
+  const int64_t K = (int64_t)NB * b;
+  const int64_t total = ngroups * K * K;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = idx / (K * K), e = idx % (K * K);
+    const int r = (int)(e % K), c = (int)(e / K);
+    double v = 0.0;
+    if (r / b == c / b) {
+      const int64_t x = g * NB + r / b;
+      if (x < R) {
+        const int pw = (x == R - 1) ? pw_last : b;
+        const int lr = r % b, lc = c % b;
+        if (lr < pw && lc < pw) v = Tall[x * b * b + lr + (int64_t)lc * pw];
+      }
+    }
+    Tagg[idx] = v;
+    G[idx] = 0.0;
+  }
+}
+
+// descriptors of one merge level: entries [0, cnt) Tmp12 = G12 T22, [cnt, 2 cnt) T12 = -T11 Tmp12
+// for every (group g, pair p) with o = 2 p s
+__global__ void tagg_args_kernel(int64_t ngroups, int64_t K, int64_t s, double* G, double* Tagg,
+                                 double* Tmp, GemmArgs* out) {
+  const int64_t pairs = K / (2 * s), cnt = ngroups * pairs;
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= 2 * cnt) return;
+  const int pass = (int)(id / cnt);
+  const int64_t g = (id % cnt) / pairs, p = (id % cnt) % pairs;
+  const int64_t o = p * 2 * s, K2 = K * K, blk12 = o + (o + s) * K;
+  double* Tg = Tagg + g * K2;
+  GemmArgs a{};
+  a.m = a.n = a.k = s;
+  a.beta = 0.0;
+  a.lda = a.ldb = a.ldc = K;
+  a.transA = a.transB = 0;
+  a.amode = A_GENERAL;
+  a.cmode = C_ALL;
+  a.amap = a.cmap = nullptr;
+  if (pass == 0) {
+    a.alpha = 1.0;
+    a.A = G + g * K2 + blk12;
+    a.B = Tg + (o + s) + (o + s) * K;
+    a.C = Tmp + g * K2 + blk12;
+  } else {
+    a.alpha = -1.0;
+    a.A = Tg + o + o * K;
+    a.B = Tmp + g * K2 + blk12;
+    a.C = Tg + blk12;
+  }
+  out[id] = a;
+}
+
 int64_t sbr_back_ws_bytes(int64_t n, int b) {
-  const int64_t K = (int64_t)NB_AGG * b;
-  return (2 * K * n + 2 * K * K + (4 << 20)) * 8 + 1024;
+  const int64_t Km = (int64_t)NB_AGG_MAX * b;
+  const int64_t gmax = sbr_back_ngroups(n, b, 1);
+  const int64_t tsz = (gmax + NB_AGG_MAX) * (int64_t)NB_AGG_MAX * b * b;
+  const int64_t nargs = 2 * (gmax + 1) * NB_AGG_MAX;
+  return (2 * Km * n + (4 << 20) + 3 * tsz) * 8 + nargs * (int64_t)sizeof(GemmArgs) + 4096;
+}
+
+// group g: panels [g NB, min(R, g NB + NB)), rows from t0 = g NB b + b, K_g reflectors
+static void group_dims(int64_t n, int b, int NB, int64_t R, int64_t g, int64_t* t0, int64_t* c0,
+                       int64_t* Kg) {
+  const int64_t x0 = g * NB, x1 = std::min<int64_t>(R, x0 + NB);
+  *c0 = x0 * b;
+  *t0 = *c0 + b;
+  int64_t K = 0;
+  for (int64_t x = x0; x < x1; ++x) K += std::min<int64_t>(b, n - b - x * b);
+  *Kg = K;
+}
+
+int sbr_back_prepare(cudaStream_t st, int64_t n, int b, const double* Yfull, const double* Tall,
+                     void* ws) {
+  if (b < 1 || n <= b) return OK;
+  const int NB = nb_agg();
+  SbrBackWs W = sbr_back_carve(n, b, ws, NB);
+  const int64_t R = sbr_num_rounds(n, b);
+  const int64_t K = W.K, K2 = K * K;
+  tagg_init_kernel<<<(unsigned)std::min<int64_t>(cdiv(W.ngroups * K2, 256), 16384), 256, 0, st>>>(
+      W.ngroups, NB, b, R, (int)(n - b - (R - 1) * b), Tall, W.Tagg, W.G);
+  PEVD_LAUNCH_CHECK();
+  // Gram matrices (the staircase is zero above each panel, so Y^T Y over rows [t0, n) is exact)
+  for (int64_t g = 0; g < W.ngroups; ++g) {
+    int64_t t0, c0, Kg;
+    group_dims(n, b, NB, R, g, &t0, &c0, &Kg);
+    const double* Y = Yfull + t0 + c0 * n;
+    GemmArgs gg{Kg, Kg, n - t0, 1.0, 0.0, Y, n, Y, n, W.G + g * K2, K, 1, 0, A_GENERAL, C_ALL};
+    PEVD_TRY(gemm(st, gg, W.sk, W.skn));
+  }
+  if (NB == 1) return OK;
+  // recursive merge, one level per doubling of the block size; descriptors written on the
+  // device (no host synchronisation, so the prep can be enqueued on a side stream)
+  int64_t off = 0;
+  for (int64_t s = b; s < K; s *= 2) {
+    const int64_t cnt = W.ngroups * (K / (2 * s));
+    tagg_args_kernel<<<(unsigned)cdiv(2 * cnt, 128), 128, 0, st>>>(W.ngroups, K, s, W.G, W.Tagg,
+                                                                   W.Tmp, W.dargs + off);
+    PEVD_LAUNCH_CHECK();
+    PEVD_TRY(gemm_grouped(st, W.dargs + off, (int)cnt, s, s));
+    PEVD_TRY(gemm_grouped(st, W.dargs + off + cnt, (int)cnt, s, s));
+    off += 2 * cnt;
+  }
+  return OK;
 }
 
 int sbr_back_form(cudaStream_t st, int64_t n, int b, const double* Yfull, const double* Tall,
-                  double* Qs, int64_t ldq, void* ws) {
+                  double* Qs, int64_t ldq, void* ws, bool prepared) {
   set_identity<<<(unsigned)std::min<int64_t>(cdiv(n * n, 256), 16384), 256, 0, st>>>(n, Qs, ldq);
   PEVD_LAUNCH_CHECK();
   if (b < 1 || n <= b) return OK;
+  if (!prepared) PEVD_TRY(sbr_back_prepare(st, n, b, Yfull, Tall, ws));
+  const int NB = nb_agg();
+  SbrBackWs W = sbr_back_carve(n, b, ws, NB);
   const int64_t R = sbr_num_rounds(n, b);
-  const int64_t Kmax = (int64_t)NB_AGG * b;
-  double* tmp1 = (double*)ws;
-  double* tmp2 = tmp1 + Kmax * n;
-  double* Gm = tmp2 + Kmax * n;
-  double* Tg = Gm + Kmax * Kmax;
-  double* sk = Tg + Kmax * Kmax;
-  const int64_t skn = 4 << 20;
-  const int64_t ngroups = cdiv(R, NB_AGG);
-  for (int64_t g = ngroups - 1; g >= 0; --g) {
-    const int64_t x0 = g * NB_AGG, x1 = std::min<int64_t>(R, x0 + NB_AGG);
-    const int64_t c0 = x0 * b, t0 = c0 + b, m = n - t0;
-    int64_t K = 0;
-    for (int64_t x = x0; x < x1; ++x) K += std::min<int64_t>(b, n - b - x * b);
+  for (int64_t g = W.ngroups - 1; g >= 0; --g) {
+    int64_t t0, c0, K;
+    group_dims(n, b, NB, R, g, &t0, &c0, &K);
+    const int64_t m = n - t0;
     const double* Y = Yfull + t0 + c0 * n;  // m x K, ld n (explicit staircase)
+    const double* Tg = W.Tagg + g * W.K * W.K;
     double* Q22 = Qs + t0 + t0 * ldq;
-    // Gram and T_agg
-    GemmArgs gg{K, K, m, 1.0, 0.0, Y, n, Y, n, Gm, K, 1, 0, A_GENERAL, C_ALL};
-    PEVD_TRY(gemm(st, gg, sk, skn));
-    PEVD_TRY(launch_larft(st, (int)K, Gm, Tall, b, (int)x0, R, (int)(n - b - (R - 1) * b), Tg));
-    PEVD_LAUNCH_CHECK();
     // tmp1 = Y^T Q22 (K x m); tmp2 = T tmp1; Q22 -= Y tmp2
-    GemmArgs g1{K, m, m, 1.0, 0.0, Y, n, Q22, ldq, tmp1, K, 1, 0, A_GENERAL, C_ALL};
-    PEVD_TRY(gemm(st, g1, sk, skn));
-    GemmArgs g2{K, m, K, 1.0, 0.0, Tg, K, tmp1, K, tmp2, K, 0, 0, A_GENERAL, C_ALL};
-    PEVD_TRY(gemm(st, g2, sk, skn));
-    GemmArgs g3{m, m, K, -1.0, 1.0, Y, n, tmp2, K, Q22, ldq, 0, 0, A_GENERAL, C_ALL};
-    PEVD_TRY(gemm(st, g3, sk, skn));
+    GemmArgs g1{K, m, m, 1.0, 0.0, Y, n, Q22, ldq, W.tmp1, K, 1, 0, A_GENERAL, C_ALL};
+    PEVD_TRY(gemm(st, g1, W.sk, W.skn));
+    GemmArgs g2{K, m, K, 1.0, 0.0, Tg, W.K, W.tmp1, K, W.tmp2, K, 0, 0, A_GENERAL, C_ALL};
+    PEVD_TRY(gemm(st, g2, W.sk, W.skn));
+    GemmArgs g3{m, m, K, -1.0, 1.0, Y, n, W.tmp2, K, Q22, ldq, 0, 0, A_GENERAL, C_ALL};
+    PEVD_TRY(gemm(st, g3, W.sk, W.skn));
   }
   return OK;
 }
 
 int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, const double* Tall,
-                        double* X, int64_t ldx, int64_t ncols, void* ws) {
+                        double* X, int64_t ldx, int64_t ncols, void* ws, bool prepared) {
   // X <- Q_s X = H_0 (H_1 ( ... (H_{R-1} X))): aggregated blocks from the last panel backwards
   if (b < 1 || n <= b) return OK;
+  if (!prepared) PEVD_TRY(sbr_back_prepare(st, n, b, Yfull, Tall, ws));
+  const int NB = nb_agg();
+  SbrBackWs W = sbr_back_carve(n, b, ws, NB);
   const int64_t R = sbr_num_rounds(n, b);
-  const int64_t Kmax = (int64_t)NB_AGG * b;
-  double* tmp1 = (double*)ws;
-  double* tmp2 = tmp1 + Kmax * n;
-  double* Gm = tmp2 + Kmax * n;
-  double* Tg = Gm + Kmax * Kmax;
-  double* sk = Tg + Kmax * Kmax;
-  const int64_t skn = 4 << 20;
-  const int64_t ngroups = cdiv(R, NB_AGG);
-  for (int64_t g = ngroups - 1; g >= 0; --g) {
-    const int64_t x0 = g * NB_AGG, x1 = std::min<int64_t>(R, x0 + NB_AGG);
-    const int64_t c0 = x0 * b, t0 = c0 + b, m = n - t0;
-    int64_t K = 0;
-    for (int64_t x = x0; x < x1; ++x) K += std::min<int64_t>(b, n - b - x * b);
+  for (int64_t g = W.ngroups - 1; g >= 0; --g) {
+    int64_t t0, c0, K;
+    group_dims(n, b, NB, R, g, &t0, &c0, &K);
+    const int64_t m = n - t0;
     const double* Y = Yfull + t0 + c0 * n;
+    const double* Tg = W.Tagg + g * W.K * W.K;
     double* X2 = X + t0;
-    GemmArgs gg{K, K, m, 1.0, 0.0, Y, n, Y, n, Gm, K, 1, 0, A_GENERAL, C_ALL};
-    PEVD_TRY(gemm(st, gg, sk, skn));
-    PEVD_TRY(launch_larft(st, (int)K, Gm, Tall, b, (int)x0, R, (int)(n - b - (R - 1) * b), Tg));
-    PEVD_LAUNCH_CHECK();
     for (int64_t c = 0; c < ncols; c += n) {
       const int64_t nc = std::min<int64_t>(n, ncols - c);
-      GemmArgs g1{K, nc, m, 1.0, 0.0, Y, n, X2 + c * ldx, ldx, tmp1, K, 1, 0, A_GENERAL, C_ALL};
-      PEVD_TRY(gemm(st, g1, sk, skn));
-      GemmArgs g2{K, nc, K, 1.0, 0.0, Tg, K, tmp1, K, tmp2, K, 0, 0, A_GENERAL, C_ALL};
-      PEVD_TRY(gemm(st, g2, sk, skn));
-      GemmArgs g3{m, nc, K, -1.0, 1.0, Y, n, tmp2, K, X2 + c * ldx, ldx, 0, 0, A_GENERAL, C_ALL};
-      PEVD_TRY(gemm(st, g3, sk, skn));
+      GemmArgs g1{K, nc, m, 1.0, 0.0, Y, n, X2 + c * ldx, ldx, W.tmp1, K, 1, 0, A_GENERAL, C_ALL};
+      PEVD_TRY(gemm(st, g1, W.sk, W.skn));
+      GemmArgs g2{K, nc, K, 1.0, 0.0, Tg, W.K, W.tmp1, K, W.tmp2, K, 0, 0, A_GENERAL, C_ALL};
+      PEVD_TRY(gemm(st, g2, W.sk, W.skn));
+      GemmArgs g3{m, nc, K, -1.0, 1.0, Y, n, W.tmp2, K, X2 + c * ldx, ldx, 0, 0, A_GENERAL,
+                  C_ALL};
+      PEVD_TRY(gemm(st, g3, W.sk, W.skn));
     }
   }
   return OK;

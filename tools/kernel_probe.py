@@ -66,14 +66,15 @@ def reflectors(n, b):
 def main():
     mode = sys.argv[1]
     out = {"mode": mode}
-    if mode == "bcback":
+    if mode in ("bcback", "bcbackl"):
         n = int(sys.argv[2])
         b = 32
         tau, V, vld, _ = reflectors(n, b)
         X = torch.randn((n, n), dtype=torch.float64, device="cuda")
         ws = torch.empty(L.pevd_bc_back_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
-        ms, ts = timed(lambda: _lib.check(L.pevd_bc_back_right(n, b, ptr(tau), ptr(V), vld, ptr(X),
-                                                               n, n, ptr(ws), stream()), "bcback"))
+        fn = L.pevd_bc_back_right if mode == "bcback" else L.pevd_bc_back_left
+        ms, ts = timed(lambda: _lib.check(fn(n, b, ptr(tau), ptr(V), vld, ptr(X), n, n, ptr(ws),
+                                             stream()), mode))
         nref = L.pevd_bc_num_reflectors(n, b)
         flops = 4.0 * b * nref * n
         out.update(n=n, G=os.environ.get("PEVD_BCBACK_G", "default"), ms=ms, ts=ts,
@@ -123,6 +124,30 @@ def main():
             _lib.check(L.pevd_sbr(n, b, ptr(A), n, ptr(bands), ptr(tall), ptr(ws), stream()), "sbr")
         ms, ts = timed(f, reps=2)
         out.update(n=n, ms=ms, tflops=4 * n ** 3 / 3 / ms / 1e9)
+    elif mode in ("sbrback", "sbrform"):
+        # SBR once (its Y staircase and T factors), then time SBR-Back on an n x n X
+        n = int(sys.argv[2])
+        b = 32
+        A = torch.randn((n, n), dtype=torch.float64, device="cuda")
+        A = (A + A.t()) / 2
+        bands = torch.empty((b + 1) * n, dtype=torch.float64, device="cuda")
+        tall = torch.empty(((n - b) // b + 1) * b * b, dtype=torch.float64, device="cuda")
+        ws = torch.empty(L.pevd_sbr_workspace_bytes(n, b), dtype=torch.uint8, device="cuda")
+        _lib.check(L.pevd_sbr(n, b, ptr(A), n, ptr(bands), ptr(tall), ptr(ws), stream()), "sbr")
+        del ws
+        X = torch.randn((n, n), dtype=torch.float64, device="cuda")
+        ws = torch.empty(L.pevd_sbr_back_workspace_bytes(n, b), dtype=torch.uint8, device="cuda")
+        if mode == "sbrback":
+            fn = lambda: _lib.check(L.pevd_sbr_back_left(n, b, ptr(A), ptr(tall), ptr(X), n, n,  # noqa
+                                                         ptr(ws), stream()), "sbr_back_left")
+            flops = 2.0 * n ** 3
+        else:
+            fn = lambda: _lib.check(L.pevd_sbr_back_form(n, b, ptr(A), ptr(tall), ptr(X), n,  # noqa
+                                                         ptr(ws), stream()), "sbr_back_form")
+            flops = 4.0 * n ** 3 / 3
+        ms, ts = timed(fn, reps=2)
+        out.update(n=n, nbagg=os.environ.get("PEVD_NBAGG", "default"), ms=ms,
+                   tflops=flops / ms / 1e9)
     elif mode == "stedc":
         n = int(sys.argv[2])
         d0 = torch.randn(n, dtype=torch.float64, device="cuda")
