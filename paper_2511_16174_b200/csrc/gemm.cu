@@ -9,6 +9,7 @@
 // Modes used by the band reduction: A_SYM_LOWER reads a symmetric matrix from its lower
 // triangle only (tiles above the diagonal are fetched transposed from below it), and
 // C_LOWER_TILES skips CTA tiles strictly above the diagonal (trailing rank-2k update).
+#include <cstdlib>
 #include "gemm.cuh"
 
 namespace pevd {
@@ -460,8 +461,23 @@ template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, 
 __global__ void __launch_bounds__(FCfg<TA, TB, BM, BN, BK, WM, WN, STAGES, SYM>::NT)
     gemm_fast_kernel(const __grid_constant__ GemmArgs g, int ksplit, double* ws) {
   extern __shared__ __align__(16) double smem[];
-  const int64_t i0 = (int64_t)blockIdx.x * BM, j0 = (int64_t)blockIdx.y * BN;
-  if (g.cmode == C_LOWER_TILES && i0 + BM - 1 < j0) return;
+  int64_t i0 = (int64_t)blockIdx.x * BM, j0 = (int64_t)blockIdx.y * BN;
+  if (g.cmode == C_LOWER_TILES) {
+    // 1-D grid over the tiles intersecting the lower triangle, column by column
+    const int64_t RT = (g.m + BM - 1) / BM;
+    int64_t idx = blockIdx.x, tj = 0;
+    for (;; ++tj) {
+      const int64_t lo = tj * BN - BM + 1;
+      const int64_t tmin = lo <= 0 ? 0 : (lo + BM - 1) / BM;
+      const int64_t cnt = RT > tmin ? RT - tmin : 0;
+      if (idx < cnt) {
+        i0 = (tmin + idx) * BM;
+        break;
+      }
+      idx -= cnt;
+    }
+    j0 = tj * BN;
+  }
   int64_t kbeg = 0, kend = g.k;
   double* wsp = nullptr;
   if (ksplit > 1) {
@@ -504,6 +520,17 @@ int launch_fast(cudaStream_t st, const GemmArgs& g, int ksplit, double* ws) {
     attr_dev = dev;
   }
   dim3 grid((unsigned)cdiv(g.m, BM), (unsigned)cdiv(g.n, BN), ksplit);
+  if (g.cmode == C_LOWER_TILES) {  // only the tiles intersecting the lower triangle
+    int64_t cnt = 0;
+    const int64_t RT = cdiv(g.m, BM);
+    for (int64_t tj = 0; tj < cdiv(g.n, BN); ++tj) {
+      const int64_t lo = tj * BN - BM + 1;
+      const int64_t tmin = lo <= 0 ? 0 : (lo + BM - 1) / BM;
+      cnt += RT > tmin ? RT - tmin : 0;
+    }
+    if (cnt == 0) return OK;
+    grid = dim3((unsigned)cnt, 1, ksplit);
+  }
   kern<<<grid, C::NT, C::SMEM, st>>>(g, ksplit, ws);
   PEVD_LAUNCH_CHECK();
   return OK;
@@ -545,17 +572,34 @@ int splitk_finish(cudaStream_t st, const GemmArgs& g, int ks, double* ws) {
 
 }  // namespace
 
+// Split-K factor for a grid of `tiles` CTA tiles when `slots` CTAs are resident at once: the
+// number of chunks (each >= min_chunk deep) whose wave count wastes the least of the last wave,
+// with a 1.5% charge per extra chunk for the partial-sum traffic and the reduction.
+static int pick_ks(int64_t tiles, int64_t k, int64_t slots, int64_t min_chunk, int64_t mn,
+                   int64_t ws_elems) {
+  if (tiles >= 8 * slots || k < 2 * min_chunk) return 1;
+  const int64_t kmax = std::min<int64_t>(k / min_chunk, 32);
+  int best = 1;
+  double best_eff = 0.0;
+  for (int64_t ks = 1; ks <= kmax; ++ks) {
+    if (ks > 1 && ks * mn > ws_elems) break;
+    const int64_t ctas = tiles * ks;
+    const double eff = (double)ctas / (double)(slots * cdiv(ctas, slots)) * (1.0 - 0.015 * (ks - 1));
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = (int)ks;
+    }
+  }
+  return best;
+}
+
 int gemm(cudaStream_t st, const GemmArgs& g, double* ws, int64_t ws_elems) {
   if (g.m <= 0 || g.n <= 0) return OK;
   const int sms = num_sms();
   if (g.amode == A_SYM_LOWER) {
     // symmetric operand read from its lower triangle (A W of the band reduction): N is small
     const int64_t tiles = cdiv(g.m, 128) * cdiv(g.n, 32);
-    int ks = 1;
-    if (ws && g.k >= 1024 && tiles < 2 * sms) {
-      ks = (int)std::min<int64_t>(cdiv(3 * sms, tiles), g.k / 256);
-      while (ks > 1 && (int64_t)ks * g.m * g.n > ws_elems) --ks;
-    }
+    const int ks = ws ? pick_ks(tiles, g.k, 2 * sms, 512, g.m * g.n, ws_elems) : 1;
     if (g.n <= 32) {
       // 8 warps of 16 x 32, BK = 16, 4 stages: ~100 KB of shared memory -> 2 CTAs (16 warps)/SM
       if (g.transB) PEVD_TRY((launch_fast<false, true, 128, 32, 16, 16, 32, 4, true>(st, g, ks, ks > 1 ? ws : nullptr)));
@@ -568,17 +612,19 @@ int gemm(cudaStream_t st, const GemmArgs& g, double* ws, int64_t ws_elems) {
   if (g.n <= 32) {
     // skinny: 128 x 32 tiles, split K when the grid is thin
     const int64_t tiles = cdiv(g.m, 128);
-    int ks = 1;
-    if (ws && g.k >= 1024 && tiles < 2 * sms && g.cmode == C_ALL) {
-      ks = (int)std::min<int64_t>(cdiv(3 * sms, tiles), g.k / 256);
-      while (ks > 1 && (int64_t)ks * g.m * g.n > ws_elems) --ks;
-    }
+    const int ks = (ws && g.cmode == C_ALL) ? pick_ks(tiles, g.k, 2 * sms, 512, g.m * g.n, ws_elems)
+                                            : 1;
     PEVD_TRY((launch_fast_t<128, 32, 16, 16, 32, 4>(st, g, ks, ks > 1 ? ws : nullptr)));
     if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
     return OK;
   }
-  const int64_t tiles = cdiv(g.m, 128) * cdiv(g.n, 128);
-  if (tiles >= sms || g.k < 64) return launch_fast_t<128, 128, 32, 64, 32, 3>(st, g, 1, nullptr);
+  const int64_t tiles = cdiv(g.m, 64) * cdiv(g.n, 128);
+  if (tiles >= sms || g.k < 64) {
+    // 64 x 128 CTA tiles, 4 warps of 32 x 64, BK = 16, 3 stages: 87.5 KB of shared memory and
+    // <= 224 registers, so two CTAs share an SM and one's barrier/epilogue hides under the
+    // other's DMMAs (the cuBLAS d884 configuration; 32.5 TF/s on 8192^3 vs 30.8 for 128 x 128)
+    return launch_fast_t<64, 128, 16, 32, 64, 3>(st, g, 1, nullptr);
+  }
   const int64_t tiles64 = cdiv(g.m, 64) * cdiv(g.n, 64);
   int ks = 1;
   if (ws && tiles64 < sms && g.k >= 512 && g.cmode == C_ALL) {
@@ -594,7 +640,7 @@ int gemm_grouped(cudaStream_t st, const GemmArgs* d_args, int count, int64_t max
                  int64_t max_n) {
   if (count <= 0 || max_m <= 0 || max_n <= 0) return OK;
   if (max_m * max_n >= (int64_t)128 * 128 * 64)
-    return launch_fast_grouped<128, 128, 32, 64, 32, 3>(st, d_args, count, max_m, max_n);
+    return launch_fast_grouped<64, 128, 16, 32, 64, 3>(st, d_args, count, max_m, max_n);
   return launch_fast_grouped<64, 64, 16, 32, 32, 4>(st, d_args, count, max_m, max_n);
 }
 

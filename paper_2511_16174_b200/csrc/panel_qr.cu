@@ -129,17 +129,23 @@ __global__ void __launch_bounds__(QR_THREADS)
     // ---- deterministic reduction of all CTA partials (identical in every CTA)
     {
       const int vi = tid % NVAL, grp = tid / NVAL;
-      // independent loads, four accumulators: the L2 round trips overlap instead of chaining
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      unsigned p = grp;
-      for (; p + 12 < ncta; p += 16) {
-        s0 += __ldcg(part + (int64_t)p * NVAL + vi);
-        s1 += __ldcg(part + (int64_t)(p + 4) * NVAL + vi);
-        s2 += __ldcg(part + (int64_t)(p + 8) * NVAL + vi);
-        s3 += __ldcg(part + (int64_t)(p + 12) * NVAL + vi);
+      // all of this thread's partials (CTAs grp, grp+4, ...) are loaded before any is summed:
+      // one L2 round trip per 40 CTAs instead of one per 16, in a fixed order
+      double acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+      for (unsigned base = grp; base < ncta; base += 160) {
+        double v[40];
+#pragma unroll
+        for (int q = 0; q < 40; ++q) {
+          const unsigned p = base + 4 * q;
+          v[q] = p < ncta ? __ldcg(part + (int64_t)p * NVAL + vi) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 40; ++q) acc[q & 7] += v[q];
       }
-      for (; p < ncta; p += 4) s0 += __ldcg(part + (int64_t)p * NVAL + vi);
-      red[grp * NVAL + vi] = (s0 + s1) + (s2 + s3);
+      red[grp * NVAL + vi] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) +
+                             ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     }
     __syncthreads();
     if (tid < NVAL) hv[tid] = red[tid] + red[NVAL + tid] + red[2 * NVAL + tid] + red[3 * NVAL + tid];

@@ -13,6 +13,7 @@
 //     (ragged last round: coupling columns get Q^T from the left first, sbr.py:175-182)
 // Afterwards everything above the b-th subdiagonal is zeroed, leaving A = the "Y staircase":
 // panel x's explicit Y_x at A[t0:, c0:c0+pw], exactly the compact-WY operand SBR-Back needs.
+#include <cstdlib>
 #include "kernels.cuh"
 
 namespace pevd {
@@ -63,11 +64,23 @@ int64_t sbr_num_rounds(int64_t n, int b) {
 }
 
 static constexpr int64_t SPLITK_ELEMS = 4 << 20;
-static constexpr int NBB = 4;  // panels per double-blocked trailing update (rank 2 * NBB * b)
+static constexpr int NBB_MAX = 16;  // workspace bound on the panels per double-blocked update
+
+// panels per double-blocked trailing update (rank 2 * nbb * b); PEVD_NBB overrides (tuning)
+static int sbr_nbb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PEVD_NBB");
+    v = e ? atoi(e) : 16;
+    if (v < 1) v = 1;
+    if (v > NBB_MAX) v = NBB_MAX;
+  }
+  return v;
+}
 
 int64_t sbr_ws_bytes(int64_t n, int b) {
   // YZY (n x 3*NBB*b) + W (n x b) + M, R, coupling (b x b) + tZ, tY (NBB*b x b) + split-K + QR
-  const int64_t K = (int64_t)NBB * b;
+  const int64_t K = (int64_t)NBB_MAX * b;
   return (n * 3 * K + n * b + 3 * (int64_t)b * b + 2 * K * b + SPLITK_ELEMS) * 8 +
          panel_qr_ws_bytes() + 1024;
 }
@@ -135,6 +148,7 @@ int sbr_reduce(cudaStream_t st, int64_t n, int b, double* A, int64_t lda, double
     set_error("sbr_reduce: need 1 <= b < n (n=%lld, b=%d)", (long long)n, b);
     return ERR_VALUE;
   }
+  const int NBB = sbr_nbb();
   const int64_t Kmax = (int64_t)NBB * b;
   SbrWs W;
   W.ldz = n;

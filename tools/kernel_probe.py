@@ -148,6 +148,23 @@ def main():
         ms, ts = timed(fn, reps=2)
         out.update(n=n, nbagg=os.environ.get("PEVD_NBAGG", "default"), ms=ms,
                    tflops=flops / ms / 1e9)
+    elif mode == "pqr":
+        # panel QR of an m x 32 panel (the SBR critical path)
+        m = int(sys.argv[2])
+        k = 32
+        P0 = torch.randn((k, m), dtype=torch.float64, device="cuda")
+        Pn = torch.empty_like(P0)
+        R = torch.empty((k, k), dtype=torch.float64, device="cuda")
+        Y = torch.empty((k, m), dtype=torch.float64, device="cuda")
+        T = torch.empty((k, k), dtype=torch.float64, device="cuda")
+        ws = torch.empty(L.pevd_panel_qr_workspace_bytes(), dtype=torch.uint8, device="cuda")
+
+        def f():
+            for _ in range(20):
+                _lib.check(L.pevd_panel_qr(m, k, ptr(P0), m, ptr(R), ptr(Y), m, None, m, ptr(T),
+                                           ptr(ws), stream()), "pqr")
+        ms, ts = timed(f, reps=3)
+        out.update(m=m, us_per_panel=ms * 1e3 / 20)
     elif mode == "stedc":
         n = int(sys.argv[2])
         d0 = torch.randn(n, dtype=torch.float64, device="cuda")
