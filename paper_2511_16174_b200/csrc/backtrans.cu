@@ -366,32 +366,30 @@ constexpr int WY_ROWS = 64;  // 8 warps x 8 rows
 constexpr int WY_THREADS = 256;
 // Shared-memory layouts, each conflict-free for its DMMA fragment pattern (a 64-bit warp access
 // is served per half-warp: lanes (r8 in 0..3, qd in 0..3) must hit 16 distinct 8-byte banks).
-// Both store reflector t (local index, shifted by its offset t % 8 inside its block of 8) at
-// window position p = (t % 8) + idx, zero outside [t % 8, t % 8 + 32):
-//  * va[h][t][s]:  P = X V operand, element p = 2 s + h  (lane reads t = tb + r8, s = 4 cc + qd:
-//                  address 20 r8 + qd -> pitch 20 = 4 mod 16)
-//  * vu[t][p]:     X += P2 V^T operand (lane reads t = tb + 2 qd + hh, p = 8 cc + r8:
-//                  address 84 qd + r8 -> pitch 42, 2 * 42 = 4 mod 16)
-//  * T[blk][s][t]: -T, pitch 10 (lane reads s = 2 qd + hh, t = r8: 20 qd + r8)
+// Window positions are relative to the block of 8 reflectors: reflector t (local index) covers
+// p = (t % 8) + idx, idx in [0, 32), so a block spans p in [0, 40).
+//  * va[h][t][s]:  P = X V operand, element p = 2 s + h of reflector t (zero outside its support;
+//                  lane reads t = tb + r8, s = 4 cc + qd: address 20 r8 + qd -> pitch 20)
+//  * zu[8 blk + s][p]: X += P Z^T operand, Z = V (-T)^T of the block (lane reads s = 2 qd + hh,
+//                  p = 8 cc + r8: address 84 qd + r8 -> pitch 42, 2 * 42 = 4 mod 16)
 constexpr int WY_PA = 20;
 constexpr int WY_PB = 42;
-constexpr int WY_TP = 10;
-constexpr int WY_PF = (Q4_SG * 32 + Q4_SG * 8) / WY_THREADS;  // prefetched doubles per thread
+constexpr int WY_ZB = 8 * 40;  // doubles of Z per block (8 rows s x 40 positions p)
 
 struct WySmem {
   double va[2][2][Q4_SG][WY_PA];  // [buf][h][t][s]
-  double vu[2][Q4_SG][WY_PB];     // [buf][t][p]
-  double T[2][Q4_SG / 8][8][WY_TP];  // -T per block, [buf][block][s][t]
+  double zu[2][Q4_SG][WY_PB];     // [buf][8 blk + s][p]
   int unit;
 };
 
-// -T of every block of 8 consecutive sweeps at every chase step.  Block (j, q) covers sweeps
-// 8q..8q+7 and lives at Tf + 64 * (tofs[j] + q).
+// Z = V (-T)^T of every block of 8 consecutive sweeps at every chase step, so that a block
+// acts as X <- X (I - V T V^T) = X + (X V) Z^T.  Block (j, q) covers sweeps 8q..8q+7; its Z
+// (row s = 0..7, window position p = 0..39) lives at Zf + 320 * (tofs[j] + q) + 40 s + p.
 template <bool BACKWARD>
 __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
                                   const double* __restrict__ V, int vld,
                                   const int64_t* __restrict__ tofs, int64_t jcount,
-                                  double* __restrict__ Tf) {
+                                  double* __restrict__ Zf) {
   // forward:  H_0 H_1 ... H_7 = I - V T V^T, T upper (LAPACK larft 'F')
   // backward: H_7 H_6 ... H_0 = I - V T V^T, T lower (larft 'B')
   constexpr int B = 32;
@@ -464,11 +462,21 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
         }
       }
     }
-    double* out = Tf + id * 64;
+    // Z[p][s] = sum_t v_t[p - t] * (-T)[s][t]
+    double* out = Zf + id * WY_ZB;
+#pragma unroll 1
+    for (int p = 0; p < 40; ++p) {
+      double vp[8];
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
+      for (int t = 0; t < 8; ++t) vp[t] = (p - t >= 0 && p - t < B) ? v[t][p - t] : 0.0;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) out[s * 8 + t] = -T[s][t];
+      for (int s2 = 0; s2 < 8; ++s2) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc = fma(vp[t], -T[s2][t], acc);
+        out[s2 * 40 + p] = acc;
+      }
+    }
   }
 }
 
@@ -481,7 +489,7 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
 template <bool LEFT>
 __global__ void __launch_bounds__(WY_THREADS, 2)
     bc_back_wy_kernel(int64_t n, const double* __restrict__ V, int vld,
-                      const double* __restrict__ Tf, const int64_t* __restrict__ tofs, double* X,
+                      const double* __restrict__ Zf, const int64_t* __restrict__ tofs, double* X,
                       int64_t ldx, int64_t nrows, int* counter, int* progress, int64_t nunits,
                       int nrb) {
   extern __shared__ __align__(16) unsigned char wyraw[];
@@ -490,44 +498,33 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qd = lane & 3, r8 = lane >> 2;
   const int64_t nsw = n - 2;
-  // zero everything once: the positions outside each reflector's support are never written
-  for (int e = tid; e < (int)(sizeof(WySmem) / 8) - 1; e += WY_THREADS) (&S.va[0][0][0][0])[e] = 0.0;
+  // zero va once: the positions outside each reflector's support are never written
+  for (int e = tid; e < 2 * 2 * Q4_SG * WY_PA; e += WY_THREADS) (&S.va[0][0][0][0])[e] = 0.0;
   __syncthreads();
-  // prefetch registers: element e = tid + p * WY_THREADS; e < 2048: V(t = e/32, r = e%32),
-  // else -T (block = (e-2048)/64, entry (e-2048)%64)
-  auto fetch = [&](int64_t i0, int64_t j, double* pf) {
+  // stage step j of sweep group i0 into buffer buf with cp.async (zero-filled past the last sweep)
+  auto issue = [&](int buf, int64_t i0, int64_t j) {
     const int64_t off = bc_slot_offset_dev(n, B, j);
     const int64_t nsw_j = n - 2 - j * B;
-    const int64_t tb = tofs[j] + i0 / 8;
 #pragma unroll
-    for (int p = 0; p < WY_PF; ++p) {
+    for (int p = 0; p < Q4_SG * B / WY_THREADS; ++p) {
       const int e = tid + p * WY_THREADS;
-      if (e < Q4_SG * B) {
-        const int t = e >> 5, r = e & 31;
-        const int64_t i = i0 + t;
-        pf[p] = (i < nsw_j) ? __ldg(V + (off + i) * vld + r) : 0.0;
-      } else {
-        const int e2 = e - Q4_SG * B;
-        const int blk = e2 >> 6;
-        pf[p] = (i0 + 8 * blk < nsw_j) ? __ldg(Tf + (tb + blk) * 64 + (e2 & 63)) : 0.0;
+      const int t = e >> 5, r = e & 31, pos = r + (t & 7);
+      const bool ok = i0 + t < nsw_j;
+      cp_async8(&S.va[buf][pos & 1][t][pos >> 1], ok ? V + (off + i0 + t) * vld + r : V, ok);
+    }
+    const int64_t zb = tofs[j] + i0 / 8;
+#pragma unroll
+    for (int p = 0; p < (Q4_SG * 40 / 2 + WY_THREADS - 1) / WY_THREADS; ++p) {
+      const int e = tid + p * WY_THREADS;  // 16-byte chunk: row = 8 blk + s, 20 chunks a row
+      if (e < Q4_SG * 20) {
+        const int row = e / 20, ch = e % 20, blk = row >> 3;
+        const bool ok = i0 + 8 * blk < nsw_j;
+        cp_async16(&S.zu[buf][row][2 * ch],
+                   ok ? Zf + (zb + blk) * WY_ZB + (row & 7) * 40 + 2 * ch : Zf, ok);
       }
     }
+    cp_async_commit();
   };
-  auto stage = [&](int buf, const double* pf) {
-#pragma unroll
-    for (int p = 0; p < WY_PF; ++p) {
-      const int e = tid + p * WY_THREADS;
-      if (e < Q4_SG * B) {
-        const int t = e >> 5, pos = (e & 31) + (t & 7);
-        S.va[buf][pos & 1][t][pos >> 1] = pf[p];
-        S.vu[buf][t][pos] = pf[p];
-      } else {
-        const int e2 = e - Q4_SG * B;
-        S.T[buf][e2 >> 6][(e2 >> 3) & 7][e2 & 7] = pf[p];
-      }
-    }
-  };
-  (void)nsw;
   for (;;) {
     if (tid == 0) S.unit = atomicAdd(counter, 1);
     __syncthreads();
@@ -553,8 +550,8 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
     const int64_t jmax = (n - 3 - i0) / B;
     const int64_t jfirst = LEFT ? 0 : jmax;
     int64_t ws = i0 + 1 + jfirst * B;
-    double pf[WY_PF];
-    fetch(i0, jfirst, pf);
+    int buf = 0;
+    issue(buf, i0, jfirst);
     __syncthreads();  // progress acquired by tid 0 before anyone reads X
     double w[12][2];
 #pragma unroll
@@ -564,13 +561,13 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
         const int64_t col = ws + 8 * c + 2 * qd + h;
         w[c][h] = (active && col < n) ? __ldcg(x + col * cs) : 0.0;
       }
-    int buf = 0;
-    stage(buf, pf);
+    cp_async_wait<0>();
     __syncthreads();
     for (int64_t jj = 0; jj <= jmax; ++jj) {
       const int64_t j = LEFT ? jj : jmax - jj;
       const bool more = jj < jmax;
-      // prefetch the next step: its new window columns and its V / -T
+      // prefetch the next step: its new window columns (registers) and its V / Z (other buffer:
+      // the barrier that ended the previous step means nobody still reads it)
       double nx[4][2];
       const int64_t nbase = LEFT ? ws + 3 * B : ws - B;
 #pragma unroll
@@ -580,8 +577,8 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
           const int64_t col = nbase + 8 * c + 2 * qd + h;
           nx[c][h] = (more && active && col < n) ? __ldcg(x + col * cs) : 0.0;
         }
-      if (more) fetch(i0, LEFT ? j + 1 : j - 1, pf);
-      // ---- apply the 8 blocks of this step
+      if (more) issue(buf ^ 1, i0, LEFT ? j + 1 : j - 1);
+      // ---- apply the 8 blocks of this step: P = X V (10 DMMA), X += P Z^T (10 DMMA)
 #pragma unroll
       for (int bb = 0; bb < Q4_SG / 8; ++bb) {
         const int blk = LEFT ? Q4_SG / 8 - 1 - bb : bb;
@@ -596,15 +593,12 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
         }
         p0 += e0;
         p1 += e1;
-        double q0 = 0.0, q1 = 0.0;
-        dmma884(q0, q1, p0, S.T[buf][blk][2 * qd][r8]);
-        dmma884(q0, q1, p1, S.T[buf][blk][2 * qd + 1][r8]);
+        const double* z0 = &S.zu[buf][tb + 2 * qd][r8];
+        const double* z1 = &S.zu[buf][tb + 2 * qd + 1][r8];
 #pragma unroll
         for (int cc = 0; cc < 5; ++cc) {
-          const double va = S.vu[buf][tb + 2 * qd][8 * cc + r8];
-          const double vb = S.vu[buf][tb + 2 * qd + 1][8 * cc + r8];
-          dmma884(w[blk + cc][0], w[blk + cc][1], q0, va);
-          dmma884(w[blk + cc][0], w[blk + cc][1], q1, vb);
+          dmma884(w[blk + cc][0], w[blk + cc][1], p0, z0[8 * cc]);
+          dmma884(w[blk + cc][0], w[blk + cc][1], p1, z1[8 * cc]);
         }
       }
       // ---- slide by b = 32 (4 tiles): the trailing 4 tiles (right) / leading 4 tiles (left)
@@ -652,7 +646,6 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
           }
           ws += B;
         }
-        stage(buf ^ 1, pf);  // the other buffer: nobody reads it during this step
       } else {
 #pragma unroll
         for (int c = 0; c < 12; ++c) {
@@ -665,6 +658,7 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
         }
       }
       buf ^= 1;
+      cp_async_wait<0>();
       __syncthreads();
     }
     if (tid == 0) {
@@ -887,7 +881,8 @@ int64_t bc_back_ws_bytes(int64_t n, int64_t nrows) {
   const int64_t jcount = n >= 3 ? (n - 3) / 32 + 1 : 1;
   int64_t nblk = 0;
   for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(std::max<int64_t>(n - 2 - j * 32, 0), 8);
-  return ((nrows / 32 + 64) * 4 + 255) / 256 * 256 + (jcount + 2) * 8 + nblk * 64 * 8 + 256;
+  return ((nrows / 32 + 64) * 4 + 255) / 256 * 256 + ((jcount + 2) * 8 + 255) / 256 * 256 +
+         nblk * (int64_t)WY_ZB * 8 + 256;
 }
 
 int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
@@ -909,7 +904,7 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
     int* progress = counter + 32;
     const int64_t jcount = (n - 3) / 32 + 1;
     int64_t* tofs = (int64_t*)((char*)ws + ((nrows / 32 + 64) * 4 + 255) / 256 * 256);
-    double* Tf = (double*)(tofs + jcount + 2);
+    double* Tf = (double*)((char*)tofs + ((jcount + 2) * 8 + 255) / 256 * 256);
     PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
     if (wy) {
       std::vector<int64_t> h(jcount + 1);
@@ -978,7 +973,7 @@ int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const dou
     int* progress = counter + 32;
     const int64_t jcount = (n - 3) / 32 + 1;
     int64_t* tofs = (int64_t*)((char*)ws + ((ncols / 32 + 64) * 4 + 255) / 256 * 256);
-    double* Tf = (double*)(tofs + jcount + 2);
+    double* Tf = (double*)((char*)tofs + ((jcount + 2) * 8 + 255) / 256 * 256);
     PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
     std::vector<int64_t> h(jcount + 1);
     h[0] = 0;
