@@ -601,9 +601,10 @@ int gemm(cudaStream_t st, const GemmArgs& g, double* ws, int64_t ws_elems) {
     const int64_t tiles = cdiv(g.m, 128) * cdiv(g.n, 32);
     const int ks = ws ? pick_ks(tiles, g.k, 2 * sms, 512, g.m * g.n, ws_elems) : 1;
     if (g.n <= 32) {
-      // 8 warps of 16 x 32, BK = 16, 4 stages: ~100 KB of shared memory -> 2 CTAs (16 warps)/SM
-      if (g.transB) PEVD_TRY((launch_fast<false, true, 128, 32, 16, 16, 32, 4, true>(st, g, ks, ks > 1 ? ws : nullptr)));
-      else PEVD_TRY((launch_fast<false, false, 128, 32, 16, 16, 32, 4, true>(st, g, ks, ks > 1 ? ws : nullptr)));
+      // 4 warps of 32 x 32, BK = 16, 3 stages: 79 KB of shared memory -> 2 CTAs/SM; 8 LDS per
+      // 16 DMMA (27-28 TF/s at m = 24576-49152 vs 23-24 for 8 warps of 16 x 32)
+      if (g.transB) PEVD_TRY((launch_fast<false, true, 128, 32, 16, 32, 32, 3, true>(st, g, ks, ks > 1 ? ws : nullptr)));
+      else PEVD_TRY((launch_fast<false, false, 128, 32, 16, 32, 32, 3, true>(st, g, ks, ks > 1 ? ws : nullptr)));
       if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
       return OK;
     }
