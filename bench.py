@@ -231,6 +231,14 @@ def run_b200_single(args):
         ms = float(t.item())
     value = world * 4 * n ** 3 / (ms * 1e-3) / 1e12
 
+    # accuracy of the last step's result on the device (outside the timed region; verification):
+    # north-star residual ||A Q - Q Lam||_F / (n ||A||_F) and orthogonality ||Q^T Q - I||_F / n
+    accuracy = None
+    if not args.no_check:
+        from paper_2511_16174_b200 import matgen
+        res, orth = matgen.accuracy(a0, lam, q)
+        accuracy = {"residual": res, "orthogonality": orth, "bound": 1e-12,
+                    "pass": bool(res <= 1e-12 and orth <= 1e-12)}
     # stage breakdown of the last step (CUDA events on the launching streams, inside the lib)
     st = stats[-1]
     stage_ms = {k: getattr(st, k + "_ms")[1] - getattr(st, k + "_ms")[0]
@@ -290,6 +298,7 @@ def run_b200_single(args):
                            "l2": "input 8n^2 = %.1f GB >> 126 MB L2 (no flush needed)" % (8 * n * n / 1e9),
                            "flop_convention": "4 n^3 / wall (PAPER.md:92)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "accuracy": accuracy,
                 "gpu_launches": int(launches), "impl": "b200"}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -370,6 +379,7 @@ def main():
     ap.add_argument("--ref-n", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip the residual/orthogonality check")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
