@@ -486,7 +486,7 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
 // LEFT = true:  X <- Q_b X, done as Y <- Y Q_b^T on the rows of Y = X^T (element (row, col) at
 //   X[row*ldx + col]): groups descending, steps top-to-bottom, sweeps descending, backward T
 //   (the conventional grouped order of backtrans.py:232-235).
-template <bool LEFT>
+template <bool LEFT, bool ONECHAIN = false>
 __global__ void __launch_bounds__(WY_THREADS, 2)
     bc_back_wy_kernel(int64_t n, const double* __restrict__ V, int vld,
                       const double* __restrict__ Zf, const int64_t* __restrict__ tofs, double* X,
@@ -589,10 +589,13 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
 #pragma unroll
         for (int cc = 0; cc < 5; ++cc) {
           dmma884(p0, p1, w[blk + cc][0], v0[4 * cc]);
-          dmma884(e0, e1, w[blk + cc][1], v1[4 * cc]);
+          if (ONECHAIN) dmma884(p0, p1, w[blk + cc][1], v1[4 * cc]);
+          else dmma884(e0, e1, w[blk + cc][1], v1[4 * cc]);
         }
-        p0 += e0;
-        p1 += e1;
+        if (!ONECHAIN) {
+          p0 += e0;
+          p1 += e1;
+        }
         const double* z0 = &S.zu[buf][tb + 2 * qd][r8];
         const double* z1 = &S.zu[buf][tb + 2 * qd + 1][r8];
 #pragma unroll
@@ -1000,6 +1003,17 @@ int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const dou
       return ERR_CUDA;
     }
     const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
+    static int onechain = -1;
+    if (onechain < 0) {
+      const char* e = getenv("PEVD_WYCHAIN");
+      onechain = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (onechain) {
+      PEVD_CUDA(cudaFuncSetAttribute(bc_back_wy_kernel<true, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      bc_back_wy_kernel<true, true><<<(unsigned)grid, WY_THREADS, smem, st>>>(
+          n, V, vld, Tf, tofs, X, ldx, ncols, counter, progress, nunits, nrb);
+    } else
     bc_back_wy_kernel<true><<<(unsigned)grid, WY_THREADS, smem, st>>>(
         n, V, vld, Tf, tofs, X, ldx, ncols, counter, progress, nunits, nrb);
     PEVD_LAUNCH_CHECK();

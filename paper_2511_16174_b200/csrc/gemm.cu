@@ -333,7 +333,7 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
   double acc[C::MI][C::NI][2];
   // beta != 0: start the accumulators at (beta/alpha) C, so the epilogue is a plain store and the
   // C reads overlap the pipeline prologue instead of trailing the (short-K) main loop
-  const bool preload = (ws_out == nullptr) && g.beta != 0.0 && g.alpha != 0.0;
+  const bool preload = (ws_out == nullptr) && g.beta != 0.0 && g.alpha != 0.0 && g.preload;
   {
     const double sc = preload ? g.beta / g.alpha : 0.0;
     const int r_in = lane >> 2, c_in = 2 * (lane & 3);
@@ -428,6 +428,47 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
   cp_async_wait<0>();
   __syncthreads();
   const int r_in = lane >> 2, c_in = 2 * (lane & 3);
+  constexpr int LDC = BM + 2;  // staged tile pitch: 8 rows x 4 column pairs hit distinct banks
+  if (ws_out == nullptr && !preload && BN * LDC <= STAGES * (C::A_STAGE + C::B_STAGE)) {
+    // Epilogue through shared memory: the accumulators are staged as a column-major tile, then
+    // every warp streams whole columns (BM contiguous rows) of C with 16-byte accesses, reading
+    // C (beta != 0) and writing the result in full lines.
+    double* Cs = smem;
+#pragma unroll
+    for (int a = 0; a < C::MI; ++a)
+#pragma unroll
+      for (int b = 0; b < C::NI; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          Cs[(wn * WN + b * 8 + c_in + h) * LDC + wm * WM + a * 8 + r_in] = acc[a][b][h];
+    __syncthreads();
+    const bool vec = ((uintptr_t)g.C % 16 == 0) && (g.ldc % 2 == 0);
+    constexpr int PAIRS = BM / 2;
+    for (int e = tid; e < BN * PAIRS; e += C::NT) {
+      const int col = e / PAIRS, rp = (e % PAIRS) * 2;
+      const int64_t gj = j0 + col, gi = i0 + rp;
+      if (gj >= g.n || gi >= g.m) continue;
+      const int64_t cj = g.cmap ? (int64_t)g.cmap[gj] : gj;
+      double* cp = g.C + gi + cj * g.ldc;
+      const double v0 = g.alpha * Cs[col * LDC + rp], v1 = g.alpha * Cs[col * LDC + rp + 1];
+      if (vec && gi + 1 < g.m) {
+        double2 o;
+        if (g.beta != 0.0) {
+          const double2 c = *reinterpret_cast<const double2*>(cp);
+          o.x = v0 + g.beta * c.x;
+          o.y = v1 + g.beta * c.y;
+        } else {
+          o.x = v0;
+          o.y = v1;
+        }
+        *reinterpret_cast<double2*>(cp) = o;
+      } else {
+        cp[0] = (g.beta == 0.0) ? v0 : v0 + g.beta * cp[0];
+        if (gi + 1 < g.m) cp[1] = (g.beta == 0.0) ? v1 : v1 + g.beta * cp[1];
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int a = 0; a < C::MI; ++a) {
     const int64_t gi = i0 + wm * WM + a * 8 + r_in;
@@ -593,8 +634,15 @@ static int pick_ks(int64_t tiles, int64_t k, int64_t slots, int64_t min_chunk, i
   return best;
 }
 
-int gemm(cudaStream_t st, const GemmArgs& g, double* ws, int64_t ws_elems) {
-  if (g.m <= 0 || g.n <= 0) return OK;
+int gemm(cudaStream_t st, const GemmArgs& g0, double* ws, int64_t ws_elems) {
+  if (g0.m <= 0 || g0.n <= 0) return OK;
+  static int pre = -1;
+  if (pre < 0) {
+    const char* e = getenv("PEVD_PRELOAD");
+    pre = e ? atoi(e) : 0;
+  }
+  GemmArgs g = g0;
+  g.preload = pre;
   const int sms = num_sms();
   if (g.amode == A_SYM_LOWER) {
     // symmetric operand read from its lower triangle (A W of the band reduction): N is small

@@ -27,6 +27,7 @@ struct GemmArgs {
   int amode, cmode;
   const int* amap;  // optional: column j of op(A) is column amap[j] of A (transA == 0 only)
   const int* cmap;  // optional: column j of the product is written to column cmap[j] of C
+  int preload = 1;  // beta != 0: start the accumulators at (beta/alpha) C (else read C at the end)
 };
 
 // Single GEMM on `stream`; `ws`/`ws_elems` optional split-K workspace (nullptr -> no split-K).

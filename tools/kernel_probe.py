@@ -88,6 +88,7 @@ def main():
         m, n, k = (int(x) for x in sys.argv[2:5])
         ta = int(sys.argv[5]) if len(sys.argv) > 5 else 0
         tb = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+        beta = float(sys.argv[7]) if len(sys.argv) > 7 else 0.0
         A = torch.randn(m * k, dtype=torch.float64, device="cuda")
         B = torch.randn(k * n, dtype=torch.float64, device="cuda")
         C = torch.zeros(m * n, dtype=torch.float64, device="cuda")
@@ -95,7 +96,7 @@ def main():
         lda = k if ta else m
         ldb = n if tb else k
         ms, ts = timed(lambda: _lib.check(L.pevd_dgemm(ta, tb, m, n, k, 1.0, ptr(A), lda, ptr(B), ldb,
-                                                       0.0, ptr(C), m, ptr(ws), ws.numel(), stream()),
+                                                       beta, ptr(C), m, ptr(ws), ws.numel(), stream()),
                                           "gemm"), reps=5)
         out.update(m=m, n=n, k=k, ms=ms, tflops=2.0 * m * n * k / ms / 1e9)
     elif mode == "symm":
