@@ -248,9 +248,17 @@ def run_b200_single(args):
     peaks = load_fp64_peaks()
     peak = peaks["dmma"]  # every GEMM-like stage (BC-Back included) runs on DMMA
     achieved = fl[dom] / (stage_ms[dom] * 1e-3) / 1e12
+    traffic, traffic_src = None, None
+    try:  # dram bytes of that kernel's launch from the committed ncu capture (same n only)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json"))).get(dom)
+        if tr and tr.get("n") == n:
+            traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+            traffic_src = "profiles/r01_traffic.json (ncu dram__bytes_read+write, one launch)"
+    except Exception:
+        pass
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3),
                 "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                "traffic": None,
+                "traffic": traffic, "traffic_source": traffic_src,
                 "peak_source": "FP64 DMMA (mma.sync m8n8k4) microbenchmark"
                                " on this pool's B200 (profiles/r01_fp64_peaks.json); "
                                "MEASURED_PEAKS.json has no FP64 entry",

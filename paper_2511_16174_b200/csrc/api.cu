@@ -155,9 +155,9 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     return ERR_VALUE;
   }
   cudaStream_t sb = nullptr;
-  const bool two_streams = want_vectors && order != PEVD_ORDER_SEQUENTIAL;
+  const bool two_streams = want_vectors && order == PEVD_ORDER_PIPELINED;
   if (two_streams) PEVD_CUDA(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
-  Ev ev[7];
+  Ev ev[6];
   for (auto& e : ev) {
     PEVD_CUDA(cudaEventCreate(&e.a));
     PEVD_CUDA(cudaEventCreate(&e.b));
@@ -178,6 +178,12 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     if ((rc = sbr_reduce(sm, n, b, A, lda, L.bands, want_vectors ? L.Tall : nullptr, L.ws_sbr)))
       break;
     cudaEventRecord(ev[0].b, sm);
+    // ---- conventional: the SBR-Back T aggregation (SBR output only, ~1% of the SBR-Back
+    //      flops) right here on the main stream: run beside the latency-bound chase it costs the
+    //      chase more than it saves
+    if (want_vectors && order == PEVD_ORDER_CONVENTIONAL) {
+      if ((rc = sbr_back_prepare(sm, n, b, A, L.Tall, L.ws_back))) break;
+    }
     // ---- BC first: its persistent CTAs must become resident before the SBR-Back GEMMs
     //      (enqueued next, on the back stream) fill the SMs
     cudaEventRecord(ev[1].a, sm);
@@ -185,13 +191,6 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
                         want_vectors ? L.V : nullptr, L.vld, L.ws_bc)))
       break;
     cudaEventRecord(ev[1].b, sm);
-    // ---- conventional: the SBR-Back T aggregation (SBR output only) on the side stream,
-    //      under the chase and the divide and conquer
-    if (want_vectors && order == PEVD_ORDER_CONVENTIONAL) {
-      cudaStreamWaitEvent(sb, ev[0].b, 0);
-      if ((rc = sbr_back_prepare(sb, n, b, A, L.Tall, L.ws_back))) break;
-      cudaEventRecord(ev[6].b, sb);
-    }
     // ---- SBR-Back (forms Q_s) overlapping the chase
     if (want_vectors && order != PEVD_ORDER_CONVENTIONAL) {
       if (two_streams) cudaStreamWaitEvent(sback, ev[0].b, 0);
@@ -219,7 +218,6 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
         cudaEventRecord(ev[4].a, sm);
         if ((rc = bc_back_left(sm, n, b, L.tau, L.V, L.vld, L.Qd, n, n, L.ws_bcb))) break;
         cudaEventRecord(ev[4].b, sm);
-        cudaStreamWaitEvent(sm, ev[6].b, 0);
         cudaEventRecord(ev[3].a, sm);
         if ((rc = sbr_back_apply_left(sm, n, b, A, L.Tall, L.Qd, n, n, L.ws_back, true))) break;
         cudaEventRecord(ev[3].b, sm);
