@@ -319,6 +319,25 @@ __device__ __forceinline__ void load_tile(double* sm, const double* base, int64_
   }
 }
 
+// load_tile for a tile known to lie inside the operand (no bounds, no gather, 16-byte chunks)
+template <int CL, int OL, int SLD, int NT>
+__device__ __forceinline__ void load_tile_inner(double* sm, const double* base, int64_t ld,
+                                                int64_t c0, int64_t o0, int tid) {
+  constexpr int CPR = CL / 2;
+  constexpr int TOT = CPR * OL;
+  constexpr int STEP = NT / CPR;
+  static_assert(NT % CPR == 0 && TOT % NT == 0, "tile/thread mismatch");
+  const int cc = (tid % CPR) * 2;
+  const int orow = tid / CPR;
+  const double* src = base + (c0 + cc) + (o0 + orow) * ld;
+  const int64_t sstep = (int64_t)STEP * ld;
+#pragma unroll
+  for (int i = 0; i < TOT / NT; ++i)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                     smem_u32(sm + (orow + i * STEP) * SLD + cc)),
+                 "l"(src + i * sstep));
+}
+
 template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int V,
           bool SYM = false>
 __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t j0, int64_t kbeg,
@@ -387,10 +406,25 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
       load_tile<BN, BK, C::B_LD, C::NT, V>(bs, g.B, g.ldb, j0, k0, g.n, kend, nullptr, tid);
   };
 
+  // interior tiles (the bulk of every large GEMM): unpredicated 16-byte copies
+  const bool inner = !SYM && V == 2 && g.amap == nullptr && i0 + BM <= g.m && j0 + BN <= g.n;
+  const int64_t kfull = kbeg + (kend - kbeg) / BK * BK;  // k-tiles below this are complete
+  auto load_stage_any = [&](int st, int64_t k0) {
+    if (inner && k0 + BK <= kfull) {
+      double* as = As + st * C::A_STAGE;
+      double* bs = Bs + st * C::B_STAGE;
+      if (!TA) load_tile_inner<BM, BK, C::A_LD, C::NT>(as, g.A, g.lda, i0, k0, tid);
+      else     load_tile_inner<BK, BM, C::A_LD, C::NT>(as, g.A, g.lda, k0, i0, tid);
+      if (!TB) load_tile_inner<BK, BN, C::B_LD, C::NT>(bs, g.B, g.ldb, k0, j0, tid);
+      else     load_tile_inner<BN, BK, C::B_LD, C::NT>(bs, g.B, g.ldb, j0, k0, tid);
+    } else {
+      load_stage(st, k0);
+    }
+  };
   const int64_t KT = (kend - kbeg + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(s, kbeg + s * BK);
+    if (s < KT) load_stage_any(s, kbeg + s * BK);
     cp_async_commit();
   }
   for (int64_t kt = 0; kt < KT; ++kt) {
@@ -398,7 +432,7 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
     __syncthreads();
     {
       const int64_t pf = kt + STAGES - 1;
-      if (pf < KT) load_stage((int)(pf % STAGES), kbeg + pf * BK);
+      if (pf < KT) load_stage_any((int)(pf % STAGES), kbeg + pf * BK);
       cp_async_commit();
     }
     const double* as = As + (kt % STAGES) * C::A_STAGE;
