@@ -273,11 +273,15 @@ template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, 
 struct FCfg {
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int NT = WARPS_M * WARPS_N * 32;
-  static constexpr int A_LD0 = BM + 4, A_LD1 = BK + 4;   // m-contiguous / k-contiguous layouts
+  // Fragment loads read the k-slot pair (k8 + 2q, k8 + 2q + 1) of lane q for two consecutive
+  // k-steps: one LDS.128 from a k-contiguous layout (pitch = 8 mod 16 doubles keeps a quarter
+  // warp's 16-byte accesses on distinct banks), two LDS.64 from an m/n-contiguous one (pitch =
+  // 2 mod 8 doubles: rows 2q apart land on distinct banks).
+  static constexpr int A_LD0 = BM + 2, A_LD1 = BK + 8;   // m-contiguous / k-contiguous layouts
   static constexpr int A_LD = TA ? A_LD1 : A_LD0;
   static constexpr int A_OUT = SYM ? (BK * A_LD0 > BM * A_LD1 ? BK : (BM * A_LD1 + A_LD0 - 1) / A_LD0)
                                    : (TA ? BM : BK);
-  static constexpr int B_LD = TB ? BN + 4 : BK + 4;
+  static constexpr int B_LD = TB ? BN + 2 : BK + 8;
   static constexpr int B_OUT = TB ? BK : BN;
   static constexpr int A_STAGE = A_OUT * A_LD, B_STAGE = B_OUT * B_LD;
   static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) * 8;
@@ -336,6 +340,26 @@ __device__ __forceinline__ void load_tile_inner(double* sm, const double* base, 
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
                      smem_u32(sm + (orow + i * STEP) * SLD + cc)),
                  "l"(src + i * sstep));
+}
+
+// load_tile_inner with the outer (k) index gathered through omap (the D&C merge's column map)
+template <int CL, int OL, int SLD, int NT>
+__device__ __forceinline__ void load_tile_inner_map(double* sm, const double* base, int64_t ld,
+                                                    int64_t c0, int64_t o0, const int* omap,
+                                                    int tid) {
+  constexpr int CPR = CL / 2;
+  constexpr int TOT = CPR * OL;
+  constexpr int STEP = NT / CPR;
+  const int cc = (tid % CPR) * 2;
+  const int orow = tid / CPR;
+  const double* src = base + (c0 + cc);
+#pragma unroll
+  for (int i = 0; i < TOT / NT; ++i) {
+    const int o = orow + i * STEP;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                     smem_u32(sm + o * SLD + cc)),
+                 "l"(src + (int64_t)__ldg(omap + o0 + o) * ld));
+  }
 }
 
 template <bool TA, bool TB, int BM, int BN, int BK, int WM, int WN, int STAGES, int V,
@@ -407,14 +431,23 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
   };
 
   // interior tiles (the bulk of every large GEMM): unpredicated 16-byte copies
-  const bool inner = !SYM && V == 2 && g.amap == nullptr && i0 + BM <= g.m && j0 + BN <= g.n;
+  const bool inner = V == 2 && (g.amap == nullptr || !TA) && i0 + BM <= g.m && j0 + BN <= g.n;
   const int64_t kfull = kbeg + (kend - kbeg) / BK * BK;  // k-tiles below this are complete
   auto load_stage_any = [&](int st, int64_t k0) {
-    if (inner && k0 + BK <= kfull) {
+    if (inner && k0 + BK <= kfull && (!SYM || sym_mode(k0) != 2)) {
       double* as = As + st * C::A_STAGE;
       double* bs = Bs + st * C::B_STAGE;
-      if (!TA) load_tile_inner<BM, BK, C::A_LD, C::NT>(as, g.A, g.lda, i0, k0, tid);
-      else     load_tile_inner<BK, BM, C::A_LD, C::NT>(as, g.A, g.lda, k0, i0, tid);
+      if (SYM) {  // a whole tile below (as stored) or above (its mirror) the diagonal
+        if (sym_mode(k0) == 0) load_tile_inner<BM, BK, C::A_LD0, C::NT>(as, g.A, g.lda, i0, k0, tid);
+        else load_tile_inner<BK, BM, C::A_LD1, C::NT>(as, g.A, g.lda, k0, i0, tid);
+      } else if (!TA) {
+        if (g.amap)
+          load_tile_inner_map<BM, BK, C::A_LD, C::NT>(as, g.A, g.lda, i0, k0, g.amap, tid);
+        else
+          load_tile_inner<BM, BK, C::A_LD, C::NT>(as, g.A, g.lda, i0, k0, tid);
+      } else {
+        load_tile_inner<BK, BM, C::A_LD, C::NT>(as, g.A, g.lda, k0, i0, tid);
+      }
       if (!TB) load_tile_inner<BK, BN, C::B_LD, C::NT>(bs, g.B, g.ldb, k0, j0, tid);
       else     load_tile_inner<BN, BK, C::B_LD, C::NT>(bs, g.B, g.ldb, j0, k0, tid);
     } else {
@@ -440,23 +473,40 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
     const int r8 = lane >> 2, c4 = lane & 3;
     const bool a_kc = SYM ? (sym_mode(kbeg + kt * BK) == 1) : TA;  // k-contiguous A layout
 #pragma unroll
-    for (int k4 = 0; k4 < BK; k4 += 4) {
-      const int kr = k4 + c4;
-      double af[C::MI], bf[C::NI];
+    for (int k8 = 0; k8 < BK; k8 += 8) {
+      const int kr = k8 + 2 * c4;  // k-step h of this pair uses k = kr + h in lane c4's slot
+      double af[2][C::MI], bf[2][C::NI];
 #pragma unroll
       for (int a = 0; a < C::MI; ++a) {
         const int r = wm * WM + a * 8 + r8;
-        af[a] = a_kc ? as[r * C::A_LD1 + kr] : as[kr * C::A_LD0 + r];
+        if (a_kc) {
+          const double2 t = *reinterpret_cast<const double2*>(as + r * C::A_LD1 + kr);
+          af[0][a] = t.x;
+          af[1][a] = t.y;
+        } else {
+          af[0][a] = as[kr * C::A_LD0 + r];
+          af[1][a] = as[(kr + 1) * C::A_LD0 + r];
+        }
       }
 #pragma unroll
       for (int b = 0; b < C::NI; ++b) {
         const int c = wn * WN + b * 8 + r8;
-        bf[b] = TB ? bs[kr * C::B_LD + c] : bs[c * C::B_LD + kr];
+        if (TB) {
+          bf[0][b] = bs[kr * C::B_LD + c];
+          bf[1][b] = bs[(kr + 1) * C::B_LD + c];
+        } else {
+          const double2 t = *reinterpret_cast<const double2*>(bs + c * C::B_LD + kr);
+          bf[0][b] = t.x;
+          bf[1][b] = t.y;
+        }
       }
 #pragma unroll
-      for (int a = 0; a < C::MI; ++a)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int b = 0; b < C::NI; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        for (int a = 0; a < C::MI; ++a)
+#pragma unroll
+          for (int b = 0; b < C::NI; ++b)
+            dmma884(acc[a][b][0], acc[a][b][1], af[h][a], bf[h][b]);
     }
   }
   cp_async_wait<0>();
@@ -697,7 +747,8 @@ int gemm(cudaStream_t st, const GemmArgs& g0, double* ws, int64_t ws_elems) {
     const int64_t tiles = cdiv(g.m, 128);
     const int ks = (ws && g.cmode == C_ALL) ? pick_ks(tiles, g.k, 2 * sms, 512, g.m * g.n, ws_elems)
                                             : 1;
-    PEVD_TRY((launch_fast_t<128, 32, 16, 16, 32, 4>(st, g, ks, ks > 1 ? ws : nullptr)));
+    // 8 warps of 16 x 32, BK = 16, 3 stages (<= 92 KB: 2 CTAs/SM); 31 TF/s at 49152 x 32 x 49152
+    PEVD_TRY((launch_fast_t<128, 32, 16, 16, 32, 3>(st, g, ks, ks > 1 ? ws : nullptr)));
     if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
     return OK;
   }
