@@ -176,3 +176,25 @@ def accuracy(A, lam, Q, block: int = 4096):
         orth2 += float(torch.sum(Rb * Rb))
     anorm = float(torch.linalg.norm(A))
     return (res2 ** 0.5) / (n * anorm), (orth2 ** 0.5) / n
+
+
+# ---------------------------------------------------------------- host generator (CLI `gen`)
+def random_orthogonal(n: int, seed) -> np.ndarray:
+    """Haar orthogonal matrix from a Philox stream (matgen.py:87-103): QR of a Gaussian matrix
+    with the signs of R's diagonal moved into Q (zero counts as +)."""
+    if n < 1:
+        raise ValueError("n >= 1 required")
+    ss = seed if isinstance(seed, np.random.SeedSequence) else np.random.SeedSequence(seed)
+    g = _philox(ss).standard_normal((n, n))
+    q, r = np.linalg.qr(g)
+    return np.asfortranarray(q * np.where(np.diag(r) < 0.0, -1.0, 1.0))
+
+
+def generate_host(spec: SpectrumSpec):
+    """(A, lam) exactly as the reference CLI's `gen` builds them (matgen.py:106-126): the basis
+    from the second child of the seed sequence, A = (V diag(lam) V^T + its transpose) / 2.
+    O(n^3) host work: the reference-compatible path for files; `generate` is the device one."""
+    lam = eigen_spectrum(spec)
+    v = random_orthogonal(spec.n, np.random.SeedSequence(spec.seed).spawn(2)[1])
+    a = (v * lam) @ v.T
+    return np.asfortranarray((a + a.T) / 2.0), lam
