@@ -23,7 +23,7 @@ namespace pevd {
 
 namespace {
 
-constexpr int NB_AGG_MAX = 16;  // workspace bound on the panels per aggregated SBR-Back block
+constexpr int NB_AGG_MAX = 32;  // workspace bound on the panels per aggregated SBR-Back block
 
 // panels per aggregated SBR-Back block (K = nb * b reflectors per compact-WY GEMM pass);
 // PEVD_NBAGG overrides the default for tuning probes

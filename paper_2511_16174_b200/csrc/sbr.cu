@@ -79,9 +79,9 @@ static int sbr_nbb() {
 }
 
 int64_t sbr_ws_bytes(int64_t n, int b) {
-  // YZY (n x 3*NBB*b) + W (n x b) + M, R, coupling (b x b) + tZ, tY (NBB*b x b) + split-K + QR
+  // P1, P2 (n x 2*NBB*b each) + W (n x b) + M, R, coupling (b x b) + t (2*NBB*b x b) + split-K + QR
   const int64_t K = (int64_t)NBB_MAX * b;
-  return (n * 3 * K + n * b + 3 * (int64_t)b * b + 2 * K * b + SPLITK_ELEMS) * 8 +
+  return (n * 4 * K + n * b + 3 * (int64_t)b * b + 2 * K * b + SPLITK_ELEMS) * 8 +
          panel_qr_ws_bytes() + 1024;
 }
 
@@ -133,15 +133,15 @@ int sbr_single_round(cudaStream_t st, int64_t n, int b, double* A, int64_t lda, 
 }  // namespace
 
 // Double-blocked band reduction.  A block of nbl <= NBB full panels (c0, t0 = c0 + b, m0 = n - t0)
-// keeps Y_p and Z_p (block-relative rows [0, m0), zero above their own start) in [Y | Z | Y];
-// for panel i of the block:
+// keeps Y_p and Z_p (block-relative rows [0, m0), zero above their own start) interleaved in
+// P1 = [Y_0 Z_0 Y_1 Z_1 ...] and P2 = [Z_0 Y_0 Z_1 Y_1 ...]; for panel i of the block:
 //   1. its columns (rows from the panel's diagonal block down) receive the pending updates of
-//      panels 0..i-1:  C -= Y_p Z_p^T + Z_p Y_p^T            (two skinny GEMMs)
+//      panels 0..i-1:  C -= Y_p Z_p^T + Z_p Y_p^T = P1 P2^T   (one skinny GEMM)
 //   2. panel QR; its band columns are now final
-//   3. AW_i = A_blockstart[t_i:, t_i:] W_i  - Y_p (Z_p^T W_i) - Z_p (Y_p^T W_i)
+//   3. AW_i = A_blockstart[t_i:, t_i:] W_i  - P1 (P2^T W_i)
 //   4. Z_i = AW_i - 1/2 Y_i (W_i^T AW_i)
 // then one rank-2*nbl*b update of the remaining trailing matrix (lower tiles):
-//   A[t0+(nbl-1)b:, same] -= [Y Z][Z Y]^T.
+//   A[t0+(nbl-1)b:, same] -= P1 P2^T.
 int sbr_reduce(cudaStream_t st, int64_t n, int b, double* A, int64_t lda, double* bands_ref,
                double* Tall, void* ws) {
   if (b < 1 || n < 2 || b >= n) {
@@ -153,7 +153,7 @@ int sbr_reduce(cudaStream_t st, int64_t n, int b, double* A, int64_t lda, double
   SbrWs W;
   W.ldz = n;
   W.YZY = (double*)ws;
-  W.Wb = W.YZY + n * 3 * Kmax;
+  W.Wb = W.YZY + n * 4 * Kmax;
   W.Mb = W.Wb + n * b;
   W.Rb = W.Mb + (int64_t)b * b;
   W.Cp = W.Rb + (int64_t)b * b;
@@ -177,59 +177,60 @@ int sbr_reduce(cudaStream_t st, int64_t n, int b, double* A, int64_t lda, double
     while (nbl < NBB && x + nbl < R && (n - b - (x + nbl) * b) >= b) ++nbl;
     const int64_t t0 = c0 + b, m0 = n - t0;
     const int64_t K = (int64_t)nbl * b;
-    double* Yb = W.YZY;            // [0, K)
-    double* Zb = W.YZY + K * ldz;  // [K, 2K)
-    double* Y3 = W.YZY + 2 * K * ldz;
+    // P1 = [Y_0 Z_0 Y_1 Z_1 ...], P2 = [Z_0 Y_0 Z_1 Y_1 ...] (block-relative rows [0, m0)):
+    // every sum over the block's panels, sum_q Y_q Z_q^T + Z_q Y_q^T, is then ONE GEMM
+    // P1[:, 0:2r] P2[:, 0:2r]^T with contiguous operands
+    double* P1 = W.YZY;
+    double* P2 = W.YZY + 2 * Kmax * ldz;
     // rows above each panel's start must read as zero
-    PEVD_CUDA(cudaMemset2DAsync(W.YZY, ldz * 8, 0, (size_t)K * 8, (size_t)(3 * K), st));
+    PEVD_CUDA(cudaMemset2DAsync(P1, ldz * 8, 0, (size_t)K * 8, (size_t)(2 * K), st));
+    PEVD_CUDA(cudaMemset2DAsync(P2, ldz * 8, 0, (size_t)K * 8, (size_t)(2 * K), st));
     for (int i = 0; i < nbl; ++i) {
       const int64_t ci = c0 + (int64_t)i * b, ti = t0 + (int64_t)i * b, mi = n - ti;
       const int64_t ri = (int64_t)i * b;
+      double* Yi = P1 + ri + (2 * ri) * ldz;      // Y_i slot of P1, from its start row
+      double* Zi = P1 + ri + (2 * ri + b) * ldz;  // Z_i slot of P1
       if (i >= 1) {
-        // 1. pending updates on the panel columns, rows [ci, n) = block rows [ri - b, m0)
+        // 1. pending updates on the panel columns, rows [ci, n) = block rows [ri - b, m0):
+        //    C -= sum_{q<i} Y_q Z_q^T + Z_q Y_q^T
         double* Cpan = A + ci + ci * lda;
-        const int64_t mc = mi + b;
-        GemmArgs g1{mc, b, ri, -1.0, 1.0, Yb + (ri - b), ldz, Zb + (ri - b), ldz, Cpan, lda,
-                    0, 1, A_GENERAL, C_ALL};
+        GemmArgs g1{mi + b, b, 2 * ri, -1.0, 1.0, P1 + (ri - b), ldz, P2 + (ri - b), ldz, Cpan,
+                    lda, 0, 1, A_GENERAL, C_ALL};
         PEVD_TRY(gemm(st, g1, W.sk, SPLITK_ELEMS));
-        GemmArgs g2{mc, b, ri, -1.0, 1.0, Zb + (ri - b), ldz, Yb + (ri - b), ldz, Cpan, lda,
-                    0, 1, A_GENERAL, C_ALL};
-        PEVD_TRY(gemm(st, g2, W.sk, SPLITK_ELEMS));
       }
-      // 2. panel QR (explicit Y into the staircase and into the block buffer)
+      // 2. panel QR (explicit Y into the staircase and into P1; P2 gets a copy)
       double* panel = A + ti + ci * lda;
       double* Tx = Tall ? Tall + (x + i) * (int64_t)b * b : nullptr;
-      double* Yi = Yb + ri + ri * ldz;
-      double* Zi = Zb + ri + ri * ldz;
       PEVD_TRY(panel_qr(st, mi, b, panel, lda, W.Rb, panel, lda, Yi, ldz, W.Wb, n, Tx, W.qrws));
+      PEVD_CUDA(cudaMemcpy2DAsync(P2 + ri + (2 * ri + b) * ldz, ldz * 8, Yi, ldz * 8, mi * 8, b,
+                                  cudaMemcpyDeviceToDevice, st));
       band_cols_from_panel<<<1, 256, 0, st>>>(n, b, ci, b, A, lda, W.Rb, bands_ref);
       PEVD_LAUNCH_CHECK();
-      // 3. AW_i into the Z slot
+      // 3. AW_i into the Z slot: A_blockstart W_i - sum_{q<i} (Y_q Z_q^T + Z_q Y_q^T) W_i
       GemmArgs g_aw{mi, b, mi, 1.0, 0.0, A + ti + ti * lda, lda, W.Wb, n, Zi, ldz, 0, 0,
                     A_SYM_LOWER, C_ALL};
       PEVD_TRY(gemm(st, g_aw, W.sk, SPLITK_ELEMS));
       if (i >= 1) {
-        GemmArgs gz{ri, b, mi, 1.0, 0.0, Zb + ri, ldz, W.Wb, n, W.tZ, ri, 1, 0, A_GENERAL, C_ALL};
-        PEVD_TRY(gemm(st, gz, W.sk, SPLITK_ELEMS));
-        GemmArgs gy{ri, b, mi, 1.0, 0.0, Yb + ri, ldz, W.Wb, n, W.tY, ri, 1, 0, A_GENERAL, C_ALL};
-        PEVD_TRY(gemm(st, gy, W.sk, SPLITK_ELEMS));
-        GemmArgs c1{mi, b, ri, -1.0, 1.0, Yb + ri, ldz, W.tZ, ri, Zi, ldz, 0, 0, A_GENERAL, C_ALL};
-        PEVD_TRY(gemm(st, c1, W.sk, SPLITK_ELEMS));
-        GemmArgs c2{mi, b, ri, -1.0, 1.0, Zb + ri, ldz, W.tY, ri, Zi, ldz, 0, 0, A_GENERAL, C_ALL};
-        PEVD_TRY(gemm(st, c2, W.sk, SPLITK_ELEMS));
+        GemmArgs gt{2 * ri, b, mi, 1.0, 0.0, P2 + ri, ldz, W.Wb, n, W.tZ, 2 * ri, 1, 0,
+                    A_GENERAL, C_ALL};                              // t = P2^T W_i
+        PEVD_TRY(gemm(st, gt, W.sk, SPLITK_ELEMS));
+        GemmArgs gc{mi, b, 2 * ri, -1.0, 1.0, P1 + ri, ldz, W.tZ, 2 * ri, Zi, ldz, 0, 0,
+                    A_GENERAL, C_ALL};                              // AW_i -= P1 t
+        PEVD_TRY(gemm(st, gc, W.sk, SPLITK_ELEMS));
       }
-      // 4. Z_i = AW_i - 1/2 Y_i (W_i^T AW_i)
+      // 4. Z_i = AW_i - 1/2 Y_i (W_i^T AW_i), then its copy in P2
       GemmArgs g_m{b, b, mi, 1.0, 0.0, W.Wb, n, Zi, ldz, W.Mb, b, 1, 0, A_GENERAL, C_ALL};
       PEVD_TRY(gemm(st, g_m, W.sk, SPLITK_ELEMS));
       GemmArgs g_z{mi, b, b, -0.5, 1.0, Yi, ldz, W.Mb, b, Zi, ldz, 0, 0, A_GENERAL, C_ALL};
       PEVD_TRY(gemm(st, g_z, W.sk, SPLITK_ELEMS));
+      PEVD_CUDA(cudaMemcpy2DAsync(P2 + ri + (2 * ri) * ldz, ldz * 8, Zi, ldz * 8, mi * 8, b,
+                                  cudaMemcpyDeviceToDevice, st));
     }
-    // copy of Y for the [Z Y] operand, then the block's rank-2K trailing update (lower tiles)
-    PEVD_CUDA(cudaMemcpy2DAsync(Y3, ldz * 8, Yb, ldz * 8, m0 * 8, K, cudaMemcpyDeviceToDevice, st));
+    // the block's rank-2K trailing update (lower tiles)
     const int64_t ru = (int64_t)(nbl - 1) * b;
     const int64_t mu = m0 - ru;
     double* Cu = A + (t0 + ru) + (t0 + ru) * lda;
-    GemmArgs g_u{mu, mu, 2 * K, -1.0, 1.0, Yb + ru, ldz, Zb + ru, ldz, Cu, lda, 0, 1, A_GENERAL,
+    GemmArgs g_u{mu, mu, 2 * K, -1.0, 1.0, P1 + ru, ldz, P2 + ru, ldz, Cu, lda, 0, 1, A_GENERAL,
                  C_LOWER_TILES};
     PEVD_TRY(gemm(st, g_u, nullptr, 0));
     c_end = c0 + K;
