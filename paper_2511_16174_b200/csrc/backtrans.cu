@@ -31,7 +31,7 @@ int nb_agg() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PEVD_NBAGG");
-    v = e ? atoi(e) : 16;
+    v = e ? atoi(e) : 32;
     if (v < 1) v = 1;
     if (v > NB_AGG_MAX) v = NB_AGG_MAX;
     while (v & (v - 1)) v &= v - 1;  // the recursive T merge pairs sibling blocks
