@@ -598,11 +598,11 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
         }
         const double* z0 = &S.zu[buf][tb + 2 * qd][r8];
         const double* z1 = &S.zu[buf][tb + 2 * qd + 1][r8];
+        // all five tiles' first k-step, then the second: two updates of a tile are 5 DMMAs apart
 #pragma unroll
-        for (int cc = 0; cc < 5; ++cc) {
-          dmma884(w[blk + cc][0], w[blk + cc][1], p0, z0[8 * cc]);
-          dmma884(w[blk + cc][0], w[blk + cc][1], p1, z1[8 * cc]);
-        }
+        for (int cc = 0; cc < 5; ++cc) dmma884(w[blk + cc][0], w[blk + cc][1], p0, z0[8 * cc]);
+#pragma unroll
+        for (int cc = 0; cc < 5; ++cc) dmma884(w[blk + cc][0], w[blk + cc][1], p1, z1[8 * cc]);
       }
       // ---- slide by b = 32 (4 tiles): the trailing 4 tiles (right) / leading 4 tiles (left)
       //      are final for this group
