@@ -374,7 +374,8 @@ constexpr int WY_THREADS = 256;
 //                  p = 8 cc + r8: address 84 qd + r8 -> pitch 42, 2 * 42 = 4 mod 16)
 constexpr int WY_PA = 20;
 constexpr int WY_PB = 42;
-constexpr int WY_ZB = 8 * 40;  // doubles of Z per block (8 rows s x 40 positions p)
+constexpr int WY_ZB = 8 * WY_PB;  // doubles of Z per block: 8 rows s x 42 (40 positions p + pad),
+                                   // the shared zu layout, so a step's 8 blocks copy linearly
 
 struct WySmem {
   double va[2][2][Q4_SG][WY_PA];  // [buf][h][t][s]
@@ -384,7 +385,7 @@ struct WySmem {
 
 // Z = V (-T)^T of every block of 8 consecutive sweeps at every chase step, so that a block
 // acts as X <- X (I - V T V^T) = X + (X V) Z^T.  Block (j, q) covers sweeps 8q..8q+7; its Z
-// (row s = 0..7, window position p = 0..39) lives at Zf + 320 * (tofs[j] + q) + 40 s + p.
+// (row s = 0..7, window position p = 0..39) lives at Zf + 336 * (tofs[j] + q) + 42 s + p.
 template <bool BACKWARD>
 __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
                                   const double* __restrict__ V, int vld,
@@ -474,7 +475,7 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
         double acc = 0.0;
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc = fma(vp[t], -T[s2][t], acc);
-        out[s2 * 40 + p] = acc;
+        out[s2 * WY_PB + p] = acc;
       }
     }
   }
@@ -502,25 +503,32 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
   for (int e = tid; e < 2 * 2 * Q4_SG * WY_PA; e += WY_THREADS) (&S.va[0][0][0][0])[e] = 0.0;
   __syncthreads();
   // stage step j of sweep group i0 into buffer buf with cp.async (zero-filled past the last sweep)
+  // Per thread the staged elements are fixed by tid: V element e = tid + 256 p is reflector
+  // t = e / 32 = t0 + 8 p, entry r = tid % 32, window position pos = r + t0 % 8 (independent of
+  // p), so each copy is one add on both sides; the step's 64 reflectors are consecutive slots
+  // (vld = 32: 2048 contiguous doubles) and its Z blocks are stored in the shared layout.
+  const int t0 = tid >> 5, rr = tid & 31, pos0 = rr + (t0 & 7);
+  double* const vdst0 = &S.va[0][pos0 & 1][t0][pos0 >> 1];
+  constexpr int VBUF = 2 * Q4_SG * WY_PA;  // doubles between the two va buffers
+  constexpr int ZBUF = Q4_SG * WY_PB;      // ... and the two zu buffers
   auto issue = [&](int buf, int64_t i0, int64_t j) {
     const int64_t off = bc_slot_offset_dev(n, B, j);
-    const int64_t nsw_j = n - 2 - j * B;
+    const int64_t nvalid = n - 2 - j * B - i0;  // sweeps of this group that exist at step j
+    const double* vsrc = V + (off + i0) * 32 + tid;
+    double* vdst = vdst0 + buf * VBUF;
 #pragma unroll
     for (int p = 0; p < Q4_SG * B / WY_THREADS; ++p) {
-      const int e = tid + p * WY_THREADS;
-      const int t = e >> 5, r = e & 31, pos = r + (t & 7);
-      const bool ok = i0 + t < nsw_j;
-      cp_async8(&S.va[buf][pos & 1][t][pos >> 1], ok ? V + (off + i0 + t) * vld + r : V, ok);
+      const bool ok = t0 + 8 * p < nvalid;
+      cp_async8(vdst + p * 8 * WY_PA, ok ? vsrc + p * WY_THREADS : V, ok);
     }
-    const int64_t zb = tofs[j] + i0 / 8;
+    const double* zsrc = Zf + (tofs[j] + i0 / 8) * WY_ZB;
+    double* zdst = &S.zu[buf][0][0];
 #pragma unroll
-    for (int p = 0; p < (Q4_SG * 40 / 2 + WY_THREADS - 1) / WY_THREADS; ++p) {
-      const int e = tid + p * WY_THREADS;  // 16-byte chunk: row = 8 blk + s, 20 chunks a row
-      if (e < Q4_SG * 20) {
-        const int row = e / 20, ch = e % 20, blk = row >> 3;
-        const bool ok = i0 + 8 * blk < nsw_j;
-        cp_async16(&S.zu[buf][row][2 * ch],
-                   ok ? Zf + (zb + blk) * WY_ZB + (row & 7) * 40 + 2 * ch : Zf, ok);
+    for (int p = 0; p < (ZBUF / 2 + WY_THREADS - 1) / WY_THREADS; ++p) {
+      const int e = tid + p * WY_THREADS;  // 16-byte chunk e of the step's 8 blocks
+      if (e < ZBUF / 2) {
+        const bool ok = 8 * (e / (WY_ZB / 2)) < nvalid;
+        cp_async16(zdst + 2 * e, ok ? zsrc + 2 * e : Zf, ok);
       }
     }
     cp_async_commit();
@@ -896,7 +904,7 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
     const char* e = getenv("PEVD_BCBACK");
     mode = (e && e[0] == 'q') ? 0 : (e && e[0] == 'r') ? 1 : 2;  // DMMA compact WY by default
   }
-  if (b == 32 && vld >= 32 && mode != 1 && ws) {
+  if (b == 32 && vld >= 32 && mode != 1 && ws && (mode == 0 || vld == 32)) {
     // mode 0: 4-lane DFMA kernel, mode 2 (default): DMMA compact-WY kernel
     const bool wy = mode == 2;
     const int rows_per = wy ? WY_ROWS : Q4_ROWS;
@@ -966,7 +974,7 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
 int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                  double* X, int64_t ldx, int64_t ncols, void* ws) {
   if (n < 3 || ncols <= 0 || b < 2) return OK;
-  if (b == 32 && vld >= 32 && ws) {
+  if (b == 32 && vld == 32 && ws) {  // the DMMA kernel reads each step's V as 2048 contiguous
     // X <- Q_b X  ==  (X^T Q_b^T)^T: the DMMA compact-WY kernel in reverse order on the rows of
     // X^T (= the columns of X, contiguous), backward T factors
     const int nrb = (int)cdiv(ncols, WY_ROWS);
