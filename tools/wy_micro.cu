@@ -11,10 +11,22 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-template <int MODE>  // 0: as BC-Back (2 P chains + DADD), 1: + __syncthreads per step, 2: independent
-__global__ void __launch_bounds__(256, 2) micro(double* out, int steps) {
+__device__ __forceinline__ void cpa8(void* smem, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+}
+__device__ __forceinline__ void cpa16(void* smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)), "l"(g));
+}
+
+// 0: as BC-Back (2 P chains + DADD), 1: + __syncthreads per step, 2: independent,
+// 3: + cp.async staging of V (2048 x 8 B) and Z (1344 x 16 B) per step from a streamed buffer
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) micro(double* out, int steps, const double* src) {
   __shared__ double va[2][64][20];
   __shared__ double zu[64][42];
+  double* stage = &va[0][0][0];  // (va and zu are contiguous; contents do not matter here)
   const int tid = threadIdx.x, lane = tid & 31, qd = lane & 3, r8 = lane >> 2;
   for (int e = tid; e < 2 * 64 * 20; e += 256) (&va[0][0][0])[e] = 1e-3 * (e % 7);
   for (int e = tid; e < 64 * 42; e += 256) (&zu[0][0])[e] = 1e-3 * (e % 5);
@@ -48,7 +60,19 @@ __global__ void __launch_bounds__(256, 2) micro(double* out, int steps) {
 #pragma unroll
       for (int cc = 0; cc < 5; ++cc) dmma(w[blk + cc][0], w[blk + cc][1], p1, z1[8 * cc]);
     }
-    if (MODE == 1) __syncthreads();
+    if (MODE == 3) {
+      const double* vs = src + ((size_t)(s % 4096) * 148 + blockIdx.x % 148) * 4736;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) cpa8(&stage[(tid + 256 * p) % 2560], vs + tid + 256 * p);
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        const int e = tid + 256 * p;
+        if (e < 1344) cpa16(&zu[0][0] + 2 * e, vs + 2048 + 2 * e);
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    if (MODE == 1 || MODE == 3) __syncthreads();
   }
   double acc = 0;
 #pragma unroll
@@ -57,13 +81,13 @@ __global__ void __launch_bounds__(256, 2) micro(double* out, int steps) {
 }
 
 template <int MODE>
-void run(double* out, int blocks, int steps) {
+void run(double* out, int blocks, int steps, const double* src) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  micro<MODE><<<blocks, 256>>>(out, 10);
+  micro<MODE><<<blocks, 256>>>(out, 10, src);
   cudaEventRecord(a);
-  micro<MODE><<<blocks, 256>>>(out, steps);
+  micro<MODE><<<blocks, 256>>>(out, steps, src);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -78,8 +102,12 @@ int main() {
   double* out;
   cudaMalloc(&out, sizeof(double) * 256 * sms * 4);
   const int blocks = 2 * sms, steps = 20000;
-  run<0>(out, blocks, steps);
-  run<1>(out, blocks, steps);
-  run<2>(out, blocks, steps);
+  double* src;
+  cudaMalloc(&src, sizeof(double) * (size_t)4096 * 148 * 4736 + 64);
+  cudaMemset(src, 0, sizeof(double) * (size_t)4096 * 148 * 4736);
+  run<0>(out, blocks, steps, src);
+  run<1>(out, blocks, steps, src);
+  run<2>(out, blocks, steps, src);
+  run<3>(out, blocks, steps, src);
   return 0;
 }
