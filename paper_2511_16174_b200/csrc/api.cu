@@ -7,6 +7,7 @@
 // overlaps the divide and conquer ("pipelined").  "sequential" runs the same stages on one
 // stream; "conventional" applies Q_b then Q_s to Q_d from the left (pipeline.py:367-387).
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -102,6 +103,16 @@ __global__ void copy_lower_to_full_kernel(int64_t n, const double* src, int64_t 
 struct Ev {
   cudaEvent_t a = nullptr, b = nullptr;
 };
+
+// conventional order on the transpose (default; PEVD_CONVT=0 applies Q_b, Q_s from the left)
+bool conv_transposed() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PEVD_CONVT");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
 
 }  // namespace
 }  // namespace pevd
@@ -214,7 +225,22 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
                   : ERR_CUDA))
       break;
     if (want_vectors) {
-      if (order == PEVD_ORDER_CONVENTIONAL) {
+      if (order == PEVD_ORDER_CONVENTIONAL && conv_transposed() && b == 32 && L.vld == 32) {
+        // Q = Q_s Q_b Q_d computed as its transpose Xt = Q_d^T Q_b^T Q_s^T, so the bulge
+        // reflectors meet X in column-major order (the BC-Back kernel's coalesced pattern):
+        // Xt lives in the D&C's (now free) ping-pong buffer; two n^2 transposes (~7 ms each)
+        double* Xt = (double*)L.ws_dc;
+        cudaEventRecord(ev[4].a, sm);
+        if ((rc = transpose(sm, n, n, L.Qd, n, Xt, n))) break;
+        if ((rc = bc_back_left_t(sm, n, b, L.tau, L.V, L.vld, Xt, n, n, L.ws_bcb))) break;
+        cudaEventRecord(ev[4].b, sm);
+        cudaEventRecord(ev[3].a, sm);
+        if ((rc = sbr_back_apply_right_t(sm, n, b, A, L.Tall, Xt, n, n, L.ws_back, true))) break;
+        cudaEventRecord(ev[3].b, sm);
+        cudaEventRecord(ev[5].a, sm);
+        if ((rc = transpose(sm, n, n, Xt, n, Q, ldq))) break;
+        cudaEventRecord(ev[5].b, sm);
+      } else if (order == PEVD_ORDER_CONVENTIONAL) {
         cudaEventRecord(ev[4].a, sm);
         if ((rc = bc_back_left(sm, n, b, L.tau, L.V, L.vld, L.Qd, n, n, L.ws_bcb))) break;
         cudaEventRecord(ev[4].b, sm);

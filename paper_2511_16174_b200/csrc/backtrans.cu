@@ -487,7 +487,10 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
 // LEFT = true:  X <- Q_b X, done as Y <- Y Q_b^T on the rows of Y = X^T (element (row, col) at
 //   X[row*ldx + col]): groups descending, steps top-to-bottom, sweeps descending, backward T
 //   (the conventional grouped order of backtrans.py:232-235).
-template <bool LEFT, bool ONECHAIN = false>
+// ROWMAJOR: a row's elements are contiguous (X[row*ldx + col]); otherwise X is column-major
+// (X[row + col*ldx], rows contiguous down a column: 64-byte segments per 8-row tile, the faster
+// pattern).  Default: the conventional LEFT application reads the columns of X as its rows.
+template <bool LEFT, bool ONECHAIN = false, bool ROWMAJOR = LEFT>
 __global__ void __launch_bounds__(WY_THREADS, 2)
     bc_back_wy_kernel(int64_t n, const double* __restrict__ V, int vld,
                       const double* __restrict__ Zf, const int64_t* __restrict__ tofs, double* X,
@@ -552,8 +555,8 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
     }
     const int64_t row = (int64_t)rb * WY_ROWS + warp * 8 + r8;
     const bool active = row < nrows;
-    const int64_t cs = LEFT ? 1 : ldx;                 // column stride of a row's elements
-    double* x = X + (active ? (LEFT ? row * ldx : row) : 0);
+    const int64_t cs = ROWMAJOR ? 1 : ldx;             // column stride of a row's elements
+    double* x = X + (active ? (ROWMAJOR ? row * ldx : row) : 0);
     const int64_t i0 = k * Q4_SG;
     const int64_t jmax = (n - 3 - i0) / B;
     const int64_t jfirst = LEFT ? 0 : jmax;
@@ -887,6 +890,65 @@ int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, 
   return OK;
 }
 
+// out (cols x rows, ld ldo) = in^T (in: rows x cols, ld ldi); 32 x 32 tiles through shared memory
+__global__ void transpose_kernel(int64_t rows, int64_t cols, const double* __restrict__ in,
+                                 int64_t ldi, double* __restrict__ out, int64_t ldo) {
+  __shared__ double t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + threadIdx.x, c = c0 + k;
+    if (r < rows && c < cols) t[k][threadIdx.x] = in[r + c * ldi];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c = c0 + threadIdx.x, r = r0 + k;
+    if (r < rows && c < cols) out[c + r * ldo] = t[threadIdx.x][k];
+  }
+}
+
+int transpose(cudaStream_t st, int64_t rows, int64_t cols, const double* in, int64_t ldi,
+              double* out, int64_t ldo) {
+  if (rows <= 0 || cols <= 0) return OK;
+  if (cdiv(cols, 32) > 65535) {
+    set_error("transpose: %lld columns exceed the grid", (long long)cols);
+    return ERR_VALUE;
+  }
+  transpose_kernel<<<dim3((unsigned)cdiv(rows, 32), (unsigned)cdiv(cols, 32)), dim3(32, 8), 0,
+                     st>>>(rows, cols, in, ldi, out, ldo);
+  PEVD_LAUNCH_CHECK();
+  return OK;
+}
+
+int sbr_back_apply_right_t(cudaStream_t st, int64_t n, int b, const double* Yfull,
+                           const double* Tall, double* Xt, int64_t ldx, int64_t nrows, void* ws,
+                           bool prepared) {
+  // Xt <- Xt Q_s^T (= (Q_s X)^T for Xt = X^T): Xt[:, t0:] -= (Xt[:, t0:] Y) T^T Y^T per
+  // aggregated block, from the last block backwards, row chunks of at most n rows
+  if (b < 1 || n <= b) return OK;
+  if (!prepared) PEVD_TRY(sbr_back_prepare(st, n, b, Yfull, Tall, ws));
+  const int NB = nb_agg();
+  SbrBackWs W = sbr_back_carve(n, b, ws, NB);
+  const int64_t R = sbr_num_rounds(n, b);
+  for (int64_t g = W.ngroups - 1; g >= 0; --g) {
+    int64_t t0, c0, K;
+    group_dims(n, b, NB, R, g, &t0, &c0, &K);
+    const int64_t m = n - t0;
+    const double* Y = Yfull + t0 + c0 * n;
+    const double* Tg = W.Tagg + g * W.K * W.K;
+    for (int64_t r = 0; r < nrows; r += n) {
+      const int64_t nr = std::min<int64_t>(n, nrows - r);
+      double* X2 = Xt + r + t0 * ldx;
+      GemmArgs g1{nr, K, m, 1.0, 0.0, X2, ldx, Y, n, W.tmp1, nr, 0, 0, A_GENERAL, C_ALL};
+      PEVD_TRY(gemm(st, g1, W.sk, W.skn));                  // tmp1 = Xt2 Y
+      GemmArgs g2{nr, K, K, 1.0, 0.0, W.tmp1, nr, Tg, W.K, W.tmp2, nr, 0, 1, A_GENERAL, C_ALL};
+      PEVD_TRY(gemm(st, g2, W.sk, W.skn));                  // tmp2 = tmp1 T^T
+      GemmArgs g3{nr, m, K, -1.0, 1.0, W.tmp2, nr, Y, n, X2, ldx, 0, 1, A_GENERAL, C_ALL};
+      PEVD_TRY(gemm(st, g3, W.sk, W.skn));                  // Xt2 -= tmp2 Y^T
+    }
+  }
+  return OK;
+}
+
 int64_t bc_back_ws_bytes(int64_t n, int64_t nrows) {
   // counters + T-factor offsets + the -T factors of every block of 8 sweeps (64 doubles each)
   const int64_t jcount = n >= 3 ? (n - 3) / 32 + 1 : 1;
@@ -971,8 +1033,9 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
   return OK;
 }
 
-int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
-                 double* X, int64_t ldx, int64_t ncols, void* ws) {
+template <bool TMEM>
+int bc_back_left_impl(cudaStream_t st, int64_t n, int b, const double* tau, const double* V,
+                      int vld, double* X, int64_t ldx, int64_t ncols, void* ws) {
   if (n < 3 || ncols <= 0 || b < 2) return OK;
   if (b == 32 && vld == 32 && ws) {  // the DMMA kernel reads each step's V as 2048 contiguous
     // X <- Q_b X  ==  (X^T Q_b^T)^T: the DMMA compact-WY kernel in reverse order on the rows of
@@ -999,12 +1062,12 @@ int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const dou
     int dev;
     PEVD_CUDA(cudaGetDevice(&dev));
     if (attr_dev != dev) {
-      PEVD_CUDA(cudaFuncSetAttribute(bc_back_wy_kernel<true>,
+      PEVD_CUDA(cudaFuncSetAttribute(bc_back_wy_kernel<true, false, !TMEM>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_dev = dev;
     }
     int per_sm = 0;
-    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bc_back_wy_kernel<true>,
+    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bc_back_wy_kernel<true, false, !TMEM>,
                                                             WY_THREADS, smem));
     if (per_sm < 1) {
       set_error("bc_back_left: persistent kernel cannot be resident");
@@ -1022,7 +1085,7 @@ int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const dou
       bc_back_wy_kernel<true, true><<<(unsigned)grid, WY_THREADS, smem, st>>>(
           n, V, vld, Tf, tofs, X, ldx, ncols, counter, progress, nunits, nrb);
     } else
-    bc_back_wy_kernel<true><<<(unsigned)grid, WY_THREADS, smem, st>>>(
+    bc_back_wy_kernel<true, false, !TMEM><<<(unsigned)grid, WY_THREADS, smem, st>>>(
         n, V, vld, Tf, tofs, X, ldx, ncols, counter, progress, nunits, nrb);
     PEVD_LAUNCH_CHECK();
     return OK;
@@ -1031,6 +1094,20 @@ int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const dou
                                                                    ncols);
   PEVD_LAUNCH_CHECK();
   return OK;
+}
+
+int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
+                 double* X, int64_t ldx, int64_t ncols, void* ws) {
+  return bc_back_left_impl<false>(st, n, b, tau, V, vld, X, ldx, ncols, ws);
+}
+
+int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
+                   double* Xt, int64_t ldx, int64_t nrows, void* ws) {
+  if (!(b == 32 && vld == 32 && ws)) {  // only the DMMA kernel has the transposed layout
+    set_error("bc_back_left_t: needs b = 32, vld = 32 and a workspace");
+    return ERR_VALUE;
+  }
+  return bc_back_left_impl<true>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws);
 }
 
 }  // namespace pevd
