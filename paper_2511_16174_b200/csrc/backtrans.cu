@@ -490,8 +490,10 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
 // ROWMAJOR: a row's elements are contiguous (X[row*ldx + col]); otherwise X is column-major
 // (X[row + col*ldx], rows contiguous down a column: 64-byte segments per 8-row tile, the faster
 // pattern).  Default: the conventional LEFT application reads the columns of X as its rows.
-template <bool LEFT, bool ONECHAIN = false, bool ROWMAJOR = LEFT>
-__global__ void __launch_bounds__(WY_THREADS, 2)
+// RT: 8-row tiles per warp.  RT = 1: 8 warps (256 threads) per 64-row block; RT = 2: 4 warps of
+// 16 rows (two independent DMMA chains per warp, every V / Z fragment feeds both tiles).
+template <bool LEFT, bool ROWMAJOR = LEFT, int RT = 1>
+__global__ void __launch_bounds__(WY_THREADS / RT, 2)
     bc_back_wy_kernel(int64_t n, const double* __restrict__ V, int vld,
                       const double* __restrict__ Zf, const int64_t* __restrict__ tofs, double* X,
                       int64_t ldx, int64_t nrows, int* counter, int* progress, int64_t nunits,
@@ -499,36 +501,35 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
   extern __shared__ __align__(16) unsigned char wyraw[];
   WySmem& S = *reinterpret_cast<WySmem*>(wyraw);
   constexpr int B = 32;
+  constexpr int NT = WY_THREADS / RT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qd = lane & 3, r8 = lane >> 2;
   const int64_t nsw = n - 2;
   // zero va once: the positions outside each reflector's support are never written
-  for (int e = tid; e < 2 * 2 * Q4_SG * WY_PA; e += WY_THREADS) (&S.va[0][0][0][0])[e] = 0.0;
+  for (int e = tid; e < 2 * 2 * Q4_SG * WY_PA; e += NT) (&S.va[0][0][0][0])[e] = 0.0;
   __syncthreads();
   // stage step j of sweep group i0 into buffer buf with cp.async (zero-filled past the last sweep)
-  // Per thread the staged elements are fixed by tid: V element e = tid + 256 p is reflector
-  // t = e / 32 = t0 + 8 p, entry r = tid % 32, window position pos = r + t0 % 8 (independent of
-  // p), so each copy is one add on both sides; the step's 64 reflectors are consecutive slots
-  // (vld = 32: 2048 contiguous doubles) and its Z blocks are stored in the shared layout.
-  const int t0 = tid >> 5, rr = tid & 31, pos0 = rr + (t0 & 7);
-  double* const vdst0 = &S.va[0][pos0 & 1][t0][pos0 >> 1];
+  // V element e = tid + NT p is reflector t = e / 32 = t0 + (NT / 32) p, entry r = tid % 32; the
+  // step's 64 reflectors are consecutive slots (vld = 32: 2048 contiguous doubles) and its Z
+  // blocks are stored in the shared layout, so every copy is an add on both sides.
+  const int t0 = tid >> 5, rr = tid & 31;
   constexpr int VBUF = 2 * Q4_SG * WY_PA;  // doubles between the two va buffers
   constexpr int ZBUF = Q4_SG * WY_PB;      // ... and the two zu buffers
   auto issue = [&](int buf, int64_t i0, int64_t j) {
     const int64_t off = bc_slot_offset_dev(n, B, j);
     const int64_t nvalid = n - 2 - j * B - i0;  // sweeps of this group that exist at step j
     const double* vsrc = V + (off + i0) * 32 + tid;
-    double* vdst = vdst0 + buf * VBUF;
 #pragma unroll
-    for (int p = 0; p < Q4_SG * B / WY_THREADS; ++p) {
-      const bool ok = t0 + 8 * p < nvalid;
-      cp_async8(vdst + p * 8 * WY_PA, ok ? vsrc + p * WY_THREADS : V, ok);
+    for (int p = 0; p < Q4_SG * B / NT; ++p) {
+      const int t = t0 + (NT / 32) * p, pos = rr + (t & 7);
+      const bool ok = t < nvalid;
+      cp_async8(&S.va[0][pos & 1][t][pos >> 1] + buf * VBUF, ok ? vsrc + p * NT : V, ok);
     }
     const double* zsrc = Zf + (tofs[j] + i0 / 8) * WY_ZB;
     double* zdst = &S.zu[buf][0][0];
 #pragma unroll
-    for (int p = 0; p < (ZBUF / 2 + WY_THREADS - 1) / WY_THREADS; ++p) {
-      const int e = tid + p * WY_THREADS;  // 16-byte chunk e of the step's 8 blocks
+    for (int p = 0; p < (ZBUF / 2 + NT - 1) / NT; ++p) {
+      const int e = tid + p * NT;  // 16-byte chunk e of the step's 8 blocks
       if (e < ZBUF / 2) {
         const bool ok = 8 * (e / (WY_ZB / 2)) < nvalid;
         cp_async16(zdst + 2 * e, ok ? zsrc + 2 * e : Zf, ok);
@@ -553,10 +554,15 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
         if (ns < 1024) ns <<= 1;
       }
     }
-    const int64_t row = (int64_t)rb * WY_ROWS + warp * 8 + r8;
-    const bool active = row < nrows;
     const int64_t cs = ROWMAJOR ? 1 : ldx;             // column stride of a row's elements
-    double* x = X + (active ? (ROWMAJOR ? row * ldx : row) : 0);
+    bool active[RT];
+    double* x[RT];
+#pragma unroll
+    for (int rt = 0; rt < RT; ++rt) {
+      const int64_t row = (int64_t)rb * WY_ROWS + warp * 8 * RT + rt * 8 + r8;
+      active[rt] = row < nrows;
+      x[rt] = X + (active[rt] ? (ROWMAJOR ? row * ldx : row) : 0);
+    }
     const int64_t i0 = k * Q4_SG;
     const int64_t jmax = (n - 3 - i0) / B;
     const int64_t jfirst = LEFT ? 0 : jmax;
@@ -564,14 +570,16 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
     int buf = 0;
     issue(buf, i0, jfirst);
     __syncthreads();  // progress acquired by tid 0 before anyone reads X
-    double w[12][2];
+    double w[RT][12][2];
 #pragma unroll
-    for (int c = 0; c < 12; ++c)
+    for (int rt = 0; rt < RT; ++rt)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t col = ws + 8 * c + 2 * qd + h;
-        w[c][h] = (active && col < n) ? __ldcg(x + col * cs) : 0.0;
-      }
+      for (int c = 0; c < 12; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t col = ws + 8 * c + 2 * qd + h;
+          w[rt][c][h] = (active[rt] && col < n) ? __ldcg(x[rt] + col * cs) : 0.0;
+        }
     cp_async_wait<0>();
     __syncthreads();
     for (int64_t jj = 0; jj <= jmax; ++jj) {
@@ -579,98 +587,109 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
       const bool more = jj < jmax;
       // prefetch the next step: its new window columns (registers) and its V / Z (other buffer:
       // the barrier that ended the previous step means nobody still reads it)
-      double nx[4][2];
+      double nx[RT][4][2];
       const int64_t nbase = LEFT ? ws + 3 * B : ws - B;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int rt = 0; rt < RT; ++rt)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t col = nbase + 8 * c + 2 * qd + h;
-          nx[c][h] = (more && active && col < n) ? __ldcg(x + col * cs) : 0.0;
-        }
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t col = nbase + 8 * c + 2 * qd + h;
+            nx[rt][c][h] = (more && active[rt] && col < n) ? __ldcg(x[rt] + col * cs) : 0.0;
+          }
       if (more) issue(buf ^ 1, i0, LEFT ? j + 1 : j - 1);
-      // ---- apply the 8 blocks of this step: P = X V (10 DMMA), X += P Z^T (10 DMMA)
+      // ---- apply the 8 blocks of this step: P = X V (10 DMMA), X += P Z^T (10 DMMA), per tile
 #pragma unroll
       for (int bb = 0; bb < Q4_SG / 8; ++bb) {
         const int blk = LEFT ? Q4_SG / 8 - 1 - bb : bb;
         const int tb = blk * 8;
-        double p0 = 0.0, p1 = 0.0, e0 = 0.0, e1 = 0.0;
+        double p0[RT], p1[RT], e0[RT], e1[RT];
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt) p0[rt] = p1[rt] = e0[rt] = e1[rt] = 0.0;
         const double* v0 = &S.va[buf][0][tb + r8][qd];
         const double* v1 = &S.va[buf][1][tb + r8][qd];
 #pragma unroll
         for (int cc = 0; cc < 5; ++cc) {
-          dmma884(p0, p1, w[blk + cc][0], v0[4 * cc]);
-          if (ONECHAIN) dmma884(p0, p1, w[blk + cc][1], v1[4 * cc]);
-          else dmma884(e0, e1, w[blk + cc][1], v1[4 * cc]);
+          const double a = v0[4 * cc], c = v1[4 * cc];
+#pragma unroll
+          for (int rt = 0; rt < RT; ++rt) {
+            dmma884(p0[rt], p1[rt], w[rt][blk + cc][0], a);
+            dmma884(e0[rt], e1[rt], w[rt][blk + cc][1], c);
+          }
         }
-        if (!ONECHAIN) {
-          p0 += e0;
-          p1 += e1;
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt) {
+          p0[rt] += e0[rt];
+          p1[rt] += e1[rt];
         }
         const double* z0 = &S.zu[buf][tb + 2 * qd][r8];
         const double* z1 = &S.zu[buf][tb + 2 * qd + 1][r8];
         // all five tiles' first k-step, then the second: two updates of a tile are 5 DMMAs apart
 #pragma unroll
-        for (int cc = 0; cc < 5; ++cc) dmma884(w[blk + cc][0], w[blk + cc][1], p0, z0[8 * cc]);
+        for (int cc = 0; cc < 5; ++cc) {
+          const double z = z0[8 * cc];
 #pragma unroll
-        for (int cc = 0; cc < 5; ++cc) dmma884(w[blk + cc][0], w[blk + cc][1], p1, z1[8 * cc]);
+          for (int rt = 0; rt < RT; ++rt)
+            dmma884(w[rt][blk + cc][0], w[rt][blk + cc][1], p0[rt], z);
+        }
+#pragma unroll
+        for (int cc = 0; cc < 5; ++cc) {
+          const double z = z1[8 * cc];
+#pragma unroll
+          for (int rt = 0; rt < RT; ++rt)
+            dmma884(w[rt][blk + cc][0], w[rt][blk + cc][1], p1[rt], z);
+        }
       }
       // ---- slide by b = 32 (4 tiles): the trailing 4 tiles (right) / leading 4 tiles (left)
       //      are final for this group
-      if (!LEFT) {
 #pragma unroll
-        for (int c = 8; c < 12; ++c)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int64_t col = ws + 8 * c + 2 * qd + h;
-            if (active && col < n) x[col * cs] = w[c][h];
-          }
-      } else {
+      for (int rt = 0; rt < RT; ++rt) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int64_t col = ws + 8 * c + 2 * qd + h;
-            if (active && col < n) x[col * cs] = w[c][h];
+            const int cw = LEFT ? c : c + 8;
+            const int64_t col = ws + 8 * cw + 2 * qd + h;
+            if (active[rt] && col < n) x[rt][col * cs] = w[rt][cw][h];
           }
-      }
-      if (more) {
-        if (!LEFT) {
+        if (more) {
+          if (!LEFT) {
 #pragma unroll
-          for (int c = 11; c >= 4; --c) {
-            w[c][0] = w[c - 4][0];
-            w[c][1] = w[c - 4][1];
-          }
+            for (int c = 11; c >= 4; --c) {
+              w[rt][c][0] = w[rt][c - 4][0];
+              w[rt][c][1] = w[rt][c - 4][1];
+            }
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            w[c][0] = nx[c][0];
-            w[c][1] = nx[c][1];
+            for (int c = 0; c < 4; ++c) {
+              w[rt][c][0] = nx[rt][c][0];
+              w[rt][c][1] = nx[rt][c][1];
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              w[rt][c][0] = w[rt][c + 4][0];
+              w[rt][c][1] = w[rt][c + 4][1];
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              w[rt][8 + c][0] = nx[rt][c][0];
+              w[rt][8 + c][1] = nx[rt][c][1];
+            }
           }
-          ws -= B;
         } else {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            w[c][0] = w[c + 4][0];
-            w[c][1] = w[c + 4][1];
-          }
+          for (int c = 0; c < 12; ++c) {
+            if (LEFT ? c < 4 : c >= 8) continue;  // already stored above
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            w[8 + c][0] = nx[c][0];
-            w[8 + c][1] = nx[c][1];
-          }
-          ws += B;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 12; ++c) {
-          if (LEFT ? c < 4 : c >= 8) continue;  // already stored above
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int64_t col = ws + 8 * c + 2 * qd + h;
-            if (active && col < n) x[col * cs] = w[c][h];
+            for (int h = 0; h < 2; ++h) {
+              const int64_t col = ws + 8 * c + 2 * qd + h;
+              if (active[rt] && col < n) x[rt][col * cs] = w[rt][c][h];
+            }
           }
         }
       }
+      if (more) ws += LEFT ? B : -B;
       buf ^= 1;
       cp_async_wait<0>();
       __syncthreads();
@@ -989,7 +1008,7 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
           n, tau, V, vld, tofs, jcount, Tf);
       PEVD_LAUNCH_CHECK();
     }
-    const void* kfn = wy ? (const void*)bc_back_wy_kernel<false> : (const void*)bc_back_q4_kernel;
+    const void* kfn = wy ? (const void*)bc_back_wy_kernel<false, false, 1> : (const void*)bc_back_q4_kernel;
     const size_t smem = wy ? sizeof(WySmem) : sizeof(Q4Smem);
     const int nthr = wy ? WY_THREADS : Q4_THREADS;
     static int attr_dev[2] = {-1, -1};
@@ -1007,7 +1026,7 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
     }
     const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
     if (wy)
-      bc_back_wy_kernel<false><<<(unsigned)grid, nthr, smem, st>>>(n, V, vld, Tf, tofs, X, ldx,
+      bc_back_wy_kernel<false, false, 1><<<(unsigned)grid, nthr, smem, st>>>(n, V, vld, Tf, tofs, X, ldx,
                                                                    nrows, counter, progress,
                                                                    nunits, nrb);
     else
@@ -1033,7 +1052,7 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
   return OK;
 }
 
-template <bool TMEM>
+template <bool TMEM, int KRT = 1>
 int bc_back_left_impl(cudaStream_t st, int64_t n, int b, const double* tau, const double* V,
                       int vld, double* X, int64_t ldx, int64_t ncols, void* ws) {
   if (n < 3 || ncols <= 0 || b < 2) return OK;
@@ -1062,30 +1081,19 @@ int bc_back_left_impl(cudaStream_t st, int64_t n, int b, const double* tau, cons
     int dev;
     PEVD_CUDA(cudaGetDevice(&dev));
     if (attr_dev != dev) {
-      PEVD_CUDA(cudaFuncSetAttribute(bc_back_wy_kernel<true, false, !TMEM>,
+      PEVD_CUDA(cudaFuncSetAttribute(bc_back_wy_kernel<true, !TMEM, KRT>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_dev = dev;
     }
     int per_sm = 0;
-    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bc_back_wy_kernel<true, false, !TMEM>,
-                                                            WY_THREADS, smem));
+    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bc_back_wy_kernel<true, !TMEM, KRT>,
+                                                            WY_THREADS / KRT, smem));
     if (per_sm < 1) {
       set_error("bc_back_left: persistent kernel cannot be resident");
       return ERR_CUDA;
     }
     const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
-    static int onechain = -1;
-    if (onechain < 0) {
-      const char* e = getenv("PEVD_WYCHAIN");
-      onechain = (e && e[0] == '1') ? 1 : 0;
-    }
-    if (onechain) {
-      PEVD_CUDA(cudaFuncSetAttribute(bc_back_wy_kernel<true, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      bc_back_wy_kernel<true, true><<<(unsigned)grid, WY_THREADS, smem, st>>>(
-          n, V, vld, Tf, tofs, X, ldx, ncols, counter, progress, nunits, nrb);
-    } else
-    bc_back_wy_kernel<true, false, !TMEM><<<(unsigned)grid, WY_THREADS, smem, st>>>(
+    bc_back_wy_kernel<true, !TMEM, KRT><<<(unsigned)grid, WY_THREADS / KRT, smem, st>>>(
         n, V, vld, Tf, tofs, X, ldx, ncols, counter, progress, nunits, nrb);
     PEVD_LAUNCH_CHECK();
     return OK;
@@ -1107,7 +1115,13 @@ int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const d
     set_error("bc_back_left_t: needs b = 32, vld = 32 and a workspace");
     return ERR_VALUE;
   }
-  return bc_back_left_impl<true>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws);
+  static int rt = -1;
+  if (rt < 0) {
+    const char* e = getenv("PEVD_WYRT");
+    rt = e ? atoi(e) : 1;
+  }
+  if (rt == 1) return bc_back_left_impl<true, 1>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws);
+  return bc_back_left_impl<true, 2>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws);
 }
 
 }  // namespace pevd
