@@ -19,10 +19,11 @@ namespace pevd {
 
 namespace {
 
-constexpr int QR_THREADS = 256;
+constexpr int QR_THREADS = 512;
 constexpr int KMAX = 32;
 constexpr int LDP = KMAX + 1;  // smem panel row stride (doubles)
 constexpr int NVAL = 2 * KMAX; // partial values per CTA per step: h[0..31], g[0..31]
+constexpr int NG = QR_THREADS / NVAL;  // thread groups splitting the rows of a partial
 
 struct QrWork {
   double* part;     // [2][MAXCTA][NVAL], double-buffered by step parity
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(QR_THREADS)
   extern __shared__ __align__(16) double sm[];
   double* P = sm;                                      // [rows_per_cta][LDP]
   double* red = P + rows_per_cta * LDP;                // [4][NVAL]
-  double* hv = red + 4 * NVAL;                         // [NVAL] reduced values
+  double* hv = red + NG * NVAL;                        // [NVAL] reduced values
   double* T = hv + NVAL;                               // [KMAX][KMAX] col-major T
   double* coef = T + KMAX * KMAX;                      // [KMAX]
   double* scal = coef + KMAX;                          // [4]: denom, tau, alpha, flag
@@ -79,19 +80,19 @@ __global__ void __launch_bounds__(QR_THREADS)
   for (int j = 0; j <= k; ++j) {
     // ---- partial sums for this CTA's rows
     {
-      const int vi = tid % NVAL, grp = tid / NVAL;  // 4 groups
+      const int vi = tid % NVAL, grp = tid / NVAL;  // NG groups
       double s = 0.0;
       if (vi < KMAX) {
         const int c = vi;
         if (j < k && c >= j && c < k) {
           double s1 = 0.0;
           int lr = grp;
-          for (; lr + 4 < nr; lr += 8) {
+          for (; lr + NG < nr; lr += 2 * NG) {
             const int64_t r = r0 + lr;
             if (r > j) s += P[lr * LDP + j] * P[lr * LDP + c];
-            if (r + 4 > j) s1 += P[(lr + 4) * LDP + j] * P[(lr + 4) * LDP + c];
+            if (r + NG > j) s1 += P[(lr + NG) * LDP + j] * P[(lr + NG) * LDP + c];
           }
-          for (; lr < nr; lr += 4) {
+          for (; lr < nr; lr += NG) {
             const int64_t r = r0 + lr;
             if (r > j) s += P[lr * LDP + j] * P[lr * LDP + c];
           }
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(QR_THREADS)
         const int q = vi - KMAX;
         const int jp = j - 1;  // previous reflector
         if (jp >= 1 && q < jp) {
-          for (int lr = grp; lr < nr; lr += 4) {
+          for (int lr = grp; lr < nr; lr += NG) {
             const int64_t r = r0 + lr;
             if (r >= jp) {
               const double v = (r == jp) ? 1.0 : P[lr * LDP + jp];
@@ -122,23 +123,25 @@ __global__ void __launch_bounds__(QR_THREADS)
     }
     __syncthreads();
     if (tid < NVAL) {
-      const double s = red[tid] + red[NVAL + tid] + red[2 * NVAL + tid] + red[3 * NVAL + tid];
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) s += red[q * NVAL + tid];
       part[(int64_t)blockIdx.x * NVAL + tid] = s;
     }
     grid_barrier(wk.bar, ncta);
     // ---- deterministic reduction of all CTA partials (identical in every CTA)
     {
       const int vi = tid % NVAL, grp = tid / NVAL;
-      // all of this thread's partials (CTAs grp, grp+4, ...) are loaded before any is summed:
+      // all of this thread's partials (CTAs grp, grp+NG, ...) are loaded before any is summed:
       // one L2 round trip per 40 CTAs instead of one per 16, in a fixed order
       double acc[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-      for (unsigned base = grp; base < ncta; base += 160) {
+      for (unsigned base = grp; base < ncta; base += NG * 40) {
         double v[40];
 #pragma unroll
         for (int q = 0; q < 40; ++q) {
-          const unsigned p = base + 4 * q;
+          const unsigned p = base + NG * q;
           v[q] = p < ncta ? __ldcg(part + (int64_t)p * NVAL + vi) : 0.0;
         }
 #pragma unroll
@@ -148,7 +151,12 @@ __global__ void __launch_bounds__(QR_THREADS)
                              ((acc[4] + acc[5]) + (acc[6] + acc[7]));
     }
     __syncthreads();
-    if (tid < NVAL) hv[tid] = red[tid] + red[NVAL + tid] + red[2 * NVAL + tid] + red[3 * NVAL + tid];
+    if (tid < NVAL) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) s += red[q * NVAL + tid];
+      hv[tid] = s;
+    }
     if (tid < KMAX) coef[tid] = (j < k && tid >= j && tid < k) ? __ldcg(piv + tid) : 0.0;
     __syncthreads();
     // ---- T column j-1: T[0:jp, jp] = -tau_jp * T[0:jp, 0:jp] * g[0:jp]  (row q per thread;
@@ -264,7 +272,7 @@ int panel_qr(cudaStream_t st, int64_t m, int k, const double* panel, int64_t ldp
   if (ncta < 1) ncta = 1;
   int64_t rows = cdiv(m, ncta);
   ncta = (int)cdiv(m, rows);
-  const size_t smem = (size_t)(rows * LDP + 4 * NVAL + NVAL + KMAX * KMAX + KMAX + 4 + KMAX) * 8;
+  const size_t smem = (size_t)(rows * LDP + NG * NVAL + NVAL + KMAX * KMAX + KMAX + 4 + KMAX) * 8;
   if (smem > 227 * 1024) {
     set_error("panel_qr: panel too tall for the resident-panel kernel (m=%lld)", (long long)m);
     return ERR_VALUE;
