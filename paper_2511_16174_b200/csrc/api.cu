@@ -166,14 +166,17 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     return ERR_VALUE;
   }
   cudaStream_t sb = nullptr;
-  const bool two_streams = want_vectors && order == PEVD_ORDER_PIPELINED;
+  const bool two_streams = want_vectors && order != PEVD_ORDER_SEQUENTIAL;
   if (two_streams) PEVD_CUDA(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
   Ev ev[6];
+  cudaEvent_t prep_done = nullptr;
   for (auto& e : ev) {
     PEVD_CUDA(cudaEventCreate(&e.a));
     PEVD_CUDA(cudaEventCreate(&e.b));
   }
+  PEVD_CUDA(cudaEventCreateWithFlags(&prep_done, cudaEventDisableTiming));
   auto cleanup = [&]() {
+    if (prep_done) cudaEventDestroy(prep_done);
     for (auto& e : ev) {
       if (e.a) cudaEventDestroy(e.a);
       if (e.b) cudaEventDestroy(e.b);
@@ -189,12 +192,6 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     if ((rc = sbr_reduce(sm, n, b, A, lda, L.bands, want_vectors ? L.Tall : nullptr, L.ws_sbr)))
       break;
     cudaEventRecord(ev[0].b, sm);
-    // ---- conventional: the SBR-Back T aggregation (SBR output only, ~1% of the SBR-Back
-    //      flops) right here on the main stream: run beside the latency-bound chase it costs the
-    //      chase more than it saves
-    if (want_vectors && order == PEVD_ORDER_CONVENTIONAL) {
-      if ((rc = sbr_back_prepare(sm, n, b, A, L.Tall, L.ws_back))) break;
-    }
     // ---- BC first: its persistent CTAs must become resident before the SBR-Back GEMMs
     //      (enqueued next, on the back stream) fill the SMs
     cudaEventRecord(ev[1].a, sm);
@@ -216,6 +213,19 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
       if ((rc = bc_back_right(sback, n, b, L.tau, L.V, L.vld, L.Qs, n, n, L.ws_bcb))) break;
       cudaEventRecord(ev[4].b, sback);
     }
+    // ---- conventional: the back-transform preparations (SBR-Back T aggregation, the Z factor
+    //      of every BC-Back block; they need only the SBR and chase outputs) on the side stream
+    //      beside the divide and conquer
+    const bool conv_t = want_vectors && order == PEVD_ORDER_CONVENTIONAL && conv_transposed() &&
+                        b == 32 && L.vld == 32;
+    if (want_vectors && order == PEVD_ORDER_CONVENTIONAL) {
+      cudaStreamWaitEvent(sb, ev[1].b, 0);
+      if ((rc = sbr_back_prepare(sb, n, b, A, L.Tall, L.ws_back))) break;
+      if (conv_t &&
+          (rc = bc_back_left_t(sb, n, b, L.tau, L.V, L.vld, nullptr, n, n, L.ws_bcb, false)))
+        break;
+      cudaEventRecord(prep_done, sb);
+    }
     // ---- D&C
     cudaEventRecord(ev[2].a, sm);
     if ((rc = stedc(sm, n, L.d, L.e, L.Qd, n, L.ws_dc, &info))) break;
@@ -225,14 +235,15 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
                   : ERR_CUDA))
       break;
     if (want_vectors) {
-      if (order == PEVD_ORDER_CONVENTIONAL && conv_transposed() && b == 32 && L.vld == 32) {
+      if (order == PEVD_ORDER_CONVENTIONAL) cudaStreamWaitEvent(sm, prep_done, 0);
+      if (conv_t) {
         // Q_b Q_d computed as its transpose Xt = Q_d^T Q_b^T, so the bulge reflectors meet X in
         // column-major order (the BC-Back kernel's coalesced pattern): Xt lives in the D&C's
         // (now free) ping-pong buffer; two n^2 transposes (~7 ms each)
         double* Xt = (double*)L.ws_dc;
         cudaEventRecord(ev[4].a, sm);
         if ((rc = transpose(sm, n, n, L.Qd, n, Xt, n))) break;
-        if ((rc = bc_back_left_t(sm, n, b, L.tau, L.V, L.vld, Xt, n, n, L.ws_bcb))) break;
+        if ((rc = bc_back_left_t(sm, n, b, L.tau, L.V, L.vld, Xt, n, n, L.ws_bcb, true))) break;
         cudaEventRecord(ev[4].b, sm);
         // back to column-major in the output, where SBR-Back's left application (its faster
         // GEMM shapes) finishes Q = Q_s (Q_b Q_d) in place

@@ -1052,9 +1052,23 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
   return OK;
 }
 
+// tofs[j] = number of 8-sweep blocks before chase step j (prefix sum of cdiv(n - 2 - 32 j, 8)),
+// on the device so the BC-Back preparation needs no host synchronisation
+__global__ void wy_tofs_kernel(int64_t n, int64_t jcount, int64_t* tofs) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int64_t acc = 0;
+    tofs[0] = 0;
+    for (int64_t j = 0; j < jcount; ++j) {
+      acc += (n - 2 - j * 32 + 7) / 8;
+      tofs[j + 1] = acc;
+    }
+  }
+}
+
 template <bool TMEM, int KRT = 1>
 int bc_back_left_impl(cudaStream_t st, int64_t n, int b, const double* tau, const double* V,
-                      int vld, double* X, int64_t ldx, int64_t ncols, void* ws) {
+                      int vld, double* X, int64_t ldx, int64_t ncols, void* ws,
+                      bool prepared = false) {
   if (n < 3 || ncols <= 0 || b < 2) return OK;
   if (b == 32 && vld == 32 && ws) {  // the DMMA kernel reads each step's V as 2048 contiguous
     // X <- Q_b X  ==  (X^T Q_b^T)^T: the DMMA compact-WY kernel in reverse order on the rows of
@@ -1067,15 +1081,17 @@ int bc_back_left_impl(cudaStream_t st, int64_t n, int b, const double* tau, cons
     const int64_t jcount = (n - 3) / 32 + 1;
     int64_t* tofs = (int64_t*)((char*)ws + ((ncols / 32 + 64) * 4 + 255) / 256 * 256);
     double* Tf = (double*)((char*)tofs + ((jcount + 2) * 8 + 255) / 256 * 256);
-    PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
-    std::vector<int64_t> h(jcount + 1);
-    h[0] = 0;
-    for (int64_t j = 0; j < jcount; ++j) h[j + 1] = h[j] + cdiv(n - 2 - j * 32, 8);
-    PEVD_CUDA(cudaMemcpyAsync(tofs, h.data(), (jcount + 1) * 8, cudaMemcpyHostToDevice, st));
-    PEVD_CUDA(cudaStreamSynchronize(st));
-    wy_tfactor_kernel<true><<<(unsigned)std::min<int64_t>(cdiv(h[jcount], 128), 16384), 128, 0, st>>>(
-        n, tau, V, vld, tofs, jcount, Tf);
-    PEVD_LAUNCH_CHECK();
+    if (!prepared) {  // counters, block offsets and the Z of every block (BC output only)
+      PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
+      wy_tofs_kernel<<<1, 32, 0, st>>>(n, jcount, tofs);
+      PEVD_LAUNCH_CHECK();
+      int64_t nblk = 0;
+      for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(n - 2 - j * 32, 8);
+      wy_tfactor_kernel<true><<<(unsigned)std::min<int64_t>(cdiv(nblk, 128), 16384), 128, 0, st>>>(
+          n, tau, V, vld, tofs, jcount, Tf);
+      PEVD_LAUNCH_CHECK();
+    }
+    if (X == nullptr) return OK;  // preparation only
     const size_t smem = sizeof(WySmem);
     static int attr_dev = -1;
     int dev;
@@ -1110,7 +1126,7 @@ int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const dou
 }
 
 int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
-                   double* Xt, int64_t ldx, int64_t nrows, void* ws) {
+                   double* Xt, int64_t ldx, int64_t nrows, void* ws, bool prepared) {
   if (!(b == 32 && vld == 32 && ws)) {  // only the DMMA kernel has the transposed layout
     set_error("bc_back_left_t: needs b = 32, vld = 32 and a workspace");
     return ERR_VALUE;
@@ -1120,8 +1136,9 @@ int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const d
     const char* e = getenv("PEVD_WYRT");
     rt = e ? atoi(e) : 1;
   }
-  if (rt == 1) return bc_back_left_impl<true, 1>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws);
-  return bc_back_left_impl<true, 2>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws);
+  if (rt == 1)
+    return bc_back_left_impl<true, 1>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws, prepared);
+  return bc_back_left_impl<true, 2>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws, prepared);
 }
 
 }  // namespace pevd

@@ -65,8 +65,10 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
                   double* X, int64_t ldx, int64_t nrows, void* ws);
 // Transposed conventional back transformation, on Xt = X^T (nrows x n, column-major), where the
 // bulge kernel's fast memory pattern applies: Xt <- Xt Q_b^T, then Xt <- Xt Q_s^T.
+// (Xt == nullptr: only the preparation (counters, Z of every block), which depends on the chase
+//  output alone; prepared = true skips it in the later call on the same ws.)
 int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
-                   double* Xt, int64_t ldx, int64_t nrows, void* ws);
+                   double* Xt, int64_t ldx, int64_t nrows, void* ws, bool prepared = false);
 int sbr_back_apply_right_t(cudaStream_t st, int64_t n, int b, const double* Yfull,
                            const double* Tall, double* Xt, int64_t ldx, int64_t nrows, void* ws,
                            bool prepared = false);
