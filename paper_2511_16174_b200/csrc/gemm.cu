@@ -528,27 +528,59 @@ __device__ __forceinline__ void fast_tile(const GemmArgs& g, int64_t i0, int64_t
     __syncthreads();
     const bool vec = ((uintptr_t)g.C % 16 == 0) && (g.ldc % 2 == 0);
     constexpr int PAIRS = BM / 2;
-    for (int e = tid; e < BN * PAIRS; e += C::NT) {
-      const int col = e / PAIRS, rp = (e % PAIRS) * 2;
-      const int64_t gj = j0 + col, gi = i0 + rp;
-      if (gj >= g.n || gi >= g.m) continue;
-      const int64_t cj = g.cmap ? (int64_t)g.cmap[gj] : gj;
-      double* cp = g.C + gi + cj * g.ldc;
-      const double v0 = g.alpha * Cs[col * LDC + rp], v1 = g.alpha * Cs[col * LDC + rp + 1];
-      if (vec && gi + 1 < g.m) {
-        double2 o;
-        if (g.beta != 0.0) {
-          const double2 c = *reinterpret_cast<const double2*>(cp);
-          o.x = v0 + g.beta * c.x;
-          o.y = v1 + g.beta * c.y;
-        } else {
-          o.x = v0;
-          o.y = v1;
+    constexpr int TOT = BN * PAIRS;
+    constexpr int EB = 8;  // C reads issued together: one memory round trip per 8 pairs
+    const bool full = vec && i0 + BM <= g.m && j0 + BN <= g.n;
+    for (int e0 = tid; e0 < TOT; e0 += EB * C::NT) {
+      if (full) {
+        double* cps[EB];
+        double2 cv[EB];
+#pragma unroll
+        for (int u = 0; u < EB; ++u) {
+          const int e = e0 + u * C::NT;
+          const int col = e / PAIRS, rp = (e % PAIRS) * 2;
+          const int64_t gj = j0 + col;
+          const int64_t cj = g.cmap ? (int64_t)g.cmap[gj] : gj;
+          cps[u] = g.C + (i0 + rp) + cj * g.ldc;
+          cv[u] = (e < TOT && g.beta != 0.0) ? *reinterpret_cast<const double2*>(cps[u])
+                                             : make_double2(0.0, 0.0);
         }
-        *reinterpret_cast<double2*>(cp) = o;
-      } else {
-        cp[0] = (g.beta == 0.0) ? v0 : v0 + g.beta * cp[0];
-        if (gi + 1 < g.m) cp[1] = (g.beta == 0.0) ? v1 : v1 + g.beta * cp[1];
+#pragma unroll
+        for (int u = 0; u < EB; ++u) {
+          const int e = e0 + u * C::NT;
+          if (e >= TOT) continue;
+          const int col = e / PAIRS, rp = (e % PAIRS) * 2;
+          double2 o;
+          o.x = g.alpha * Cs[col * LDC + rp] + g.beta * cv[u].x;
+          o.y = g.alpha * Cs[col * LDC + rp + 1] + g.beta * cv[u].y;
+          *reinterpret_cast<double2*>(cps[u]) = o;
+        }
+        continue;
+      }
+      for (int u = 0; u < EB; ++u) {
+        const int e = e0 + u * C::NT;
+        if (e >= TOT) break;
+        const int col = e / PAIRS, rp = (e % PAIRS) * 2;
+        const int64_t gj = j0 + col, gi = i0 + rp;
+        if (gj >= g.n || gi >= g.m) continue;
+        const int64_t cj = g.cmap ? (int64_t)g.cmap[gj] : gj;
+        double* cp = g.C + gi + cj * g.ldc;
+        const double v0 = g.alpha * Cs[col * LDC + rp], v1 = g.alpha * Cs[col * LDC + rp + 1];
+        if (vec && gi + 1 < g.m) {
+          double2 o;
+          if (g.beta != 0.0) {
+            const double2 c = *reinterpret_cast<const double2*>(cp);
+            o.x = v0 + g.beta * c.x;
+            o.y = v1 + g.beta * c.y;
+          } else {
+            o.x = v0;
+            o.y = v1;
+          }
+          *reinterpret_cast<double2*>(cp) = o;
+        } else {
+          cp[0] = (g.beta == 0.0) ? v0 : v0 + g.beta * cp[0];
+          if (gi + 1 < g.m) cp[1] = (g.beta == 0.0) ? v1 : v1 + g.beta * cp[1];
+        }
       }
     }
     return;
