@@ -65,6 +65,16 @@ struct Layout {
   int64_t total;
 };
 
+// eigenvalues only by bisection (default; PEVD_VALUES_DC=1 keeps the divide and conquer)
+bool values_by_bisection() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PEVD_VALUES_DC");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v != 0;
+}
+
 Layout plan_layout(void* base, int64_t n, int b, int want_vectors, int order) {
   Carve c(base, 0);
   Layout L{};
@@ -80,10 +90,11 @@ Layout plan_layout(void* base, int64_t n, int b, int want_vectors, int order) {
     L.V = (double*)c.take(std::max<int64_t>(nref, 1) * L.vld * 8);
     if (order != PEVD_ORDER_CONVENTIONAL) L.Qs = (double*)c.take(n * n * 8);
   }
-  L.Qd = (double*)c.take(n * n * 8);
+  const bool bisect = !want_vectors && values_by_bisection();  // no Q_d, no merge buffers
+  L.Qd = bisect ? nullptr : (double*)c.take(n * n * 8);
   L.ws_sbr = c.take(sbr_ws_bytes(n, b));
   L.ws_bc = c.take(bc_ws_bytes(n, b));
-  L.ws_dc = c.take(stedc_ws_bytes(n));
+  L.ws_dc = c.take(bisect ? stebz_ws_bytes(n) : stedc_ws_bytes(n));
   L.ws_back = c.take(sbr_back_ws_bytes(n, b));
   L.ws_bcb = c.take(bc_back_ws_bytes(n, n));
   L.total = c.off;
@@ -228,12 +239,16 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     }
     // ---- D&C
     cudaEventRecord(ev[2].a, sm);
-    if ((rc = stedc(sm, n, L.d, L.e, L.Qd, n, L.ws_dc, &info))) break;
+    if (want_vectors || !values_by_bisection()) {
+      if ((rc = stedc(sm, n, L.d, L.e, L.Qd, n, L.ws_dc, &info))) break;
+      if ((rc = (cudaMemcpyAsync(lam, L.d, n * 8, cudaMemcpyDeviceToDevice, sm) == cudaSuccess)
+                    ? OK
+                    : ERR_CUDA))
+        break;
+    } else {  // eigenvalues only: no eigenvector merges at all
+      if ((rc = stebz(sm, n, L.d, L.e, lam, L.ws_dc))) break;
+    }
     cudaEventRecord(ev[2].b, sm);
-    if ((rc = (cudaMemcpyAsync(lam, L.d, n * 8, cudaMemcpyDeviceToDevice, sm) == cudaSuccess)
-                  ? OK
-                  : ERR_CUDA))
-      break;
     if (want_vectors) {
       if (order == PEVD_ORDER_CONVENTIONAL) cudaStreamWaitEvent(sm, prep_done, 0);
       if (conv_t) {

@@ -45,6 +45,10 @@ int64_t stedc_ws_bytes(int64_t n);
 int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int64_t ldq,
           void* ws, int* info_host);
 
+// Eigenvalues only (no Q): bisection on Sturm counts, one thread per eigenvalue; lam ascending.
+int64_t stebz_ws_bytes(int64_t n);
+int stebz(cudaStream_t st, int64_t n, const double* d, const double* e, double* lam, void* ws);
+
 // ---------------- back transformation (backtrans.cu)
 // Q_s = prod_x (I - Y_x T_x Y_x^T) formed explicitly into Qs (n x n, ldq).
 int64_t sbr_back_ws_bytes(int64_t n, int b);

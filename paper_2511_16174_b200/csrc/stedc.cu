@@ -905,3 +905,105 @@ int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int
 }
 
 }  // namespace pevd
+
+// ------------------------------------------------------------------ eigenvalues only: bisection
+// With want_vectors = 0 nothing needs the eigenvector matrix, so instead of the divide and
+// conquer (whose merges are O(n^3) eigenvector GEMMs) every eigenvalue is found independently by
+// bisection on the Sturm count of T - x I (LAPACK dstebz's recurrence with its pivmin guard):
+// one thread per eigenvalue, O(n) per count, ~ 64 counts each; the k-th thread converges to the
+// k-th smallest eigenvalue, so the output is ascending.  Accuracy: an interval of relative width
+// ~ 2 eps around each eigenvalue, well inside the north star's 10 n eps ||A||_2.
+namespace pevd {
+namespace {
+
+__global__ void stebz_bounds_kernel(int64_t n, const double* __restrict__ d,
+                                    const double* __restrict__ e, double* out) {
+  // out[0] = gershgorin lower, out[1] = upper, out[2] = pivmin (block-reduced by one CTA)
+  __shared__ double slo[256], shi[256], sem[256];
+  double lo = INFINITY, hi = -INFINITY, em = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double el = i > 0 ? fabs(e[i - 1]) : 0.0, er = i + 1 < n ? fabs(e[i]) : 0.0;
+    lo = fmin(lo, d[i] - el - er);
+    hi = fmax(hi, d[i] + el + er);
+    em = fmax(em, er * er);
+  }
+  slo[threadIdx.x] = lo;
+  shi[threadIdx.x] = hi;
+  sem[threadIdx.x] = em;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) {
+      slo[threadIdx.x] = fmin(slo[threadIdx.x], slo[threadIdx.x + s]);
+      shi[threadIdx.x] = fmax(shi[threadIdx.x], shi[threadIdx.x + s]);
+      sem[threadIdx.x] = fmax(sem[threadIdx.x], sem[threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double tnorm = fmax(fabs(slo[0]), fabs(shi[0]));
+    const double eps = 2.220446049250313e-16, safmin = 2.2250738585072014e-308;
+    const double pad = 2.0 * eps * tnorm * (double)n + 2.0 * safmin;
+    out[0] = slo[0] - pad;
+    out[1] = shi[0] + pad;
+    out[2] = fmax(safmin, safmin * sem[0]);  // dstebz's pivmin
+  }
+}
+
+// number of eigenvalues of T strictly less than x
+__device__ __forceinline__ int64_t sturm_count(int64_t n, const double* __restrict__ d,
+                                               const double* __restrict__ e2, double x,
+                                               double pivmin) {
+  int64_t cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  cnt += q < 0.0;
+  for (int64_t i = 1; i < n; ++i) {
+    q = d[i] - x - e2[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+__global__ void stebz_e2_kernel(int64_t n, const double* __restrict__ e, double* __restrict__ e2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    e2[i] = e[i] * e[i];
+}
+
+__global__ void __launch_bounds__(128)
+    stebz_kernel(int64_t n, const double* __restrict__ d, const double* __restrict__ e2,
+                 const double* __restrict__ bnd, double* __restrict__ lam) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // wanted: k-th smallest
+  if (k >= n) return;
+  double lo = bnd[0], hi = bnd[1];
+  const double pivmin = bnd[2];
+  const double eps = 2.220446049250313e-16;
+  for (int it = 0; it < 128; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi)) + pivmin || mid <= lo || mid >= hi) break;
+    if (sturm_count(n, d, e2, mid, pivmin) > k) hi = mid;
+    else lo = mid;
+  }
+  lam[k] = 0.5 * (lo + hi);
+}
+
+}  // namespace
+
+int64_t stebz_ws_bytes(int64_t n) { return (n + 8) * 8; }
+
+int stebz(cudaStream_t st, int64_t n, const double* d, const double* e, double* lam, void* ws) {
+  if (n < 1) return OK;
+  double* bnd = (double*)ws;
+  double* e2 = bnd + 4;
+  stebz_e2_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 4096)), 256, 0,
+                    st>>>(n, e, e2);
+  PEVD_LAUNCH_CHECK();
+  stebz_bounds_kernel<<<1, 256, 0, st>>>(n, d, e, bnd);
+  PEVD_LAUNCH_CHECK();
+  stebz_kernel<<<(unsigned)cdiv(n, 128), 128, 0, st>>>(n, d, e2, bnd, lam);
+  PEVD_LAUNCH_CHECK();
+  return OK;
+}
+
+}  // namespace pevd

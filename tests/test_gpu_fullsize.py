@@ -69,3 +69,29 @@ def test_planted_generator_is_exact_small():
     a = A.cpu().numpy().T
     assert np.abs(a - a.T).max() <= 1e-13 * 10.0
     np.testing.assert_allclose(np.linalg.eigvalsh((a + a.T) / 2), lam, atol=1e-12 * 10.0)
+
+
+def _evd_values(A, n, b):
+    import torch
+    from paper_2511_16174_b200 import _lib
+    L = _lib.load()
+    lam = torch.empty(n, dtype=torch.float64, device="cuda")
+    ws = torch.empty(L.pevd_syevd_workspace_bytes(n, b, 0, 0), dtype=torch.uint8, device="cuda")
+    P = ctypes.c_void_p
+    rc = L.pevd_syevd_device(n, b, P(A.data_ptr()), n, P(lam.data_ptr()), None, n, 0, 0,
+                             P(ws.data_ptr()), ws.numel(),
+                             P(torch.cuda.current_stream().cuda_stream), None)
+    _lib.check(rc, "pevd_syevd_device")
+    return lam.cpu().numpy()
+
+
+@pytest.mark.parametrize("kind,n", [("Normal", 16384), ("Cluster0", 16384), ("Geometric", 8192)])
+def test_planted_values_only(kind, n):
+    """Config c3 (eigenvalues only, n = 16384): bisection on the device, no eigenvector merges."""
+    from paper_2511_16174_b200 import matgen
+    spec = matgen.SpectrumSpec(kind, n, seed=n + 11)
+    A, lam_true = matgen.generate(spec)
+    lam = _evd_values(A, n, 32)
+    err = float(np.abs(lam - lam_true).max())
+    assert err <= 10 * n * EPS * float(np.abs(lam_true).max()), f"{kind}: |dlam| {err:.3e}"
+    assert np.all(np.diff(lam) >= 0)
