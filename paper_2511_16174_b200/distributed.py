@@ -180,6 +180,40 @@ def _allgather_uneven(t: torch.Tensor, counts, group, dim0_extra):
     return res.to(t.device) if staged else res
 
 
+SBR_BACK_AGG = 32  # panels per aggregated SBR-Back block reflector (as the single-GPU path)
+
+
+def _aggregate(ops, group, n):
+    """One block reflector I - Y T Y^T = H_x0 ... H_x1 for consecutive panels (LAPACK larft
+    'F', merged panel by panel): Y is the m0 x K staircase of the panels' Y (zero above each
+    panel's first row), T_new = [[T, -T (Y^T Y_x) T_x], [0, T_x]].  Returns (t0, Y, T) as
+    column-major device tensors."""
+    t0 = group[0][2]
+    m0 = n - t0
+    K = sum(pw for _, pw, _, _, _ in group)
+    Y = ops.zeros(m0, K)
+    off = 0
+    T = None
+    for (c0, pw, tx, Yx, Tx) in group:
+        Y[off:off + pw, tx - t0:] = Yx
+        if T is None:
+            T = Tx.clone()
+        else:
+            G = ops.zeros(off, pw)
+            ops.gemm(Y[:off], Y[off:off + pw], G, ta=True)   # Y_prev^T Y_x
+            Tg = ops.zeros(off, pw)
+            ops.gemm(T, G, Tg)                                # T G
+            T12 = ops.zeros(off, pw)
+            ops.gemm(Tg, Tx, T12, alpha=-1.0)                 # -T G T_x
+            Tn = ops.zeros(off + pw, off + pw)
+            Tn[:off, :off] = T
+            Tn[off:, :off] = T12
+            Tn[off:, off:] = Tx
+            T = Tn
+        off += pw
+    return t0, Y, T
+
+
 def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
     """Blockwise multi-process EVD.
 
@@ -336,14 +370,15 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
     Mrow = np.zeros((r1 - r0, n))
     Mrow[np.arange(r1 - r0), np.arange(r0, r1)] = 1.0
     Mt = ops.from_host(Mrow)                 # column-major (r x n)
-    for (c0, pw, t0, Y, T) in panels:        # M <- M (I - Y T Y^T), creation order
-        m = n - t0
+    for g0 in range(0, len(panels), SBR_BACK_AGG):    # M <- M (I - Y T Y^T), creation order
+        t0, Yg, Tg = _aggregate(ops, panels[g0:g0 + SBR_BACK_AGG], n)
+        K = Tg.shape[0]
         Ms = Mt[t0:]                          # column-major r x m
-        P1 = ops.zeros(r1 - r0, pw)
-        ops.gemm(Ms, Y, P1)                   # M Y
-        P2 = ops.zeros(r1 - r0, pw)
-        ops.gemm(P1, T, P2)                   # (M Y) T
-        ops.gemm(P2, Y, Ms, alpha=-1.0, beta=1.0, tb=True)  # -= (M Y T) Y^T
+        P1 = ops.zeros(r1 - r0, K)
+        ops.gemm(Ms, Yg, P1)                  # M Y
+        P2 = ops.zeros(r1 - r0, K)
+        ops.gemm(P1, Tg, P2)                  # (M Y) T
+        ops.gemm(P2, Yg, Ms, alpha=-1.0, beta=1.0, tb=True)  # -= (M Y T) Y^T
     trace.add(rank, "SBR-Back", rank, t_sb, now())
     t_bb = now()
     Msb = ops.bc_back_right(n, b, tau, V, Mt)   # rows of Q_s Q_b (in place)
