@@ -181,6 +181,7 @@ def _allgather_uneven(t: torch.Tensor, counts, group, dim0_extra):
 
 
 SBR_BACK_AGG = 32  # panels per aggregated SBR-Back block reflector (as the single-GPU path)
+SBR_NBB = 16       # panels per double-blocked SBR group (rank-2 * 16 * b trailing updates)
 
 
 def _aggregate(ops, group, n):
@@ -250,12 +251,14 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
 
     # own column block, all rows: tensor (width, n) = column-major n x width
     blk = a(c0w, c1w) if dense is None else ops.from_host(dense[:, c0w:c1w])
-    panels = []  # (c0, pw, Y (pw, m) col-major, T (pw, pw))
+    panels = []  # (c0, pw, t0, Y (pw, m) col-major, T (pw, pw))
     t_sbr0 = now()
-    for idx, (c0, pw, t0) in enumerate(round_schedule(n, b)):
+
+    def factor(c0, pw, t0):
+        """Gather the panel at its owner (pieces of straddling panels, C2), factor it there,
+        return the R pieces (C3) and broadcast the factor (C4).  Returns (Y, T)."""
         m = n - t0
         owner = owner_of(c0)
-        # ---- gather the panel at its owner (pieces of straddling panels, C2) ----
         if rank == owner:
             P = ops.zeros(m, pw)
             hi = min(c0 + pw, c1w)
@@ -266,13 +269,11 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
                 continue
             ledger.record(x, owner, "SBR-panel", (xhi - xlo) * m)
             if rank == x:
-                piece = blk[xlo - c0w: xhi - c0w, t0:].contiguous()
-                _send(piece, owner, group)
+                _send(blk[xlo - c0w: xhi - c0w, t0:].contiguous(), owner, group)
             elif rank == owner:
                 piece = torch.empty((xhi - xlo, m), dtype=torch.float64, device=blk.device)
                 _recv(piece, x, group)
                 P[xlo - c0: xhi - c0] = piece
-        # ---- factor at the owner, return R pieces (C3), broadcast the factor (C4) ----
         if rank == owner:
             R, Y, T = ops.panel_qr(P)
             Rfull = torch.zeros((pw, m), dtype=torch.float64, device=blk.device)
@@ -296,45 +297,101 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
         _bcast(Y, owner, group)
         _bcast(T, owner, group)
         ledger.record(owner, BROADCAST, "SBR", 2 * m * pw)  # the reference ships (W, Y)
-        W = ops.zeros(m, pw)
-        ops.gemm(Y, T, W)  # W = Y T
-        # ---- A W rows of our columns, by symmetry (C5) ----
+        return Y, T
+
+    def form_z(t0, pw, Y, W, corr=None):
+        """A W from our columns by symmetry (C5; `corr` subtracts the block's pending
+        contribution from our rows), all-gathered, then Z = AW - 1/2 Y (W^T AW)."""
         rlo = max(t0, c0w)
         counts = [max(0, ranges[x][1] - max(t0, ranges[x][0])) for x in range(G)]
         if rlo < c1w:
             cols = blk[rlo - c0w:, t0:]            # (c, m): column-major m x c
             piece_cm = ops.zeros(c1w - rlo, pw)     # (pw, c): column-major c x pw
             ops.gemm(cols, W, piece_cm, ta=True)    # cols^T W
+            if corr is not None:
+                corr(piece_cm, rlo)
             piece = piece_cm.t().contiguous()       # (c, pw): row-major rows of AW
         else:
             piece = torch.zeros((0, pw), dtype=torch.float64, device=blk.device)
         for x in range(G):
             if counts[x] > 0:
                 ledger.record(x, BROADCAST, "SBR", counts[x] * pw)
-        AW_rows = _allgather_uneven(piece, counts, group, (pw,))   # (m, pw) row-major
-        AW = AW_rows.t().contiguous()                               # column-major m x pw
-        # Z = AW - 1/2 Y (W^T AW)
+        AW = _allgather_uneven(piece, counts, group, (pw,)).t().contiguous()  # col-major m x pw
         M = ops.zeros(pw, pw)
         ops.gemm(W, AW, M, ta=True)
         Z = AW.clone()
         ops.gemm(Y, M, Z, alpha=-0.5, beta=1.0)
-        # ---- two-sided update of our columns (rows t0..n) ----
-        if rlo < c1w:
-            zlo = rlo - t0
-            C = blk[rlo - c0w:, t0:]                  # column-major m x c
-            Yc = Y[:, zlo:zlo + (c1w - rlo)]          # column-major c x pw (rows of Y)
-            Zc = Z[:, zlo:zlo + (c1w - rlo)]
-            ops.gemm(Y, Zc, C, alpha=-1.0, beta=1.0, tb=True)   # -= Y Z_c^T
-            ops.gemm(Z, Yc, C, alpha=-1.0, beta=1.0, tb=True)   # -= Z Y_c^T
-        # ---- ragged last round: coupling columns get Q^T from the left (sbr.py:175-182) ----
+        return Z
+
+    sched = round_schedule(n, b)
+    nrounds = len(sched)
+    x = 0
+    while x < nrounds:
+        c0, pw, t0 = sched[x]
         if pw < b:
-            klo, khi = max(c0 + pw, c0w), min(t0, c1w)
+            # ---- the ragged last round, one panel (sbr.py:175-182) ----
+            Y, T = factor(c0, pw, t0)
+            W = ops.zeros(n - t0, pw)
+            ops.gemm(Y, T, W)  # W = Y T
+            Z = form_z(t0, pw, Y, W)
+            rlo = max(t0, c0w)
+            if rlo < c1w:   # two-sided update of our columns (rows t0..n)
+                zlo = rlo - t0
+                C = blk[rlo - c0w:, t0:]
+                ops.gemm(Y, Z[:, zlo:zlo + (c1w - rlo)], C, alpha=-1.0, beta=1.0, tb=True)
+                ops.gemm(Z, Y[:, zlo:zlo + (c1w - rlo)], C, alpha=-1.0, beta=1.0, tb=True)
+            klo, khi = max(c0 + pw, c0w), min(t0, c1w)   # coupling columns get Q^T
             if klo < khi:
                 cp = blk[klo - c0w: khi - c0w, t0:]
                 tmp = ops.zeros(pw, khi - klo)
                 ops.gemm(W, cp, tmp, ta=True)
                 ops.gemm(Y, tmp, cp, alpha=-1.0, beta=1.0)
-        panels.append((c0, pw, t0, Y, T))
+            panels.append((c0, pw, t0, Y, T))
+            x += 1
+            continue
+        # ---- a double-blocked group of nbl full panels (as the single-GPU SBR, PAPER.md:377):
+        #      P1 = [Y_0 Z_0 Y_1 Z_1 ...], P2 = [Z_0 Y_0 ...] (block rows from t0); panel i's
+        #      columns take the pending updates P1 P2^T just before its QR, A W_i is corrected by
+        #      -P1 (P2^T W_i), and our trailing columns get ONE rank-2K update at the end
+        nbl = 1
+        while nbl < SBR_NBB and x + nbl < nrounds and sched[x + nbl][1] == b:
+            nbl += 1
+        m0 = n - t0
+        K = nbl * b
+        P1 = ops.zeros(m0, 2 * K)
+        P2 = ops.zeros(m0, 2 * K)
+        for i in range(nbl):
+            ci, _, ti = sched[x + i]
+            ri = i * b
+            if i:
+                lo, hi = max(ci, c0w), min(ci + b, c1w)
+                if lo < hi:
+                    ops.gemm(P1[: 2 * ri, ri - b:], P2[: 2 * ri, lo - t0: hi - t0],
+                             blk[lo - c0w: hi - c0w, ci:], alpha=-1.0, beta=1.0, tb=True)
+            Y, T = factor(ci, b, ti)
+            W = ops.zeros(n - ti, b)
+            ops.gemm(Y, T, W)
+            corr = None
+            if i:
+                tv = ops.zeros(2 * ri, b)
+                ops.gemm(P2[: 2 * ri, ri:], W, tv, ta=True)     # P2^T W_i
+
+                def corr(piece_cm, rlo, tv=tv, ri=ri):
+                    ops.gemm(P1[: 2 * ri, rlo - t0: c1w - t0], tv, piece_cm, alpha=-1.0,
+                             beta=1.0)
+            Z = form_z(ti, b, Y, W, corr)
+            P1[2 * ri: 2 * ri + b, ri:] = Y
+            P1[2 * ri + b: 2 * ri + 2 * b, ri:] = Z
+            P2[2 * ri: 2 * ri + b, ri:] = Z
+            P2[2 * ri + b: 2 * ri + 2 * b, ri:] = Y
+            panels.append((ci, b, ti, Y, T))
+        ru = (nbl - 1) * b
+        tl = t0 + ru
+        lo = max(tl, c0w)
+        if lo < c1w:
+            ops.gemm(P1[:, ru:], P2[:, lo - t0: c1w - t0], blk[lo - c0w:, tl:], alpha=-1.0,
+                     beta=1.0, tb=True)
+        x += nbl
     trace.add(rank, "SBR", rank, t_sbr0, now())
 
     # ---- band: our columns' diagonals, all-gathered (replaces C6/C7) ----

@@ -51,7 +51,8 @@ def _run(world, n, b, seed, skew=0.0):
     return dict(out)
 
 
-@pytest.mark.parametrize("world,n,b,skew", [(2, 48, 8, 0.0), (2, 40, 4, 0.05), (3, 91, 7, 0.0)])
+@pytest.mark.parametrize("world,n,b,skew", [(2, 48, 8, 0.0), (2, 40, 4, 0.05), (3, 91, 7, 0.0),
+                                          (2, 150, 4, 0.0)])
 def test_blockwise_protocol_matches_oracle(world, n, b, skew):
     out = _run(world, n, b, seed=n + world, skew=skew)
     g = np.random.default_rng(n + world).standard_normal((n, n))
