@@ -241,7 +241,11 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
     ledger = CommLedger()
     trace = TraceLog()
     t_base = time.perf_counter_ns()
-    now = lambda: time.perf_counter_ns() - t_base  # noqa: E731
+
+    def now():  # stage boundaries wait for the device, so the trace spans are device time
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            torch.cuda.synchronize()
+        return time.perf_counter_ns() - t_base
 
     def owner_of(col):
         for x, (lo, hi) in enumerate(ranges):
@@ -424,9 +428,9 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
     bounds = np.cumsum([0] + sizes)
     r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
     t_sb = now()
-    Mrow = np.zeros((r1 - r0, n))
-    Mrow[np.arange(r1 - r0), np.arange(r0, r1)] = 1.0
-    Mt = ops.from_host(Mrow)                 # column-major (r x n)
+    Mt = ops.zeros(r1 - r0, n)               # column-major (r x n): rows r0..r1 of I
+    ir = torch.arange(r1 - r0, device=Mt.device)
+    Mt[r0 + ir, ir] = 1.0
     for g0 in range(0, len(panels), SBR_BACK_AGG):    # M <- M (I - Y T Y^T), creation order
         t0, Yg, Tg = _aggregate(ops, panels[g0:g0 + SBR_BACK_AGG], n)
         K = Tg.shape[0]
