@@ -120,7 +120,7 @@ def run_b200_distributed(args):
     a0 = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
     a0.add_(a0.t().clone())
     a0.mul_(0.5)
-    cfg = PipelineConfig(workers=world, b=b)
+    cfg = PipelineConfig(workers=world, b=b, order=args.order)
 
     def block(c0, c1):
         return a0[c0:c1].clone()
@@ -159,7 +159,8 @@ def run_b200_distributed(args):
                 "wall_s_per_evd": round(ms / 1e3, 3), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"ONE dense symmetric FP64 EVD with eigenvectors, n={n}, "
-                                       f"b={b}, blockwise columns over {world} GPUs",
+                                       f"b={b}, order={args.order}, blockwise columns over "
+                                       f"{world} GPUs",
                            "n": n, "b": b, "parallelism": f"blockwise{world}",
                            "l2": "input >> 126 MB L2 (no flush needed)",
                            "flop_convention": "4 n^3 / wall (PAPER.md:92)"},

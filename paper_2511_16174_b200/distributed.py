@@ -122,6 +122,17 @@ class CudaOps:
         self._lib.check(rc, "stedc")
         return dd.cpu().numpy(), Q
 
+    def bc_back_left(self, n, b, tau, Vpack, X):
+        """X (column-major n x cols device tensor) <- Q_b X in place (conventional BC-Back)."""
+        V, vld = Vpack
+        cols = X.shape[0]
+        ws = torch.empty(self.L.pevd_bc_back_workspace_bytes(n, cols), dtype=torch.uint8,
+                         device=self.device)
+        rc = self.L.pevd_bc_back_left(n, b, self._p(tau), self._p(V), vld, self._p(X),
+                                      X.stride(0), cols, self._p(ws), self._stream())
+        self._lib.check(rc, "bc_back_left")
+        return X
+
     def bc_back_right(self, n, b, tau, Vpack, X):
         """X (column-major rows x n device tensor) <- X Q_b in place."""
         V, vld = Vpack
@@ -423,6 +434,36 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
     trace.add(HOST, "Solver", 0, t_s, now())
     if not cfg.want_vectors:
         return EigenResult(lam=lam), trace.events(), ledger, {}
+    if cfg.order == "conventional":
+        # ---- conventional order by columns: Q[:, ours] = Q_s Q_b Q_d[:, ours].  Every rank
+        #      already holds Q_d, the bulge reflectors and the SBR panels, so the column blocks
+        #      are independent: no Q_d / U broadcasts, no final GEMM (pipeline.py:367-387) ----
+        t_bb = now()
+        X = Qd[c0w:c1w].clone()                       # column-major n x (c1w - c0w)
+        X = ops.bc_back_left(n, b, tau, V, X)         # Q_b X
+        trace.add(rank, "BC-Back", rank, t_bb, now())
+        t_sb = now()
+        groups = [panels[g0:g0 + SBR_BACK_AGG] for g0 in range(0, len(panels), SBR_BACK_AGG)]
+        for grp in reversed(groups):                  # Q_s X = H_0 (H_1 (... X))
+            t0, Yg, Tg = _aggregate(ops, grp, n)
+            K = Tg.shape[0]
+            X2 = X[:, t0:]                            # rows t0.. of our columns
+            P1 = ops.zeros(K, c1w - c0w)
+            ops.gemm(Yg, X2, P1, ta=True)             # Y^T X
+            P2 = ops.zeros(K, c1w - c0w)
+            ops.gemm(Tg, P1, P2)                      # T (Y^T X)
+            ops.gemm(Yg, P2, X2, alpha=-1.0, beta=1.0)  # X -= Y T Y^T X
+        trace.add(rank, "SBR-Back", rank, t_sb, now())
+        if not gather_q:
+            return (EigenResult(lam=lam), trace.events(), ledger,
+                    {"cols": (c0w, c1w), "q_cols": X})
+        counts = [hi - lo for lo, hi in ranges]
+        Qc = _allgather_uneven(X, counts, group, (n,))   # (n cols, n rows): column-major Q
+        for w in range(G):
+            ledger.record(w, HOST, "Result", counts[w] * n)
+        return (EigenResult(lam=lam, Q=np.asfortranarray(Qc.cpu().numpy().T),
+                            vectors_computed=True),
+                trace.events(), ledger, {"cols": (c0w, c1w)})
     # ---- back transformation of our rows ----
     sizes = back_plan_sizes(n, G, cfg.back_skew)
     bounds = np.cumsum([0] + sizes)

@@ -47,6 +47,10 @@ class CpuOps:
         lam, q = orc.tridiag_eig(np.asarray(d), np.asarray(e), want_vectors=True)
         return lam, self.from_host(q)
 
+    def bc_back_left(self, n, b, refl, _, X):
+        x = self.to_host(X)                              # n x cols
+        return self.from_host(orc.bc_back_apply(refl, x, "conventional"))
+
     def bc_back_right(self, n, b, refl, _, X):
         x = self.to_host(X)                              # rows x n
         out = orc.bc_back_apply(refl, x.T, "reordered").T

@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n, b, seed, skew, out):
+def _worker(rank, world, port, n, b, seed, skew, out, order="pipelined"):
     import torch.distributed as dist
     import sys
     sys.path.insert(0, os.getcwd())
@@ -35,26 +35,31 @@ def _worker(rank, world, port, n, b, seed, skew, out):
         g = np.random.default_rng(seed).standard_normal((n, n))
         a = (g + g.T) / 2
         res, events, ledger, info = run_distributed(a, PipelineConfig(workers=world, b=b,
-                                                                       back_skew=skew),
+                                                                       back_skew=skew,
+                                                                       order=order),
                                                     ops=CpuOps())
         out[rank] = (res.lam, res.Q, ledger.words(stage="SBR"), ledger.words(stage="BC"),
-                     ledger.messages(stage="BC"), info["rows"])
+                     ledger.messages(stage="BC"), info.get("rows", info.get("cols")))
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, n, b, seed, skew=0.0):
+def _run(world, n, b, seed, skew=0.0, order="pipelined"):
     mgr = mp.Manager()
     out = mgr.dict()
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, n, b, seed, skew, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, n, b, seed, skew, out, order), nprocs=world, join=True)
     return dict(out)
 
 
-@pytest.mark.parametrize("world,n,b,skew", [(2, 48, 8, 0.0), (2, 40, 4, 0.05), (3, 91, 7, 0.0),
-                                          (2, 150, 4, 0.0)])
-def test_blockwise_protocol_matches_oracle(world, n, b, skew):
-    out = _run(world, n, b, seed=n + world, skew=skew)
+@pytest.mark.parametrize("world,n,b,skew,order", [(2, 48, 8, 0.0, "pipelined"),
+                                                (2, 40, 4, 0.05, "pipelined"),
+                                                (3, 91, 7, 0.0, "pipelined"),
+                                                (2, 150, 4, 0.0, "pipelined"),
+                                                (3, 91, 7, 0.0, "conventional"),
+                                                (2, 150, 4, 0.0, "conventional")])
+def test_blockwise_protocol_matches_oracle(world, n, b, skew, order):
+    out = _run(world, n, b, seed=n + world, skew=skew, order=order)
     g = np.random.default_rng(n + world).standard_normal((n, n))
     a = (g + g.T) / 2
     lam_o, _ = orc.evd(a, b, True)

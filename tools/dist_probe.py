@@ -27,7 +27,8 @@ def main():
     a0 = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
     a0.add_(a0.t().clone())
     a0.mul_(0.5)
-    cfg = PipelineConfig(workers=dist.get_world_size(), b=32)
+    order = sys.argv[2] if len(sys.argv) > 2 else "conventional"
+    cfg = PipelineConfig(workers=dist.get_world_size(), b=32, order=order)
     out = []
     for rep in range(2):
         dist.barrier()
@@ -43,7 +44,8 @@ def main():
         out.append({"rep": rep, "wall_s": round(dt, 3),
                     "stages_s": {k: round(v, 3) for k, v in stages.items()}})
     if dist.get_rank() == 0:
-        print(json.dumps({"n": n, "world": dist.get_world_size(), "runs": out}), flush=True)
+        print(json.dumps({"n": n, "world": dist.get_world_size(), "order": order, "runs": out}),
+              flush=True)
     dist.destroy_process_group()
 
 
