@@ -433,7 +433,12 @@ int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, const double* Tal
   return sbr_back_apply_left((cudaStream_t)stream, n, b, Ystair, Tall, X, ldx, ncols, workspace);
 }
 
-int64_t pevd_bc_back_workspace_bytes(int64_t n, int64_t nrows) { return bc_back_ws_bytes(n, nrows); }
+static int64_t ws_round(int64_t x) { return (x + 255) / 256 * 256; }
+
+// + room for the transpose of a left operand (the fast column-major BC-Back path, below)
+int64_t pevd_bc_back_workspace_bytes(int64_t n, int64_t nrows) {
+  return ws_round(bc_back_ws_bytes(n, nrows)) + n * nrows * 8 + 256;
+}
 
 int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
                        int64_t ldx, int64_t nrows, void* workspace, void* stream) {
@@ -442,7 +447,15 @@ int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int
 
 int pevd_bc_back_left(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
                       int64_t ldx, int64_t ncols, void* workspace, void* stream) {
-  return bc_back_left((cudaStream_t)stream, n, b, tau, V, vld, X, ldx, ncols, workspace);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (b == 32 && vld == 32 && workspace && n >= 3 && ncols > 0) {
+    // on the transpose: the DMMA kernel then reads X column-major (its coalesced pattern)
+    double* Xt = (double*)((char*)workspace + ws_round(bc_back_ws_bytes(n, ncols)));
+    PEVD_TRY(transpose(st, n, ncols, X, ldx, Xt, ncols));
+    PEVD_TRY(bc_back_left_t(st, n, b, tau, V, vld, Xt, ncols, ncols, workspace));
+    return transpose(st, ncols, n, Xt, ncols, X, ldx);
+  }
+  return bc_back_left(st, n, b, tau, V, vld, X, ldx, ncols, workspace);
 }
 
 }  // extern "C"
