@@ -111,6 +111,13 @@ int pevd_bc(int64_t n, int b, const double* bands, double* d, double* e, double*
 /* Tridiagonal divide and conquer (replaces tridiag_eig, tridiag.py:298-334): d in/out (lam
  * ascending), e (n-1) preserved, Q (n x n, ldq) eigenvectors with the reference sign convention.
  * Synchronous (returns PEVD_ERR_CONVERGE on non-convergence). */
+/* bc_reduce_partition (bulge.py:348-385): chase the sweeps [0, sweep_end) down a band of
+ * semi-bandwidth bw <= 2b (the tail relayed by the predecessor, columns renumbered from the
+ * partition start); band_out ((2b+1) x n, bands[d, j] layout) receives the band afterwards
+ * (finished rows + residual fill of the tail); reflectors in the pevd_bc slot layout of size n. */
+int pevd_bc_partition(int64_t n, int b, int bw, const double* bands, int64_t sweep_end,
+                      double* band_out, double* tau, double* V, int vld, void* workspace,
+                      void* stream);
 int64_t pevd_stedc_workspace_bytes(int64_t n);
 int pevd_stedc(int64_t n, double* d, const double* e, double* Q, int64_t ldq, void* workspace,
                void* stream);

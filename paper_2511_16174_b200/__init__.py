@@ -12,15 +12,16 @@ from .messaging import BROADCAST, HOST, CommLedger, TraceEvent, TraceLog
 from .pipeline import ORDERS, PipelineConfig, PipelineError, run, run_auto_skew
 from .schedule import (BackPlan, back_plan_sizes, comm_broadcast_words, comm_triangular_words,
                        crossover_bandwidth, make_back_plan, partition, round_schedule)
-from .stages import (BulgeReflectorSet, OverlapBlock, RowAccumulator, SbrConfig, SbrFactors,
+from .stages import (BcPartitionResult, BulgeReflectorSet, OverlapBlock, RowAccumulator, SbrConfig, SbrFactors,
                      application_order, apply_block_reflector, bc_back_apply, bc_reduce,
+                     bc_reduce_partition,
                      final_gemm, form_z, house_vector, panel_qr, sbr_back_accumulate,
                      sbr_back_rows, sbr_reduce, sym_rank2k_update, trailing_update, tridiag_eig)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BackPlan", "BandMatrix", "BulgeReflectorSet", "OverlapBlock", "RowAccumulator",
+    "BackPlan", "BandMatrix", "BcPartitionResult", "bc_reduce_partition", "BulgeReflectorSet", "OverlapBlock", "RowAccumulator",
     "application_order", "apply_block_reflector", "form_z", "sym_rank2k_update", "trailing_update", "CommLedger", "EigenResult", "FlopCounter",
     "HOST", "BROADCAST", "ORDERS", "PipelineConfig", "PipelineError", "ProtocolError",
     "ReflectorPanel", "SbrConfig", "SbrFactors", "SymmetricMatrix", "TraceEvent", "TraceLog",

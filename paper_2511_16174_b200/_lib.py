@@ -47,6 +47,7 @@ SIGNATURES = {
     "pevd_bc_num_reflectors": (_i64, [_i64, _int]),
     "pevd_bc_workspace_bytes": (_i64, [_i64, _int]),
     "pevd_bc": (_int, [_i64, _int, _vp, _vp, _vp, _vp, _vp, _int, _vp, _vp]),
+    "pevd_bc_partition": (_int, [_i64, _int, _int, _vp, _i64, _vp, _vp, _vp, _int, _vp, _vp]),
     "pevd_stedc_workspace_bytes": (_i64, [_i64]),
     "pevd_stedc": (_int, [_i64, _vp, _vp, _vp, _i64, _vp, _vp]),
     "pevd_sbr_back_workspace_bytes": (_i64, [_i64, _int]),

@@ -406,6 +406,13 @@ int pevd_bc(int64_t n, int b, const double* bands, double* d, double* e, double*
   return bc_reduce((cudaStream_t)stream, n, b, bands, d, e, tau, V, vld, workspace);
 }
 
+int pevd_bc_partition(int64_t n, int b, int bw, const double* bands, int64_t sweep_end,
+                      double* band_out, double* tau, double* V, int vld, void* workspace,
+                      void* stream) {
+  return bc_reduce_range((cudaStream_t)stream, n, b, bw, bands, sweep_end, nullptr, nullptr,
+                         band_out, tau, V, vld, workspace);
+}
+
 int64_t pevd_stedc_workspace_bytes(int64_t n) { return stedc_ws_bytes(n); }
 
 int pevd_stedc(int64_t n, double* d, const double* e, double* Q, int64_t ldq, void* workspace,

@@ -38,12 +38,23 @@ struct WarpSmem {
 
 __global__ void band_to_work(int64_t n, int b, const double* __restrict__ bands,
                              double* __restrict__ Bd, int64_t LDB, int* __restrict__ prog) {
+  // b here is the INPUT band's semi-bandwidth (<= 2 b_chase for a relayed tail)
   const int64_t total = n * LDB;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = idx / LDB, d = idx % LDB;
     Bd[idx] = (d <= b && c + d < n) ? bands[d * n + c] : 0.0;
     if (d == 0) prog[c] = 0;
+  }
+}
+
+__global__ void work_to_band(int64_t n, int bw, const double* __restrict__ Bd, int64_t LDB,
+                             double* __restrict__ out) {
+  const int64_t total = (int64_t)(bw + 1) * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t dd = idx / n, c = idx % n;
+    out[idx] = (c + dd < n) ? Bd[c * LDB + dd] : 0.0;
   }
 }
 
@@ -59,13 +70,14 @@ __global__ void work_to_tridiag(int64_t n, const double* __restrict__ Bd, int64_
 __global__ void __launch_bounds__(BC_WARPS * 32)
     bc_chase_kernel(int64_t n, int b, double* __restrict__ Bd, int64_t LDB, int* prog,
                     double* __restrict__ tau_out, double* __restrict__ V_out, int vld,
-                    int total_warps) {
+                    int total_warps, int64_t sweep_end) {
   extern __shared__ __align__(16) unsigned char smraw[];
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smraw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int64_t wglob = (int64_t)blockIdx.x * BC_WARPS + (threadIdx.x >> 5);
 
-  for (int64_t gi = wglob; gi < n - 2; gi += total_warps) {
+  const int64_t gend = sweep_end < n - 2 ? sweep_end : n - 2;
+  for (int64_t gi = wglob; gi < gend; gi += total_warps) {
     for (int64_t j = 0; gi + 1 + j * b <= n - 2; ++j) {
       // ---- wait for the predecessor sweep to complete step j+2.  Polling is a relaxed L2 load
       //      (an acquire would invalidate L1 on every poll); every band access of this kernel
@@ -221,8 +233,12 @@ static int64_t bc_ldb(int b) { return (2 * b + 2 + 1) / 2 * 2; }
 
 int64_t bc_ws_bytes(int64_t n, int b) { return n * bc_ldb(b) * 8 + n * 4 + 256; }
 
-int bc_reduce(cudaStream_t st, int64_t n, int b, const double* bands_ref, double* d, double* e,
-              double* tau, double* V, int vld, void* ws) {
+// The chase of the sweeps [0, sweep_end) on a band of semi-bandwidth bw <= 2b (the relayed tail
+// of a partition, bulge.py:348-385); band_out (optional, (2b+1) x n reference layout) receives the
+// resulting band with its residual fill, d / e (optional) its tridiagonal part.
+int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* bands_ref,
+                    int64_t sweep_end, double* d, double* e, double* band_out, double* tau,
+                    double* V, int vld, void* ws) {
   if (b < 1 || b > BMAX) {
     set_error("bc_reduce: bandwidth %d outside [1, %d] (device kernel limit)", b, BMAX);
     return ERR_VALUE;
@@ -234,8 +250,12 @@ int bc_reduce(cudaStream_t st, int64_t n, int b, const double* bands_ref, double
   const int64_t LDB = bc_ldb(b);
   double* Bd = (double*)ws;
   int* prog = (int*)(Bd + n * LDB);
+  if (bw < 0 || bw > 2 * b) {
+    set_error("bc_reduce: input bandwidth %d outside [0, 2b]", bw);
+    return ERR_VALUE;
+  }
   band_to_work<<<(unsigned)std::min<int64_t>(cdiv(n * LDB, 256), 8192), 256, 0, st>>>(
-      n, b, bands_ref, Bd, LDB, prog);
+      n, bw, bands_ref, Bd, LDB, prog);
   PEVD_LAUNCH_CHECK();
   if (b >= 2 && n >= 3) {
     const size_t smem = sizeof(WarpSmem) * BC_WARPS;
@@ -261,15 +281,27 @@ int bc_reduce(cudaStream_t st, int64_t n, int b, const double* bands_ref, double
     const int64_t need = cdiv(want_warps, BC_WARPS);
     const int grid = (int)std::min<int64_t>((int64_t)per_sm * num_sms(), need);
     bc_chase_kernel<<<grid, BC_WARPS * 32, smem, st>>>(n, b, Bd, LDB, prog, tau, V, vld,
-                                                       grid * BC_WARPS);
+                                                       grid * BC_WARPS, sweep_end);
     PEVD_LAUNCH_CHECK();
   } else if (tau && n >= 3) {
     PEVD_CUDA(cudaMemsetAsync(tau, 0, 8 * bc_num_reflectors(n, b), st));
   }
-  work_to_tridiag<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4096), 256, 0, st>>>(n, Bd, LDB, d,
-                                                                                  e);
-  PEVD_LAUNCH_CHECK();
+  if (d && e) {
+    work_to_tridiag<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4096), 256, 0, st>>>(n, Bd, LDB,
+                                                                                    d, e);
+    PEVD_LAUNCH_CHECK();
+  }
+  if (band_out) {
+    work_to_band<<<(unsigned)std::min<int64_t>(cdiv(n * (2 * b + 1), 256), 8192), 256, 0, st>>>(
+        n, 2 * b, Bd, LDB, band_out);
+    PEVD_LAUNCH_CHECK();
+  }
   return OK;
+}
+
+int bc_reduce(cudaStream_t st, int64_t n, int b, const double* bands_ref, double* d, double* e,
+              double* tau, double* V, int vld, void* ws) {
+  return bc_reduce_range(st, n, b, b, bands_ref, n, d, e, nullptr, tau, V, vld, ws);
 }
 
 }  // namespace pevd

@@ -37,6 +37,11 @@ int64_t bc_ws_bytes(int64_t n, int b);
 // stride vld) in canonical chase-step-major order when tau != null.
 int bc_reduce(cudaStream_t st, int64_t n, int b, const double* bands_ref, double* d, double* e,
               double* tau, double* V, int vld, void* ws);
+// Partition chase (bulge.py:348-385): sweeps [0, sweep_end) on a band of semi-bandwidth bw <= 2b;
+// band_out ((2b+1) x n, may be null) gets the band afterwards, d / e (may be null) its diagonals.
+int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* bands_ref,
+                    int64_t sweep_end, double* d, double* e, double* band_out, double* tau,
+                    double* V, int vld, void* ws);
 
 // ---------------- tridiagonal divide and conquer (stedc.cu)
 int64_t stedc_ws_bytes(int64_t n);

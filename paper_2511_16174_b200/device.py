@@ -138,6 +138,27 @@ def bc(bands, want_reflectors=True):
     return d.cpu().numpy()[:n], e.cpu().numpy()[: n - 1], out_tau, out_v
 
 
+def bc_partition(bands, b: int, sweep_end: int):
+    """Partition chase (bulge.py:348-385) on a band of semi-bandwidth bw = bands.shape[0] - 1
+    <= 2b: sweeps [0, sweep_end) -> ((2b+1) x n band afterwards, tau slots, V slots)."""
+    L = _lib.load()
+    bands = np.ascontiguousarray(bands, dtype=np.float64)
+    bw, n = bands.shape[0] - 1, bands.shape[1]
+    torch = _torch()
+    dbands = torch.from_numpy(bands.reshape(-1)).cuda()
+    out = torch.zeros((2 * b + 1) * n, dtype=torch.float64, device="cuda")
+    nref = L.pevd_bc_num_reflectors(n, b)
+    vld = ((b + 7) // 8) * 8
+    tau = torch.zeros(max(nref, 1), dtype=torch.float64, device="cuda")
+    V = torch.zeros(max(nref, 1) * vld, dtype=torch.float64, device="cuda")
+    ws = workspace(L.pevd_bc_workspace_bytes(n, b))
+    rc = L.pevd_bc_partition(n, b, bw, _p(dbands), int(sweep_end), _p(out), _p(tau), _p(V), vld,
+                             _p(ws), _stream())
+    _lib.check(rc, "bc_partition")
+    return (out.cpu().numpy().reshape(2 * b + 1, n), tau.cpu().numpy()[:nref],
+            V.cpu().numpy()[: nref * vld].reshape(nref, vld))
+
+
 def slot_offset(n: int, b: int, j: int) -> int:
     """Fixed reflector slot layout of pevd_bc: slot(i, j) = offset(j) + i (include/pevd.h)."""
     return j * (n - 2) - b * j * (j - 1) // 2

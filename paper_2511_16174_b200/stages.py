@@ -279,6 +279,87 @@ class BulgeReflectorSet:
         return self._slots
 
 
+@dataclass
+class BcPartitionResult:
+    """One worker's share of the relayed chase (bulge.py:312-318)."""
+
+    d_part: np.ndarray
+    e_part: np.ndarray
+    reflectors: "BulgeReflectorSet"
+    outgoing: "OverlapBlock | None"
+    tail: BandMatrix | None  # the modified band beyond pivot_end, None for the last worker
+
+
+def _validate_incoming(incoming, col0: int, b: int) -> None:
+    """bulge.py:335-345: the predecessor's overlap block must be empty but the bridge entry."""
+    if incoming.offset != col0:
+        raise ProtocolError(f"overlap offset {incoming.offset} does not match boundary {col0}")
+    if incoming.b != b:
+        raise ProtocolError("overlap bandwidth mismatch")
+    mask = np.ones(incoming.values.shape, dtype=bool)
+    mask[0, b - 1] = False  # the subdiagonal bridge entry may be nonzero
+    if np.any(incoming.values[mask] != 0.0):
+        raise ProtocolError("overlap block contains fill outside the bridge entry")
+
+
+def bc_reduce_partition(band_tail: BandMatrix, b: int, col0: int, pivot_end: int,
+                        incoming=None, is_last: bool = False,
+                        counter: FlopCounter | None = None) -> BcPartitionResult:
+    """Chase all sweeps with pivot in [col0, pivot_end) down the band tail on the GPU
+    (bulge.py:348-385).  `band_tail` covers global columns [col0, n) with semi-bandwidth <= 2b.
+    The device chase runs on the tail renumbered from 0 (the chase is translation invariant) and
+    stops after the partition's sweeps; the result is bit-identical to the same sweeps of the
+    whole-band chase."""
+    m = band_tail.n
+    n = col0 + m
+    if col0 > 0:
+        if incoming is None:
+            raise ProtocolError("interior worker started bulge chasing without its "
+                                "predecessor's overlap block")
+        _validate_incoming(incoming, col0, b)
+    elif incoming is not None:
+        raise ProtocolError("first worker must not receive an overlap block")
+    npiv = max(0, min(pivot_end, n) - col0)
+    if b <= 1 or m < 3:
+        out = np.zeros((max(2 * b, 1) + 1, m))
+        src = band_tail.bands
+        out[: src.shape[0], :] = src[:, :m]
+        refl = BulgeReflectorSet.empty(n, max(b, 1))
+    else:
+        out, tau, V = device.bc_partition(band_tail.bands, b, npiv)
+        r = device.slots_to_reference(m, b, tau, V)
+        keep = r["i"] < npiv
+        refl = BulgeReflectorSet(n, b, r["i"][keep] + col0, r["j"][keep], r["row0"][keep] + col0,
+                                 r["len"][keep], r["tau"][keep], r["v"][keep])
+        if counter is not None:
+            counter.add("BC", int(7 * b * b * len(refl)))
+    # finished rows: the band below the first subdiagonal must be exactly zero there
+    hi = npiv
+    for dd in range(2, out.shape[0]):
+        if hi and np.any(out[dd, : max(0, min(hi, m - dd))] != 0.0):
+            raise ProtocolError("bulge chasing left fill in finished columns")
+    d_part = np.ascontiguousarray(out[0, :hi])
+    e_part = np.ascontiguousarray(out[1, : min(hi, m - 1)]) if out.shape[0] > 1 else np.zeros(0)
+    if is_last:
+        return BcPartitionResult(d_part, e_part, refl, None, None)
+    # the 2b x b overlap block: rows [pivot_end, pivot_end+2b) x columns [pivot_end-b, pivot_end)
+    vals = np.zeros((2 * b, b))
+    for rr in range(2 * b):
+        gr = pivot_end + rr
+        if gr >= n:
+            break
+        for cc in range(b):
+            gc = pivot_end - b + cc
+            if gc >= col0 and 0 <= gr - gc < out.shape[0]:
+                vals[rr, cc] = out[gr - gc, gc - col0]
+    outgoing = OverlapBlock(values=vals, offset=pivot_end, b=b)
+    rest = out[:, pivot_end - col0:]
+    mr = rest.shape[1]
+    bw = min(2 * b, mr - 1) if mr > 1 else 0
+    tail = BandMatrix(n=mr, b=bw, bands=np.ascontiguousarray(rest[: bw + 1]))
+    return BcPartitionResult(d_part, e_part, refl, outgoing, tail)
+
+
 def bc_reduce(band: BandMatrix, counter: FlopCounter | None = None):
     """Band -> tridiagonal on the GPU wavefront chase (bulge.py:299-309)."""
     n, b = band.n, band.b
