@@ -11,7 +11,8 @@ from .core import (EPS, BandMatrix, EigenResult, FlopCounter, ProtocolError, Ref
 from .messaging import BROADCAST, HOST, CommLedger, TraceEvent, TraceLog
 from .pipeline import ORDERS, PipelineConfig, PipelineError, run, run_auto_skew
 from .schedule import (BackPlan, back_plan_sizes, comm_broadcast_words, comm_triangular_words,
-                       crossover_bandwidth, make_back_plan, partition, round_schedule)
+                       crossover_bandwidth, make_back_plan, mean_idle_fraction, partition,
+                       round_schedule, validate_trace)
 from .stages import (BcPartitionResult, BulgeReflectorSet, OverlapBlock, RowAccumulator, SbrConfig, SbrFactors,
                      application_order, apply_block_reflector, bc_back_apply, bc_reduce,
                      bc_reduce_partition,
@@ -28,5 +29,6 @@ __all__ = [
     "TridiagonalMatrix", "back_plan_sizes", "bc_back_apply", "bc_reduce", "comm_broadcast_words",
     "comm_triangular_words", "crossover_bandwidth", "final_gemm", "house_vector",
     "make_back_plan", "panel_qr", "partition", "round_schedule", "run", "run_auto_skew",
-    "sbr_back_accumulate", "sbr_back_rows", "sbr_reduce", "tridiag_eig",
+    "sbr_back_accumulate", "sbr_back_rows", "sbr_reduce", "tridiag_eig", "validate_trace",
+    "mean_idle_fraction",
 ]

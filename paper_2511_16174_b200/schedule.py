@@ -190,3 +190,62 @@ def bc_back_macs_fast(n: int, b: int, ncols: int) -> int:
         nref += n - 2 - j * b
         j += 1
     return 2 * b * nref * ncols
+
+
+# ------------------------------------------------------------------ trace contract
+def validate_trace(events, workers: int, ledger=None) -> None:
+    """Raise ValueError when a trace breaks the pipeline's dependency contract
+    (schedule.py:334-386): no two non-Comm events of one worker overlap; the SBR and BC chains
+    run worker after worker; BC-Back starts after every BC event (the reflector gather);
+    FinalMultiply starts after the solver; with a ledger, exactly one boundary message per
+    neighbouring worker pair in the BC stage."""
+    for w in range(workers):
+        mine = sorted((e for e in events if e.worker == w and e.stage != "Comm"),
+                      key=lambda e: (e.t_start, e.t_end))
+        for x, y in zip(mine, mine[1:]):
+            if y.t_start < x.t_end:
+                raise ValueError(f"worker {w}: {x.stage} [{x.t_start},{x.t_end}) overlaps "
+                                 f"{y.stage} [{y.t_start},{y.t_end})")
+    for stage in ("SBR", "BC"):
+        for w in range(workers - 1):
+            left = [e.t_end for e in events if e.stage == stage and e.worker == w]
+            right = [e.t_start for e in events if e.stage == stage and e.worker == w + 1]
+            if left and right and max(left) > min(right):
+                raise ValueError(f"{stage} chain broken between workers {w} and {w + 1}")
+
+    def ends(stage):
+        return [e.t_end for e in events if e.stage == stage]
+
+    def starts(stage):
+        return [e.t_start for e in events if e.stage == stage]
+
+    if ends("BC") and starts("BC-Back") and min(starts("BC-Back")) < max(ends("BC")):
+        raise ValueError(f"BC-Back starts at {min(starts('BC-Back'))} before the reflector "
+                         f"gather completes at {max(ends('BC'))}")
+    if ends("Solver") and starts("FinalMultiply") and \
+            min(starts("FinalMultiply")) < max(ends("Solver")):
+        raise ValueError(f"FinalMultiply starts at {min(starts('FinalMultiply'))} before the "
+                         f"solver finishes at {max(ends('Solver'))}")
+    if ledger is not None and workers > 1:
+        for w in range(workers - 1):
+            m = ledger.messages(stage="BC", src=w, dst=w + 1)
+            if m != 1:
+                raise ValueError(f"expected exactly one overlap message from worker {w} to "
+                                 f"{w + 1}, ledger has {m}")
+        total = ledger.messages(stage="BC")
+        if total != workers - 1:
+            raise ValueError(f"stray BC-stage messages: {total} total for {workers - 1} "
+                             f"boundaries")
+
+
+def mean_idle_fraction(events, workers: int) -> float:
+    """1 - busy / span averaged over the workers, helper lanes excluded (schedule.py:389-402)."""
+    spans = [e for e in events if e.stage != "Comm"]
+    if not spans:
+        return 0.0
+    t0 = min(e.t_start for e in spans)
+    t1 = max(e.t_end for e in spans)
+    if t1 == t0:
+        return 0.0
+    return sum(1.0 - sum(e.duration for e in spans if e.worker == w) / (t1 - t0)
+               for w in range(workers)) / workers
