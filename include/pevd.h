@@ -123,6 +123,11 @@ int pevd_stedc(int64_t n, double* d, const double* e, double* Q, int64_t ldq, vo
                void* stream);
 
 /* SBR-Back: Qs (n x n, ldq) = prod_x (I - Y_x T_x Y_x^T) (backtrans.py:128-192). */
+/* pevd_stedc restricted to the eigenvector columns [col_lo, col_hi) (all eigenvalues; the other
+ * columns of Q are left zero): the top-level merge GEMM only forms the wanted columns, as the
+ * distributed conventional order needs for a rank's column block. */
+int pevd_stedc_cols(int64_t n, double* d, const double* e, double* Q, int64_t ldq, int64_t col_lo,
+                    int64_t col_hi, void* workspace, void* stream);
 int64_t pevd_sbr_back_workspace_bytes(int64_t n, int b);
 int pevd_sbr_back_form(int64_t n, int b, const double* Ystair, const double* Tall, double* Qs,
                        int64_t ldq, void* workspace, void* stream);

@@ -428,6 +428,19 @@ int pevd_stedc(int64_t n, double* d, const double* e, double* Q, int64_t ldq, vo
   return OK;
 }
 
+int pevd_stedc_cols(int64_t n, double* d, const double* e, double* Q, int64_t ldq, int64_t col_lo,
+                    int64_t col_hi, void* workspace, void* stream) {
+  int info = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  PEVD_TRY(stedc(st, n, d, e, Q, ldq, workspace, &info, col_lo, col_hi));
+  PEVD_CUDA(cudaStreamSynchronize(st));
+  if (info != 0) {
+    set_error("tridiagonal divide and conquer did not converge (info=%d)", info);
+    return ERR_CONVERGE;
+  }
+  return OK;
+}
+
 int64_t pevd_sbr_back_workspace_bytes(int64_t n, int b) { return sbr_back_ws_bytes(n, b); }
 
 int pevd_sbr_back_form(int64_t n, int b, const double* Ystair, const double* Tall, double* Qs,

@@ -47,8 +47,10 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
 int64_t stedc_ws_bytes(int64_t n);
 // d (n) in: diagonal, out: eigenvalues ascending; e (n-1) off-diagonal (preserved).
 // Q (n x n, ldq) out: eigenvectors.  Sign convention of tridiag.py:325-333 applied.
+// (col_lo, col_hi): compute only the columns [col_lo, col_hi) of Q (the rest stays zero); the
+// eigenvalues are always complete.
 int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int64_t ldq,
-          void* ws, int* info_host);
+          void* ws, int* info_host, int64_t col_lo = 0, int64_t col_hi = -1);
 
 // Eigenvalues only (no Q): bisection on Sturm counts, one thread per eigenvalue; lam ascending.
 int64_t stebz_ws_bytes(int64_t n);

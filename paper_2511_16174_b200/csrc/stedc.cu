@@ -584,24 +584,37 @@ __global__ void merge_vectors(MergeBufs B) {
   }
 }
 
+// (clo, chi): only the output columns [clo, chi) are wanted (the columns of a rank in the
+// distributed conventional order).  cmap is increasing (roots ascending, deflated values merged
+// in), so the U columns landing there are one contiguous range [ja, jb).
 __global__ void merge_gemm_args(MergeBufs B, const double* X, int64_t ldx, double* Y, int64_t ldy,
-                                int nm) {
+                                int nm, int64_t clo, int64_t chi) {
   const int mi = blockIdx.x * blockDim.x + threadIdx.x;
   if (mi >= nm) return;
   const int lo = B.lo[mi], mid = B.mid[mi], hi = B.hi[mi];
   const int* mint = B.mint + mi * M_NINT;
   const int K = mint[M_K], k1 = mint[M_K1], k2 = mint[M_K2], k3 = mint[M_K3];
   double* U = B.U + B.uoff[mi];
+  const int* cm = B.cmap + lo;
+  auto lower = [&](int64_t v) {  // first j with cmap[j] >= v - lo
+    int a = 0, b2 = K;
+    while (a < b2) {
+      const int c = (a + b2) >> 1;
+      if (cm[c] < v - lo) a = c + 1; else b2 = c;
+    }
+    return a;
+  };
+  const int ja = lower(clo), jb = lower(chi);
   GemmArgs t{};
-  t.m = mid - lo; t.n = K; t.k = k1 + k2; t.alpha = 1.0; t.beta = 0.0;
+  t.m = mid - lo; t.n = jb - ja; t.k = k1 + k2; t.alpha = 1.0; t.beta = 0.0;
   t.A = X + lo + (int64_t)lo * ldx; t.lda = ldx; t.amap = B.amapT + lo;
-  t.B = U; t.ldb = K;
-  t.C = Y + lo + (int64_t)lo * ldy; t.ldc = ldy; t.cmap = B.cmap + lo;
+  t.B = U + (int64_t)ja * K; t.ldb = K;
+  t.C = Y + lo + (int64_t)lo * ldy; t.ldc = ldy; t.cmap = cm + ja;
   t.transA = 0; t.transB = 0; t.amode = A_GENERAL; t.cmode = C_ALL;
   GemmArgs bt = t;
   bt.m = hi - mid; bt.k = k2 + k3;
   bt.A = X + mid + (int64_t)lo * ldx; bt.amap = B.amapB + lo;
-  bt.B = U + k1;
+  bt.B = U + k1 + (int64_t)ja * K;
   bt.C = Y + mid + (int64_t)lo * ldy;
   if (K == 0) { t.m = 0; bt.m = 0; }
   B.gargs[2 * mi] = t;
@@ -610,7 +623,7 @@ __global__ void merge_gemm_args(MergeBufs B, const double* X, int64_t ldx, doubl
 
 // deflated eigenpairs: copy the (rotated) column of X into its sorted output position
 __global__ void merge_deflated_copy(MergeBufs B, const double* X, int64_t ldx, double* Y,
-                                    int64_t ldy) {
+                                    int64_t ldy, int64_t clo, int64_t chi) {
   const int mi = blockIdx.y;
   const int lo = B.lo[mi], hi = B.hi[mi];
   const int K = B.mint[mi * M_NINT + M_K];
@@ -621,10 +634,11 @@ __global__ void merge_deflated_copy(MergeBufs B, const double* X, int64_t ldx, d
   int a = 0, b = K;  // roots <= v
   while (a < b) { const int c = (a + b) >> 1; if (B.lam[lo + c] <= v) a = c + 1; else b = c; }
   const int pos = q + a;
+  if (threadIdx.x == 0) B.Dnext[lo + pos] = v;
+  if (lo + pos < clo || lo + pos >= chi) return;  // column not wanted (eigenvalue kept above)
   const int64_t src = lo + B.dcols[lo + q];
   for (int r = lo + threadIdx.x; r < hi; r += blockDim.x)
     Y[r + (int64_t)(lo + pos) * ldy] = X[r + src * ldx];
-  if (threadIdx.x == 0) B.Dnext[lo + pos] = v;
 }
 
 __global__ void finalize_kernel(int64_t n, const double* dw, double* d, const double* scal) {
@@ -634,8 +648,8 @@ __global__ void finalize_kernel(int64_t n, const double* dw, double* d, const do
 }
 
 // sign convention: largest |q_ij| in each column positive, earliest index on ties
-__global__ void sign_fix(int64_t n, double* Q, int64_t ldq) {
-  const int64_t j = blockIdx.x;
+__global__ void sign_fix(int64_t n, double* Q, int64_t ldq, int64_t j0) {
+  const int64_t j = j0 + blockIdx.x;
   __shared__ double bv[256];
   __shared__ int64_t bi[256];
   double best = -1.0;
@@ -751,7 +765,10 @@ int64_t stedc_ws_bytes(int64_t n) {
 }
 
 int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int64_t ldq,
-          void* ws, int* info_host) {
+          void* ws, int* info_host, int64_t col_lo, int64_t col_hi) {
+  if (col_hi < 0 || col_hi > n) col_hi = n;
+  if (col_lo < 0) col_lo = 0;
+  if (col_lo > col_hi) col_lo = col_hi;
   if (info_host) *info_host = 0;
   if (n < 1) return OK;
   if (n > (int64_t)1 << 30) {
@@ -884,11 +901,12 @@ int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int
     PEVD_LAUNCH_CHECK();
     merge_vectors<<<dim3((unsigned)cdiv(smax, 8), nm), 256, 0, st>>>(B);
     PEVD_LAUNCH_CHECK();
-    merge_gemm_args<<<(unsigned)cdiv(nm, 128), 128, 0, st>>>(B, X, ldx, Y, ldy, nm);
+    // only the last level writes Q: it alone is restricted to the wanted columns
+    const int64_t clo = (l == nlev - 1) ? col_lo : 0, chi = (l == nlev - 1) ? col_hi : n;
+    merge_gemm_args<<<(unsigned)cdiv(nm, 128), 128, 0, st>>>(B, X, ldx, Y, ldy, nm, clo, chi);
     PEVD_LAUNCH_CHECK();
     PEVD_TRY(gemm_grouped(st, B.gargs, 2 * nm, hmax, smax));
-    merge_deflated_copy<<<dim3((unsigned)smax, nm), 256, 0, st>>>(B, X, ldx, Y,
-                                                                                  ldy);
+    merge_deflated_copy<<<dim3((unsigned)smax, nm), 256, 0, st>>>(B, X, ldx, Y, ldy, clo, chi);
     PEVD_LAUNCH_CHECK();
     std::swap(dw, dn);
     cur ^= 1;
@@ -896,7 +914,9 @@ int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int
   // cur now indexes Q
   finalize_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 4096), 256, 0, st>>>(n, dw, d, scal);
   PEVD_LAUNCH_CHECK();
-  sign_fix<<<(unsigned)n, 256, 0, st>>>(n, Q, ldq);
+  if (col_hi > col_lo) {
+    sign_fix<<<(unsigned)(col_hi - col_lo), 256, 0, st>>>(n, Q, ldq, col_lo);
+  }
   PEVD_LAUNCH_CHECK();
   if (info_host) {
     PEVD_CUDA(cudaMemcpyAsync(info_host, d_info, 4, cudaMemcpyDeviceToHost, st));

@@ -109,14 +109,20 @@ class CudaOps:
         self._lib.check(rc, "bc")
         return d, e[: n - 1], tau, (V, vld)
 
-    def stedc(self, d, e):
-        """Device divide and conquer on (d, e) device tensors -> (lam host, Q_d device)."""
+    def stedc(self, d, e, cols=None):
+        """Device divide and conquer on (d, e) device tensors -> (lam host, Q_d device); with
+        cols = (c0, c1) only those eigenvector columns are formed (the rest stays zero)."""
         n = d.shape[0]
         dd = d.clone()
         ee = e.clone() if n > 1 else torch.zeros(1, dtype=torch.float64, device=self.device)
         Q = torch.empty((n, n), dtype=torch.float64, device=self.device)
         ws = torch.empty(self.L.pevd_stedc_workspace_bytes(n), dtype=torch.uint8, device=self.device)
-        rc = self.L.pevd_stedc(n, self._p(dd), self._p(ee), self._p(Q), n, self._p(ws), self._stream())
+        if cols is None:
+            rc = self.L.pevd_stedc(n, self._p(dd), self._p(ee), self._p(Q), n, self._p(ws),
+                                   self._stream())
+        else:
+            rc = self.L.pevd_stedc_cols(n, self._p(dd), self._p(ee), self._p(Q), n, int(cols[0]),
+                                        int(cols[1]), self._p(ws), self._stream())
         if rc == self._lib.PEVD_ERR_CONVERGE:
             raise RuntimeError(self.L.pevd_last_error().decode())
         self._lib.check(rc, "stedc")
@@ -430,7 +436,11 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
         ledger.record(w, w + 1, "BC", 2 * b * b)  # the overlap-block hand-off of the relay
     # ---- solver ----
     t_s = now()
-    lam, Qd = ops.stedc(d, e)      # lam on the host, Q_d column-major (device for CudaOps)
+    # (conventional order: each rank forms only its own columns of Q_d)
+    if cfg.order == "conventional" and cfg.want_vectors:
+        lam, Qd = ops.stedc(d, e, cols=(c0w, c1w))
+    else:
+        lam, Qd = ops.stedc(d, e)  # lam on the host, Q_d column-major (device for CudaOps)
     trace.add(HOST, "Solver", 0, t_s, now())
     if not cfg.want_vectors:
         return EigenResult(lam=lam), trace.events(), ledger, {}

@@ -43,8 +43,12 @@ class CpuOps:
         d, e, refl = orc.bc_reduce(b)
         return d, e, refl, None
 
-    def stedc(self, d, e):
+    def stedc(self, d, e, cols=None):
         lam, q = orc.tridiag_eig(np.asarray(d), np.asarray(e), want_vectors=True)
+        if cols is not None:  # mimic the device: only the requested columns are formed
+            q2 = np.zeros_like(q)
+            q2[:, cols[0]:cols[1]] = q[:, cols[0]:cols[1]]
+            q = q2
         return lam, self.from_host(q)
 
     def bc_back_left(self, n, b, refl, _, X):

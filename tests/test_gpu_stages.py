@@ -151,3 +151,36 @@ def test_sbr_back_form_matches_oracle(n, b):
     np.testing.assert_allclose(qs, qs_o, atol=1e-12 * np.sqrt(n))
     band_dense = orc.band_to_dense(bands)
     np.testing.assert_allclose(qs.T @ a @ qs, band_dense, atol=1e-12 * np.linalg.norm(a))
+
+
+@pytest.mark.parametrize("n,c0,c1", [(2000, 600, 1400), (4096, 0, 1000), (4096, 3000, 4096),
+                                     (700, 350, 351)])
+def test_stedc_column_range_matches_full(n, c0, c1):
+    """pevd_stedc_cols forms exactly the wanted eigenvector columns of the full D&C (the top
+    merge GEMM restricted to them), bit for bit; all eigenvalues; the rest of Q stays zero."""
+    import ctypes
+    import torch
+    from paper_2511_16174_b200 import _lib
+    L = _lib.load()
+    rng = np.random.default_rng(n + c0)
+    d0 = rng.standard_normal(n)
+    e0 = rng.standard_normal(n - 1)
+    P = ctypes.c_void_p
+    s = P(torch.cuda.current_stream().cuda_stream)
+    out = []
+    for cols in (None, (c0, c1)):
+        d = torch.from_numpy(d0.copy()).cuda()
+        e = torch.from_numpy(np.append(e0, 0.0)).cuda()
+        Q = torch.full((n, n), 7.0, dtype=torch.float64, device="cuda")
+        ws = torch.empty(L.pevd_stedc_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+        if cols is None:
+            rc = L.pevd_stedc(n, P(d.data_ptr()), P(e.data_ptr()), P(Q.data_ptr()), n,
+                              P(ws.data_ptr()), s)
+        else:
+            rc = L.pevd_stedc_cols(n, P(d.data_ptr()), P(e.data_ptr()), P(Q.data_ptr()), n,
+                                   cols[0], cols[1], P(ws.data_ptr()), s)
+        _lib.check(rc, "stedc")
+        out.append((d.cpu().numpy(), Q.cpu().numpy().T))
+    (lam_f, q_f), (lam_c, q_c) = out
+    np.testing.assert_array_equal(lam_c, lam_f)
+    np.testing.assert_array_equal(q_c[:, c0:c1], q_f[:, c0:c1])
