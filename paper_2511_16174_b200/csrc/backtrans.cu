@@ -938,36 +938,6 @@ int transpose(cudaStream_t st, int64_t rows, int64_t cols, const double* in, int
   return OK;
 }
 
-int sbr_back_apply_right_t(cudaStream_t st, int64_t n, int b, const double* Yfull,
-                           const double* Tall, double* Xt, int64_t ldx, int64_t nrows, void* ws,
-                           bool prepared) {
-  // Xt <- Xt Q_s^T (= (Q_s X)^T for Xt = X^T): Xt[:, t0:] -= (Xt[:, t0:] Y) T^T Y^T per
-  // aggregated block, from the last block backwards, row chunks of at most n rows
-  if (b < 1 || n <= b) return OK;
-  if (!prepared) PEVD_TRY(sbr_back_prepare(st, n, b, Yfull, Tall, ws));
-  const int NB = nb_agg();
-  SbrBackWs W = sbr_back_carve(n, b, ws, NB);
-  const int64_t R = sbr_num_rounds(n, b);
-  for (int64_t g = W.ngroups - 1; g >= 0; --g) {
-    int64_t t0, c0, K;
-    group_dims(n, b, NB, R, g, &t0, &c0, &K);
-    const int64_t m = n - t0;
-    const double* Y = Yfull + t0 + c0 * n;
-    const double* Tg = W.Tagg + g * W.K * W.K;
-    for (int64_t r = 0; r < nrows; r += n) {
-      const int64_t nr = std::min<int64_t>(n, nrows - r);
-      double* X2 = Xt + r + t0 * ldx;
-      GemmArgs g1{nr, K, m, 1.0, 0.0, X2, ldx, Y, n, W.tmp1, nr, 0, 0, A_GENERAL, C_ALL};
-      PEVD_TRY(gemm(st, g1, W.sk, W.skn));                  // tmp1 = Xt2 Y
-      GemmArgs g2{nr, K, K, 1.0, 0.0, W.tmp1, nr, Tg, W.K, W.tmp2, nr, 0, 1, A_GENERAL, C_ALL};
-      PEVD_TRY(gemm(st, g2, W.sk, W.skn));                  // tmp2 = tmp1 T^T
-      GemmArgs g3{nr, m, K, -1.0, 1.0, W.tmp2, nr, Y, n, X2, ldx, 0, 1, A_GENERAL, C_ALL};
-      PEVD_TRY(gemm(st, g3, W.sk, W.skn));                  // Xt2 -= tmp2 Y^T
-    }
-  }
-  return OK;
-}
-
 int64_t bc_back_ws_bytes(int64_t n, int64_t nrows) {
   // counters + T-factor offsets + the -T factors of every block of 8 sweeps (64 doubles each)
   const int64_t jcount = n >= 3 ? (n - 3) / 32 + 1 : 1;

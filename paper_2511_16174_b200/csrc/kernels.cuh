@@ -74,15 +74,12 @@ int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, 
 int64_t bc_back_ws_bytes(int64_t n, int64_t nrows);
 int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                   double* X, int64_t ldx, int64_t nrows, void* ws);
-// Transposed conventional back transformation, on Xt = X^T (nrows x n, column-major), where the
-// bulge kernel's fast memory pattern applies: Xt <- Xt Q_b^T, then Xt <- Xt Q_s^T.
+// Conventional BC-Back on Xt = X^T (nrows x n, column-major), where the bulge kernel's fast
+// memory pattern applies: Xt <- Xt Q_b^T.
 // (Xt == nullptr: only the preparation (counters, Z of every block), which depends on the chase
 //  output alone; prepared = true skips it in the later call on the same ws.)
 int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                    double* Xt, int64_t ldx, int64_t nrows, void* ws, bool prepared = false);
-int sbr_back_apply_right_t(cudaStream_t st, int64_t n, int b, const double* Yfull,
-                           const double* Tall, double* Xt, int64_t ldx, int64_t nrows, void* ws,
-                           bool prepared = false);
 // out (cols x rows) = in^T (in: rows x cols)
 int transpose(cudaStream_t st, int64_t rows, int64_t cols, const double* in, int64_t ldi,
               double* out, int64_t ldo);
