@@ -42,6 +42,9 @@ def _evd(A, n, b, order):
     ("Cluster0", 16384, "conventional"),    # c5 family: one eigenvalue + a 16383-fold cluster
     ("Cluster1", 16384, "pipelined"),
     ("Uniform", 16384, "conventional"),
+    ("Normal", 20001, "conventional"),      # ragged sizes: partial row blocks, groups, tiles
+    ("Normal", 12345, "pipelined"),
+    ("Normal", 9999, "sequential"),
 ])
 def test_planted_spectrum(kind, n, order):
     import torch
