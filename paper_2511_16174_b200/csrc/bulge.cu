@@ -191,11 +191,19 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
         }
         __syncwarp();
         // ---- write back
-        for (int q = 0; q < nleft; ++q)
-          if (lane < L) Bd[(cg + q) * LDB + (w0 - cg - q) + lane] = S.SL[lane * LDS_ + q];
-        for (int c = 0; c < L; ++c) {
-          if (lane >= c && lane < L) Bd[(w0 + c) * LDB + (lane - c)] = S.SW[lane * LDS_ + c];
-          if (lane < nT) Bd[(w0 + c) * LDB + (L + lane - c)] = S.SC[lane * LDS_ + c];
+        {
+          // one pointer per region, advanced by LDB - 1 per column: no 64-bit multiplies in
+          // the store loops
+          const int64_t stp = LDB - 1;
+          double* pl = Bd + cg * LDB + (w0 - cg) + lane;
+          for (int q = 0; q < nleft; ++q, pl += stp)
+            if (lane < L) *pl = S.SL[lane * LDS_ + q];
+          double* pw = Bd + w0 * LDB + lane;
+          double* pc = pw + L;
+          for (int c = 0; c < L; ++c, pw += stp, pc += stp) {
+            if (lane >= c && lane < L) *pw = S.SW[lane * LDS_ + c];
+            if (lane < nT) *pc = S.SC[lane * LDS_ + c];
+          }
         }
         if (tau_out) {
           if (lane == 0) tau_out[slot] = tau;
