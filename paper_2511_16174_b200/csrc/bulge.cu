@@ -101,11 +101,22 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
 
       // ---- stage the whole region with independent loads (one L2 round trip, not 3b)
       double rl[BMAX], rw[BMAX], rc[BMAX];
+      {
+        // element q of this lane's row in each region: one pointer per region advanced by
+        // LDB - 1 per column (no 64-bit multiply per element)
+        const int64_t stp = LDB - 1;
+        const double* pl = Bd + cg * LDB + (w0 - cg) + lane;
+        const double* pw = Bd + w0 * LDB + lane;
+        const double* pc = pw + L;
 #pragma unroll
-      for (int q = 0; q < BMAX; ++q) {
-        rl[q] = (q < nleft && lane < L) ? __ldcg(Bd + (cg + q) * LDB + (w0 - cg - q) + lane) : 0.0;
-        rw[q] = (q < L && lane >= q && lane < L) ? __ldcg(Bd + (w0 + q) * LDB + (lane - q)) : 0.0;
-        rc[q] = (q < L && lane < nT) ? __ldcg(Bd + (w0 + q) * LDB + (L + lane - q)) : 0.0;
+        for (int q = 0; q < BMAX; ++q) {
+          rl[q] = (q < nleft && lane < L) ? __ldcg(pl) : 0.0;
+          rw[q] = (q < L && lane >= q && lane < L) ? __ldcg(pw) : 0.0;
+          rc[q] = (q < L && lane < nT) ? __ldcg(pc) : 0.0;
+          pl += stp;
+          pw += stp;
+          pc += stp;
+        }
       }
 #pragma unroll
       for (int q = 0; q < BMAX; ++q) {
