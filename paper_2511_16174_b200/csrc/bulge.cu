@@ -207,10 +207,12 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
           // the store loops
           const int64_t stp = LDB - 1;
           double* pl = Bd + cg * LDB + (w0 - cg) + lane;
+#pragma unroll 4
           for (int q = 0; q < nleft; ++q, pl += stp)
             if (lane < L) *pl = S.SL[lane * LDS_ + q];
           double* pw = Bd + w0 * LDB + lane;
           double* pc = pw + L;
+#pragma unroll 4
           for (int c = 0; c < L; ++c, pw += stp, pc += stp) {
             if (lane >= c && lane < L) *pw = S.SW[lane * LDS_ + c];
             if (lane < nT) *pc = S.SC[lane * LDS_ + c];
