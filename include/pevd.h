@@ -129,11 +129,12 @@ int pevd_stedc(int64_t n, double* d, const double* e, double* Q, int64_t ldq, vo
 int pevd_stedc_cols(int64_t n, double* d, const double* e, double* Q, int64_t ldq, int64_t col_lo,
                     int64_t col_hi, void* workspace, void* stream);
 int64_t pevd_sbr_back_workspace_bytes(int64_t n, int b);
-int pevd_sbr_back_form(int64_t n, int b, const double* Ystair, const double* Tall, double* Qs,
-                       int64_t ldq, void* workspace, void* stream);
+/* Ystair: the Y staircase pevd_sbr / pevd_syevd_device leave in A (leading dimension ldy = lda). */
+int pevd_sbr_back_form(int64_t n, int b, const double* Ystair, int64_t ldy, const double* Tall,
+                       double* Qs, int64_t ldq, void* workspace, void* stream);
 /* X (n x ncols, ldx) <- Q_s X (conventional order, pipeline.py:380-384). */
-int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, const double* Tall, double* X,
-                       int64_t ldx, int64_t ncols, void* workspace, void* stream);
+int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, int64_t ldy, const double* Tall,
+                       double* X, int64_t ldx, int64_t ncols, void* workspace, void* stream);
 
 /* BC-Back backtrans.py:277-310.  right: X (nrows x n, ldx) <- X Q_b ("reordered", i.e. the
  * transpose of Q_b^T X^T).  left: X (n x ncols, ldx) <- Q_b X ("conventional"; for b = 32 it runs

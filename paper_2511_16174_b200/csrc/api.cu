@@ -187,6 +187,10 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
   }
   PEVD_CUDA(cudaEventCreateWithFlags(&prep_done, cudaEventDisableTiming));
   auto cleanup = [&]() {
+    // the call is synchronous even on an error path: nothing may still write the caller's
+    // workspace or Q once we return (errors of these waits are the error being reported)
+    if (sb) cudaStreamSynchronize(sb);
+    cudaStreamSynchronize(sm);
     if (prep_done) cudaEventDestroy(prep_done);
     for (auto& e : ev) {
       if (e.a) cudaEventDestroy(e.a);
@@ -214,7 +218,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     if (want_vectors && order != PEVD_ORDER_CONVENTIONAL) {
       if (two_streams) cudaStreamWaitEvent(sback, ev[0].b, 0);
       cudaEventRecord(ev[3].a, sback);
-      if ((rc = sbr_back_form(sback, n, b, A, L.Tall, L.Qs, n, L.ws_back))) break;
+      if ((rc = sbr_back_form(sback, n, b, A, lda, L.Tall, L.Qs, n, L.ws_back))) break;
       cudaEventRecord(ev[3].b, sback);
     }
     // ---- BC-Back on Q_s (back stream) overlapping the divide and conquer
@@ -231,7 +235,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
                         b == 32 && L.vld == 32;
     if (want_vectors && order == PEVD_ORDER_CONVENTIONAL) {
       cudaStreamWaitEvent(sb, ev[1].b, 0);
-      if ((rc = sbr_back_prepare(sb, n, b, A, L.Tall, L.ws_back))) break;
+      if ((rc = sbr_back_prepare(sb, n, b, A, lda, L.Tall, L.ws_back))) break;
       if (conv_t &&
           (rc = bc_back_left_t(sb, n, b, L.tau, L.V, L.vld, nullptr, n, n, L.ws_bcb, false)))
         break;
@@ -266,14 +270,14 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
         if ((rc = transpose(sm, n, n, Xt, n, Q, ldq))) break;
         cudaEventRecord(ev[5].b, sm);
         cudaEventRecord(ev[3].a, sm);
-        if ((rc = sbr_back_apply_left(sm, n, b, A, L.Tall, Q, ldq, n, L.ws_back, true))) break;
+        if ((rc = sbr_back_apply_left(sm, n, b, A, lda, L.Tall, Q, ldq, n, L.ws_back, true))) break;
         cudaEventRecord(ev[3].b, sm);
       } else if (order == PEVD_ORDER_CONVENTIONAL) {
         cudaEventRecord(ev[4].a, sm);
         if ((rc = bc_back_left(sm, n, b, L.tau, L.V, L.vld, L.Qd, n, n, L.ws_bcb))) break;
         cudaEventRecord(ev[4].b, sm);
         cudaEventRecord(ev[3].a, sm);
-        if ((rc = sbr_back_apply_left(sm, n, b, A, L.Tall, L.Qd, n, n, L.ws_back, true))) break;
+        if ((rc = sbr_back_apply_left(sm, n, b, A, lda, L.Tall, L.Qd, n, n, L.ws_back, true))) break;
         cudaEventRecord(ev[3].b, sm);
         cudaEventRecord(ev[5].a, sm);
         if (cudaMemcpy2DAsync(Q, ldq * 8, L.Qd, n * 8, n * 8, n, cudaMemcpyDeviceToDevice, sm) !=
@@ -443,14 +447,23 @@ int pevd_stedc_cols(int64_t n, double* d, const double* e, double* Q, int64_t ld
 
 int64_t pevd_sbr_back_workspace_bytes(int64_t n, int b) { return sbr_back_ws_bytes(n, b); }
 
-int pevd_sbr_back_form(int64_t n, int b, const double* Ystair, const double* Tall, double* Qs,
-                       int64_t ldq, void* workspace, void* stream) {
-  return sbr_back_form((cudaStream_t)stream, n, b, Ystair, Tall, Qs, ldq, workspace);
+int pevd_sbr_back_form(int64_t n, int b, const double* Ystair, int64_t ldy, const double* Tall,
+                       double* Qs, int64_t ldq, void* workspace, void* stream) {
+  if (ldy < n) {
+    set_error("pevd_sbr_back_form: ldy=%lld < n=%lld", (long long)ldy, (long long)n);
+    return ERR_VALUE;
+  }
+  return sbr_back_form((cudaStream_t)stream, n, b, Ystair, ldy, Tall, Qs, ldq, workspace);
 }
 
-int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, const double* Tall, double* X,
-                       int64_t ldx, int64_t ncols, void* workspace, void* stream) {
-  return sbr_back_apply_left((cudaStream_t)stream, n, b, Ystair, Tall, X, ldx, ncols, workspace);
+int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, int64_t ldy, const double* Tall,
+                       double* X, int64_t ldx, int64_t ncols, void* workspace, void* stream) {
+  if (ldy < n) {
+    set_error("pevd_sbr_back_left: ldy=%lld < n=%lld", (long long)ldy, (long long)n);
+    return ERR_VALUE;
+  }
+  return sbr_back_apply_left((cudaStream_t)stream, n, b, Ystair, ldy, Tall, X, ldx, ncols,
+                             workspace);
 }
 
 static int64_t ws_round(int64_t x) { return (x + 255) / 256 * 256; }

@@ -59,16 +59,17 @@ int stebz(cudaStream_t st, int64_t n, const double* d, const double* e, double* 
 // ---------------- back transformation (backtrans.cu)
 // Q_s = prod_x (I - Y_x T_x Y_x^T) formed explicitly into Qs (n x n, ldq).
 int64_t sbr_back_ws_bytes(int64_t n, int b);
-// (Yfull = the Y staircase left by sbr_reduce, leading dimension n.)
+// (Yfull = the Y staircase left by sbr_reduce in A, leading dimension ldy = lda.)
 // Aggregated T factors of every SBR-Back block (depends only on the SBR output); the
 // form/apply calls run it themselves unless `prepared` says it already ran on ws.
-int sbr_back_prepare(cudaStream_t st, int64_t n, int b, const double* Yfull, const double* Tall,
-                     void* ws);
-int sbr_back_form(cudaStream_t st, int64_t n, int b, const double* Yfull, const double* Tall,
-                  double* Qs, int64_t ldq, void* ws, bool prepared = false);
+int sbr_back_prepare(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_t ldy,
+                     const double* Tall, void* ws);
+int sbr_back_form(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_t ldy,
+                  const double* Tall, double* Qs, int64_t ldq, void* ws, bool prepared = false);
 // Apply the SBR reflectors from the left to X (n x ncols): X <- Q_s X (conventional order).
-int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, const double* Tall,
-                        double* X, int64_t ldx, int64_t ncols, void* ws, bool prepared = false);
+int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_t ldy,
+                        const double* Tall, double* X, int64_t ldx, int64_t ncols, void* ws,
+                        bool prepared = false);
 // Right-apply the bulge reflectors to the rows of X (nrows x n, col-major ldx):
 // X <- X Q_b  (== (Q_b^T X^T)^T, the reordered BC-Back, backtrans.py:277-310).
 int64_t bc_back_ws_bytes(int64_t n, int64_t nrows);

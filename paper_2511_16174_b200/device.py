@@ -211,7 +211,7 @@ def sbr_back_form(n, b, ystair, tall):
     dt = torch.from_numpy(np.ascontiguousarray(tall, dtype=np.float64).reshape(-1)).cuda()
     q = empty(n, n)
     ws = workspace(L.pevd_sbr_back_workspace_bytes(n, b))
-    rc = L.pevd_sbr_back_form(n, b, _p(dy), _p(dt), _p(q), n, _p(ws), _stream())
+    rc = L.pevd_sbr_back_form(n, b, _p(dy), n, _p(dt), _p(q), n, _p(ws), _stream())
     _lib.check(rc, "sbr_back_form")
     return from_dev(q)
 

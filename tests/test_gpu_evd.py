@@ -61,3 +61,31 @@ def test_syevd_large_residual(n):
     assert orc.orthogonality(q) <= 1e-15
     lam_np = np.linalg.eigvalsh(a)
     np.testing.assert_allclose(lam, lam_np, atol=10 * n * EPS * np.abs(lam_np).max())
+
+
+@pytest.mark.parametrize("order", ["pipelined", "sequential", "conventional"])
+def test_padded_leading_dimensions(order):
+    """lda = n + 7 and ldq = n + 3: the Y staircase SBR leaves in A is read back with lda by
+    every SBR-Back path, and Q is written with its own stride (padding untouched)."""
+    import ctypes
+    import torch
+    from paper_2511_16174_b200 import _lib
+    L = _lib.load()
+    n, b, lda, ldq = 300, 32, 307, 303
+    a = sym(n, 77)
+    oc = _lib.ORDER_CODES[order]
+    A = torch.full((n, lda), 1e300, dtype=torch.float64, device="cuda")  # column-major, padded
+    A[:, :n] = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
+    Q = torch.full((n, ldq), -7.0, dtype=torch.float64, device="cuda")
+    lam = torch.empty(n, dtype=torch.float64, device="cuda")
+    ws = torch.empty(L.pevd_syevd_workspace_bytes(n, b, 1, oc), dtype=torch.uint8, device="cuda")
+    P = ctypes.c_void_p
+    rc = L.pevd_syevd_device(n, b, P(A.data_ptr()), lda, P(lam.data_ptr()), P(Q.data_ptr()), ldq,
+                             1, oc, P(ws.data_ptr()), ws.numel(),
+                             P(torch.cuda.current_stream().cuda_stream), ctypes.byref(_lib.PevdStats()))
+    _lib.check(rc, "pevd_syevd_device")
+    q = np.asfortranarray(Q[:, :n].cpu().numpy().T)
+    assert np.all(Q[:, n:].cpu().numpy() == -7.0)
+    lam_h = lam.cpu().numpy()
+    assert orc.backward_error(a, q, lam_h) <= 1e-15
+    assert orc.orthogonality(q) <= 1e-15

@@ -139,11 +139,11 @@ def main():
         X = torch.randn((n, n), dtype=torch.float64, device="cuda")
         ws = torch.empty(L.pevd_sbr_back_workspace_bytes(n, b), dtype=torch.uint8, device="cuda")
         if mode == "sbrback":
-            fn = lambda: _lib.check(L.pevd_sbr_back_left(n, b, ptr(A), ptr(tall), ptr(X), n, n,  # noqa
+            fn = lambda: _lib.check(L.pevd_sbr_back_left(n, b, ptr(A), n, ptr(tall), ptr(X), n, n,  # noqa
                                                          ptr(ws), stream()), "sbr_back_left")
             flops = 2.0 * n ** 3
         else:
-            fn = lambda: _lib.check(L.pevd_sbr_back_form(n, b, ptr(A), ptr(tall), ptr(X), n,  # noqa
+            fn = lambda: _lib.check(L.pevd_sbr_back_form(n, b, ptr(A), n, ptr(tall), ptr(X), n,  # noqa
                                                          ptr(ws), stream()), "sbr_back_form")
             flops = 4.0 * n ** 3 / 3
         ms, ts = timed(fn, reps=2)
