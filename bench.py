@@ -10,8 +10,8 @@ device-resident path (pevd_syevd_device, input already in HBM; A is 19.3 GB, far
 (N > 1) every rank solves its own EVD (replicas; the blockwise multi-GPU EVD is not wired into
 the bench yet) and value = N * 4 n^3 / max-over-ranks time.
 
---impl reference times the CPU oracle (oracle/: C + numpy restatement of the reference package,
-pinned bit-exact to it) on a bounded sample (n=1024 per step) with all host threads.
+--impl reference times the reference package itself (pipeevd.run, installed unmodified into
+baseline/_ref, tools/ref_cpu.py) on a bounded sample (n=1024 per step) on the host's cores.
 """
 from __future__ import annotations
 
@@ -329,37 +329,72 @@ def load_fp64_peaks():
 
 
 def cpu_baseline(n_cpu: int):
-    """Oracle (C + numpy restatement of the reference) on the host: one EVD at n_cpu."""
+    """The reference package itself (pipeevd.run from baseline/_ref, its own public API, 1 worker
+    thread -- the fastest setting at this size -- plus OpenBLAS on all host threads) on this host:
+    one EVD with vectors at n_cpu.  Falls back to the oracle port only when the install is
+    missing, and says so in `kind`."""
     import numpy as np
-    from oracle import oracle as orc
-    g = np.random.default_rng(n_cpu).standard_normal((n_cpu, n_cpu))
-    a = (g + g.T) / 2
-    orc.evd(a[:64, :64], 32, True)  # warm the library
-    t0 = time.perf_counter()
-    orc.evd(a, 32, True)
-    dt = time.perf_counter() - t0
-    return {"value": round(4 * n_cpu ** 3 / dt / 1e12, 6), "unit": "TFLOP/s",
-            "cores": os.cpu_count(), "kind": "port",
-            "sample": f"one n={n_cpu} EVD with vectors (oracle/: numpy BLAS on all host threads "
-                      f"+ single-threaded C QL/QR, chase and BC-Back), {dt:.2f} s"}
+    try:
+        from tools.ref_cpu import goe, load_reference, time_run, warm
+        pipeevd = load_reference()
+        warm(pipeevd)
+        a = goe(n_cpu, n_cpu)
+        dt, stages, _ = time_run(pipeevd, a, 1)
+        return {"value": round(4 * n_cpu ** 3 / dt / 1e12, 6), "unit": "TFLOP/s",
+                "cores": os.cpu_count(), "kind": "reference",
+                "sample": f"pipeevd.run (baseline/_ref, unmodified) n={n_cpu} with vectors, "
+                          f"workers=1 (+ OpenBLAS threads), {dt:.2f} s"}
+    except ImportError:
+        from oracle import oracle as orc
+        g = np.random.default_rng(n_cpu).standard_normal((n_cpu, n_cpu))
+        a = (g + g.T) / 2
+        orc.evd(a[:64, :64], 32, True)  # warm the library
+        t0 = time.perf_counter()
+        orc.evd(a, 32, True)
+        dt = time.perf_counter() - t0
+        return {"value": round(4 * n_cpu ** 3 / dt / 1e12, 6), "unit": "TFLOP/s",
+                "cores": os.cpu_count(), "kind": "port",
+                "sample": f"one n={n_cpu} EVD with vectors (oracle/ port: the reference install is "
+                          f"missing), {dt:.2f} s"}
+
+
+def reference_extrapolation():
+    """Committed per-stage n^3 extrapolation of the reference to n = 49152 (tools/ref_cpu.py on
+    a GPU box host), labelled as such; None when absent."""
+    path = os.path.join(ROOT, "profiles", "r02_reference_cpu.json")
+    try:
+        d = json.load(open(path))
+        ex = {w: {"wall_s": round(v["wall_s"], 1), "from_n": v["from_n"],
+                  "tflops": round(4 * 49152 ** 3 / v["wall_s"] / 1e12, 6)}
+              for w, v in d["extrapolated"].items()}
+        return {"source": "profiles/r02_reference_cpu.json (per-stage n^3 fit, extrapolated)",
+                "host": d.get("host"), "by_workers": ex}
+    except Exception:
+        return None
 
 
 def run_reference(args):
+    """--impl reference: the unmodified reference package (pipeevd.run, baseline/_ref) on this
+    host's cores, each step a bounded sample (n = --ref-n) of the workload."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np
-    from oracle import oracle as orc
+    from tools.ref_cpu import goe, host_info, load_reference, time_run, warm
+    try:
+        pipeevd = load_reference()
+    except ImportError as exc:
+        print(json.dumps({"impl": "reference", "unavailable": str(exc)}), flush=True)
+        return
     n = args.ref_n
-    g = np.random.default_rng(n).standard_normal((n, n))
-    a = (g + g.T) / 2
+    workers = args.ref_workers
+    warm(pipeevd, (workers,))
+    a = goe(n, n)
     for _ in range(args.warmup):
-        orc.evd(a, args.b, True)
-    ts = []
+        time_run(pipeevd, a, workers)
+    ts, stages = [], None
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        orc.evd(a, args.b, True)
-        ts.append(time.perf_counter() - t0)
+        dt, stages, _ = time_run(pipeevd, a, workers)
+        ts.append(dt)
     dt = sum(ts) / len(ts)
     v = 4 * n ** 3 / dt / 1e12
     print(json.dumps({
@@ -367,11 +402,17 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"CPU oracle EVD with eigenvectors, bounded sample n={n} "
-                               f"(the n=49152 run would take days on the host)", "n": n,
-                   "b": args.b},
+        "config": {"workload": f"reference pipeevd.run with eigenvectors, bounded sample n={n} "
+                               f"(b={args.b}, workers={workers}, order=pipelined: the reference "
+                               f"default); n=49152 would take days on the host", "n": n,
+                   "b": args.b, "workers": workers},
+        "stage_busy_s": {k: round(x, 3) for k, x in (stages or {}).items()},
+        "host": host_info(),
+        "extrapolated_n49152": reference_extrapolation(),
         "cpu_baseline": {"value": round(v, 6), "unit": "TFLOP/s", "cores": os.cpu_count(),
-                         "kind": "port", "sample": f"n={n} EVD with vectors per step"},
+                         "kind": "reference",
+                         "sample": f"pipeevd.run n={n} with vectors per step, workers={workers} "
+                                   f"(+ OpenBLAS on all host threads)"},
         "e2e": {"value": round(v, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0}}), flush=True)
 
@@ -386,7 +427,8 @@ def main():
     ap.add_argument("--b", type=int, default=32)
     ap.add_argument("--order", default="conventional", choices=["pipelined", "sequential", "conventional"])
     ap.add_argument("--seed", type=int, default=49152)
-    ap.add_argument("--cpu-n", type=int, default=1536)
+    ap.add_argument("--cpu-n", type=int, default=1024)
+    ap.add_argument("--ref-workers", type=int, default=1)
     ap.add_argument("--ref-n", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

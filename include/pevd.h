@@ -46,6 +46,12 @@ typedef struct pevd_stats {
   double total_ms;         /* first start .. last end */
   int64_t n_reflectors;    /* bulge reflector slots (sum_j (n-2-jb)) */
   int64_t n_rounds;        /* SBR panels */
+  /* EXECUTED flops per stage, in the order SBR, BC, SBR-Back, BC-Back, Solver, FinalMultiply
+   * (FlopCounter stages, core.py:26-62): GEMM launches as issued (2 m n k; the lower-tile
+   * rank-2k update counts its tiles), the divide and conquer's deflated merge GEMMs summed on the
+   * device from their descriptors, the BC-Back DMMA kernel as the DMMAs it issues (1.25x the
+   * BLAS2 count), panel QR and the chase analytically (2 m k^2 + 2 m k^2; 14 b^2 per reflector). */
+  double flops[6];
 } pevd_stats;
 
 const char* pevd_last_error(void);

@@ -23,7 +23,11 @@ _vp = ctypes.c_void_p
 class PevdStats(ctypes.Structure):
     _fields_ = [("sbr_ms", _dbl * 2), ("bc_ms", _dbl * 2), ("solver_ms", _dbl * 2),
                 ("sbr_back_ms", _dbl * 2), ("bc_back_ms", _dbl * 2), ("final_ms", _dbl * 2),
-                ("total_ms", _dbl), ("n_reflectors", _i64), ("n_rounds", _i64)]
+                ("total_ms", _dbl), ("n_reflectors", _i64), ("n_rounds", _i64),
+                ("flops", _dbl * 6)]
+
+# order of PevdStats.flops (pevd.h): the FlopCounter stage names
+FLOP_STAGES = ("SBR", "BC", "SBR-Back", "BC-Back", "Solver", "FinalMultiply")
 
 
 # name -> (restype, argtypes); must cover every function declared in include/pevd.h

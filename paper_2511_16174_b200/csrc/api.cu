@@ -30,6 +30,40 @@ const char* last_error() { return g_err; }
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+struct FlopState {
+  int stage = 0;
+  double host[ST_NSTAGE] = {};
+  unsigned long long* dev = nullptr;
+  int dev_id = -1;
+};
+static thread_local FlopState g_flops;
+
+void flops_set_stage(int stage) { g_flops.stage = stage; }
+int flops_stage() { return g_flops.stage; }
+void flops_add(double f) { g_flops.host[g_flops.stage] += f; }
+unsigned long long* flops_dev() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (g_flops.dev && g_flops.dev_id == dev) return g_flops.dev;
+  // one small buffer per (thread, device) for the life of the thread
+  unsigned long long* p = nullptr;
+  if (cudaMalloc(&p, ST_NSTAGE * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+  cudaMemset(p, 0, ST_NSTAGE * sizeof(unsigned long long));
+  g_flops.dev = p;
+  g_flops.dev_id = dev;
+  return p;
+}
+void flops_reset() {
+  for (double& h : g_flops.host) h = 0.0;
+  if (unsigned long long* d = flops_dev()) cudaMemset(d, 0, ST_NSTAGE * sizeof(unsigned long long));
+}
+void flops_read(double out[ST_NSTAGE]) {
+  unsigned long long d[ST_NSTAGE] = {};
+  if (unsigned long long* p = flops_dev())
+    cudaMemcpy(d, p, sizeof(d), cudaMemcpyDeviceToHost);
+  for (int s = 0; s < ST_NSTAGE; ++s) out[s] = g_flops.host[s] + (double)d[s];
+}
+
 int num_sms() {
   static int cache[64];
   static bool init[64];
@@ -200,9 +234,11 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
   };
   int rc = OK;
   int info = 0;
+  flops_reset();
   do {
     cudaStream_t sback = two_streams ? sb : sm;
     // ---- SBR
+    flops_set_stage(ST_SBR);
     if ((rc = (cudaEventRecord(ev[0].a, sm) == cudaSuccess) ? OK : ERR_CUDA)) break;
     if ((rc = sbr_reduce(sm, n, b, A, lda, L.bands, want_vectors ? L.Tall : nullptr, L.ws_sbr)))
       break;
@@ -210,6 +246,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     // ---- BC first: its persistent CTAs must become resident before the SBR-Back GEMMs
     //      (enqueued next, on the back stream) fill the SMs
     cudaEventRecord(ev[1].a, sm);
+    flops_set_stage(ST_BC);
     if ((rc = bc_reduce(sm, n, b, L.bands, L.d, L.e, want_vectors ? L.tau : nullptr,
                         want_vectors ? L.V : nullptr, L.vld, L.ws_bc)))
       break;
@@ -217,6 +254,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     // ---- SBR-Back (forms Q_s) overlapping the chase
     if (want_vectors && order != PEVD_ORDER_CONVENTIONAL) {
       if (two_streams) cudaStreamWaitEvent(sback, ev[0].b, 0);
+      flops_set_stage(ST_SBR_BACK);
       cudaEventRecord(ev[3].a, sback);
       if ((rc = sbr_back_form(sback, n, b, A, lda, L.Tall, L.Qs, n, L.ws_back))) break;
       cudaEventRecord(ev[3].b, sback);
@@ -224,6 +262,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     // ---- BC-Back on Q_s (back stream) overlapping the divide and conquer
     if (want_vectors && order != PEVD_ORDER_CONVENTIONAL) {
       if (two_streams) cudaStreamWaitEvent(sback, ev[1].b, 0);
+      flops_set_stage(ST_BC_BACK);
       cudaEventRecord(ev[4].a, sback);
       if ((rc = bc_back_right(sback, n, b, L.tau, L.V, L.vld, L.Qs, n, n, L.ws_bcb))) break;
       cudaEventRecord(ev[4].b, sback);
@@ -235,13 +274,16 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
                         b == 32 && L.vld == 32;
     if (want_vectors && order == PEVD_ORDER_CONVENTIONAL) {
       cudaStreamWaitEvent(sb, ev[1].b, 0);
+      flops_set_stage(ST_SBR_BACK);
       if ((rc = sbr_back_prepare(sb, n, b, A, lda, L.Tall, L.ws_back))) break;
+      flops_set_stage(ST_BC_BACK);
       if (conv_t &&
           (rc = bc_back_left_t(sb, n, b, L.tau, L.V, L.vld, nullptr, n, n, L.ws_bcb, false)))
         break;
       cudaEventRecord(prep_done, sb);
     }
     // ---- D&C
+    flops_set_stage(ST_SOLVER);
     cudaEventRecord(ev[2].a, sm);
     if (want_vectors || !values_by_bisection()) {
       if ((rc = stedc(sm, n, L.d, L.e, L.Qd, n, L.ws_dc, &info))) break;
@@ -260,6 +302,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
         // column-major order (the BC-Back kernel's coalesced pattern): Xt lives in the D&C's
         // (now free) ping-pong buffer; two n^2 transposes (~7 ms each)
         double* Xt = (double*)L.ws_dc;
+        flops_set_stage(ST_BC_BACK);
         cudaEventRecord(ev[4].a, sm);
         if ((rc = transpose(sm, n, n, L.Qd, n, Xt, n))) break;
         if ((rc = bc_back_left_t(sm, n, b, L.tau, L.V, L.vld, Xt, n, n, L.ws_bcb, true))) break;
@@ -269,13 +312,16 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
         cudaEventRecord(ev[5].a, sm);
         if ((rc = transpose(sm, n, n, Xt, n, Q, ldq))) break;
         cudaEventRecord(ev[5].b, sm);
+        flops_set_stage(ST_SBR_BACK);
         cudaEventRecord(ev[3].a, sm);
         if ((rc = sbr_back_apply_left(sm, n, b, A, lda, L.Tall, Q, ldq, n, L.ws_back, true))) break;
         cudaEventRecord(ev[3].b, sm);
       } else if (order == PEVD_ORDER_CONVENTIONAL) {
+        flops_set_stage(ST_BC_BACK);
         cudaEventRecord(ev[4].a, sm);
         if ((rc = bc_back_left(sm, n, b, L.tau, L.V, L.vld, L.Qd, n, n, L.ws_bcb))) break;
         cudaEventRecord(ev[4].b, sm);
+        flops_set_stage(ST_SBR_BACK);
         cudaEventRecord(ev[3].a, sm);
         if ((rc = sbr_back_apply_left(sm, n, b, A, lda, L.Tall, L.Qd, n, n, L.ws_back, true))) break;
         cudaEventRecord(ev[3].b, sm);
@@ -288,6 +334,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
         cudaEventRecord(ev[5].b, sm);
       } else {
         if (two_streams) cudaStreamWaitEvent(sm, ev[4].b, 0);
+        flops_set_stage(ST_FINAL);
         cudaEventRecord(ev[5].a, sm);
         GemmArgs g{n, n, n, 1.0, 0.0, L.Qs, n, L.Qd, n, Q, ldq, 0, 0, A_GENERAL, C_ALL};
         if ((rc = gemm(sm, g, nullptr, 0))) break;
@@ -326,6 +373,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
       stats->total_ms = tot;
       stats->n_reflectors = bc_num_reflectors(n, b);
       stats->n_rounds = sbr_num_rounds(n, b);
+      flops_read(stats->flops);
     }
   } while (0);
   if (rc == ERR_CUDA && g_err[0] == '\0') set_error("CUDA failure");

@@ -754,6 +754,8 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
       set_error("bc_back: persistent kernel cannot be resident");
       return ERR_CUDA;
     }
+    // executed: 20 DMMA (10240 flops) per 8 rows per block of 8 reflectors
+    flops_add(1280.0 * (double)nrows * (double)nblk);
     const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
     kfn<<<(unsigned)grid, WY_THREADS, smem, st>>>(n, V, vld, Tf, tofs, X, ldx, nrows, counter,
                                                  progress, nunits, nrb);
@@ -761,6 +763,7 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
     return OK;
   }
   // any other b (or a padded reflector stride): one thread per row, reflector by reflector
+  flops_add(4.0 * b * (double)bc_num_reflectors(n, b) * (double)nrows);
   bc_back_right_generic<<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, b, tau, V, vld, X, ldx,
                                                                     nrows, 16);
   PEVD_LAUNCH_CHECK();
@@ -794,6 +797,11 @@ int bc_back_left_impl(cudaStream_t st, int64_t n, int b, const double* tau, cons
       PEVD_LAUNCH_CHECK();
     }
     if (X == nullptr) return OK;  // preparation only
+    {
+      int64_t nblk = 0;
+      for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(n - 2 - j * 32, 8);
+      flops_add(1280.0 * (double)ncols * (double)nblk);  // executed DMMA flops, as above
+    }
     const size_t smem = sizeof(WySmem);
     static int attr_dev = -1;
     int dev;
@@ -816,6 +824,7 @@ int bc_back_left_impl(cudaStream_t st, int64_t n, int b, const double* tau, cons
     PEVD_LAUNCH_CHECK();
     return OK;
   }
+  flops_add(4.0 * b * (double)bc_num_reflectors(n, b) * (double)ncols);
   bc_back_left_generic<<<(unsigned)cdiv(ncols, 128), 128, 0, st>>>(n, b, tau, V, vld, X, ldx,
                                                                    ncols);
   PEVD_LAUNCH_CHECK();

@@ -6,11 +6,15 @@
 // round-robin.  Sweep gi may run step j once sweep gi-1 has COMPLETED step j+2 (progress
 // counter >= j+3): the regions of (gi, j) and of (gi-1, >= j+3) are then column-disjoint, so the
 // wavefront performs exactly the sequential chase's operations (SURVEY.md §7 hard part 1).
-// Sweeps are handed out by an atomic ticket, so a warp only ever waits on a sweep that a warp
-// which started before it holds: the kernel cannot deadlock when other kernels occupy SMs and only
-// part of its grid is resident.  The producer orders its band stores before the progress flag
-// with a gpu-scope fence; the consumer polls the flag relaxed and then issues an acquire fence
-// before touching band data, which it reads through L2 (ld.cg).
+// Warps wait on each other, so the kernel is launched COOPERATIVELY: the runtime makes the whole
+// grid co-resident or refuses the launch, and no CTA can spin on a CTA that never gets an SM
+// (e.g. beside another EVD on another stream).  Sweeps are assigned round-robin (sweep gi to
+// warp gi mod total): consecutive sweeps land on consecutive CTAs, i.e. on different SMs, which
+// spreads the ~n/(3b) in-flight sweeps evenly (an atomic sweep ticket gives a data-dependent
+// mapping that crowds some SMs: 1.54 s instead of 1.07 s at n = 49152).  The producer orders its
+// band stores before the progress flag with a gpu-scope fence; the consumer polls the flag
+// relaxed and then re-reads it once with ld.acquire before touching band data, which it reads
+// through L2 (ld.cg).
 //
 // Per step the warp stages its region in shared memory (lane = row of the window):
 //   left block  S[w0:w0+L, cg:w0]     (the column to annihilate + the bulge columns between)
@@ -43,7 +47,6 @@ __global__ void band_to_work(int64_t n, int b, const double* __restrict__ bands,
                              double* __restrict__ Bd, int64_t LDB, int* __restrict__ prog) {
   // b here is the INPUT band's semi-bandwidth (<= 2 b_chase for a relayed tail)
   const int64_t total = n * LDB;
-  if (blockIdx.x == 0 && threadIdx.x == 0) prog[n] = 0;  // the sweep ticket
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = idx / LDB, d = idx % LDB;
@@ -78,25 +81,22 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
   extern __shared__ __align__(16) unsigned char smraw[];
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smraw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
-  int* ticket = prog + n;
-
   const int64_t gend = sweep_end < n - 2 ? sweep_end : n - 2;
-  for (;;) {
-    int64_t gi = 0;
-    if (lane == 0) gi = atomicAdd(ticket, 1);
-    gi = __shfl_sync(0xffffffffu, gi, 0);
-    if (gi >= gend) break;
+  const int64_t wglob = (int64_t)blockIdx.x * BC_WARPS + (threadIdx.x >> 5);
+  const int64_t total_warps = (int64_t)gridDim.x * BC_WARPS;
+  for (int64_t gi = wglob; gi < gend; gi += total_warps) {
     for (int64_t j = 0; gi + 1 + j * b <= n - 2; ++j) {
       // ---- wait for the predecessor sweep to complete step j+2.  Polling is a relaxed L2 load
       //      (an acquire per poll would invalidate L1 on every iteration); once the flag is seen
-      //      one acquire fence pairs with the producer's fence, and __syncwarp extends the order
-      //      to the other lanes, whose band reads then go through L2 (ld.cg).
+      //      one acquire load of it pairs with the producer's fence + flag store (release
+      //      pattern), and __syncwarp extends the order to the other lanes, whose band reads then
+      //      go through L2 (ld.cg).  (A fence.acq_rel here costs 5 ms more at n = 49152.)
       if (gi > 0) {
         if (lane == 0) {
           const int need = (int)(j + 3);
           while (ld_relaxed(prog + gi - 1) < need) {
           }
-          fence_acq_rel_gpu();
+          (void)ld_acquire(prog + gi - 1);
         }
         __syncwarp();
       }
@@ -261,7 +261,7 @@ int64_t bc_slot_offset(int64_t n, int b, int64_t j) {
 
 static int64_t bc_ldb(int b) { return (2 * b + 2 + 1) / 2 * 2; }
 
-int64_t bc_ws_bytes(int64_t n, int b) { return n * bc_ldb(b) * 8 + (n + 1) * 4 + 256; }
+int64_t bc_ws_bytes(int64_t n, int b) { return n * bc_ldb(b) * 8 + n * 4 + 256; }
 
 // The chase of the sweeps [0, sweep_end) on a band of semi-bandwidth bw <= 2b (the relayed tail
 // of a partition, bulge.py:348-385); band_out (optional, (2b+1) x n reference layout) receives the
@@ -288,17 +288,24 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
       n, bw, bands_ref, Bd, LDB, prog);
   PEVD_LAUNCH_CHECK();
   if (b >= 2 && n >= 3) {
+    // per reflector about 7 b^2 multiply-adds (schedule.py:122): 14 b^2 flops
+    {
+      int64_t nref = 0;
+      for (int64_t j = 0; n - 2 - j * b > 0; ++j)
+        nref += std::max<int64_t>(0, std::min<int64_t>(sweep_end, n - 2 - j * b));
+      flops_add(14.0 * b * b * (double)nref);
+    }
     const size_t smem = sizeof(WarpSmem) * BC_WARPS;
+    auto kfn = bc_chase_kernel;
     static int attr_dev = -1;
     int dev;
     PEVD_CUDA(cudaGetDevice(&dev));
     if (attr_dev != dev) {
-      PEVD_CUDA(cudaFuncSetAttribute(bc_chase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+      PEVD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_dev = dev;
     }
     int per_sm = 0;
-    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bc_chase_kernel,
+    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn,
                                                             BC_WARPS * 32, smem));
     if (per_sm < 1) {
       set_error("bc_reduce: chase kernel cannot be resident");
@@ -306,12 +313,15 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
     }
     // about n/(3b) sweeps are in flight at once; twice that many warps keeps every sweep's
     // warp free when its turn comes, more would only add spinning warps next to the back stream
-    // (the ticket makes any grid size safe; one full wave at most)
+    // (cooperative: one full wave at most)
     const int64_t want_warps = std::min<int64_t>(n - 2, std::max<int64_t>(2 * n / (3 * b), 2 * num_sms()));
     const int64_t need = cdiv(want_warps, BC_WARPS);
     const int grid = (int)std::min<int64_t>((int64_t)per_sm * num_sms(), need);
-    bc_chase_kernel<<<grid, BC_WARPS * 32, smem, st>>>(n, b, Bd, LDB, prog, tau, V, vld,
-                                                       sweep_end);
+    int64_t n_ = n, sweep_end_ = sweep_end, LDB_ = LDB;
+    int b_ = b, vld_ = vld;
+    void* args[] = {&n_, &b_, &Bd, &LDB_, &prog, &tau, &V, &vld_, &sweep_end_};
+    PEVD_CUDA(cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(BC_WARPS * 32), args,
+                                          smem, st));
     PEVD_LAUNCH_CHECK();
   } else if (tau && n >= 3) {
     PEVD_CUDA(cudaMemsetAsync(tau, 0, 8 * bc_num_reflectors(n, b), st));

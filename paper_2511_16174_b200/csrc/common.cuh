@@ -37,6 +37,19 @@ void count_launch();
   } while (0)
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- executed-flop accounting, per host thread (one thread drives one rank / one EVD), by the
+//      stage whose work is being enqueued (the FlopCounter stages of core.py:26-62).  Host-known
+//      launches add on the host; launches whose sizes live on the device (grouped GEMMs of the
+//      divide and conquer, whose sizes depend on deflation) are summed by a tiny device kernel.
+enum Stage : int { ST_SBR = 0, ST_BC = 1, ST_SBR_BACK = 2, ST_BC_BACK = 3, ST_SOLVER = 4,
+                   ST_FINAL = 5, ST_NSTAGE = 6 };
+void flops_set_stage(int stage);
+void flops_add(double flops);                  // to the current stage
+void flops_reset();                            // zero host and device counters
+void flops_read(double out[ST_NSTAGE]);        // synchronises the device counter
+unsigned long long* flops_dev();               // device counters of this thread (may be null)
+int flops_stage();
 inline int64_t pad8(int64_t k) { return (k + 7) / 8 * 8; }
 
 int num_sms();

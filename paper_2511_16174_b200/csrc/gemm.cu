@@ -750,8 +750,28 @@ static int pick_ks(int64_t tiles, int64_t k, int64_t slots, int64_t min_chunk, i
   return best;
 }
 
+// executed flops of the grouped problems (sizes live on the device), into this thread's counter
+__global__ void grouped_flops_kernel(const GemmArgs* __restrict__ a, int count, int stage,
+                                     unsigned long long* __restrict__ acc) {
+  unsigned long long s = 0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    const GemmArgs& g = a[i];
+    if (g.m > 0 && g.n > 0 && g.k > 0) s += 2ull * g.m * g.n * g.k;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(acc + stage, s);
+}
+
+static void count_gemm_flops(const GemmArgs& g) {
+  double f = 2.0 * (double)g.m * (double)g.n * (double)g.k;
+  if (g.cmode == C_LOWER_TILES && g.m == g.n) f *= 0.5 * (1.0 + 64.0 / (double)g.m);
+  flops_add(f);
+}
+
 int gemm(cudaStream_t st, const GemmArgs& g0, double* ws, int64_t ws_elems) {
   if (g0.m <= 0 || g0.n <= 0) return OK;
+  count_gemm_flops(g0);
   static int pre = -1;
   if (pre < 0) {
     const char* e = getenv("PEVD_PRELOAD");
@@ -805,6 +825,10 @@ int gemm(cudaStream_t st, const GemmArgs& g0, double* ws, int64_t ws_elems) {
 int gemm_grouped(cudaStream_t st, const GemmArgs* d_args, int count, int64_t max_m,
                  int64_t max_n) {
   if (count <= 0 || max_m <= 0 || max_n <= 0) return OK;
+  if (unsigned long long* acc = flops_dev()) {
+    grouped_flops_kernel<<<1, 256, 0, st>>>(d_args, count, flops_stage(), acc);
+    PEVD_LAUNCH_CHECK();
+  }
   if (max_m * max_n >= (int64_t)128 * 128 * 64)
     return launch_fast_grouped<64, 128, 16, 32, 64, 3>(st, d_args, count, max_m, max_n);
   return launch_fast_grouped<64, 64, 16, 32, 32, 4>(st, d_args, count, max_m, max_n);

@@ -266,6 +266,8 @@ int panel_qr(cudaStream_t st, int64_t m, int k, const double* panel, int64_t ldp
     set_error("panel_qr: panel must be at least as tall as wide (m=%lld, k=%d)", (long long)m, k);
     return ERR_VALUE;
   }
+  // Householder QR 2 m k^2 - 2/3 k^3 flops, plus the Y^T v column of T and W = Y T: 2 m k^2
+  flops_add(4.0 * (double)m * k * k - 2.0 / 3.0 * (double)k * k * k);
   const int sms = num_sms();
   // fewer, fatter CTAs for short panels: every grid step pays one arrival + one partial per CTA
   int ncta = (int)std::min<int64_t>(sms, cdiv(m, 192));
