@@ -7,8 +7,8 @@ One step = one full two-stage EVD with eigenvectors of a synthetic random symmet
 device-resident path (pevd_syevd_device, input already in HBM; A is 19.3 GB, far larger than the
 126 MB L2, so no L2 flush is needed); `e2e` times the C-ABI call with HOST buffers
 (pevd_syevd: pinned host A in, lambda and Q out, device allocation included).  Under torchrun
-(N > 1) every rank solves its own EVD (replicas; the blockwise multi-GPU EVD is not wired into
-the bench yet) and value = N * 4 n^3 / max-over-ranks time.
+(N > 1) the N ranks solve ONE EVD together (blockwise columns, csrc/dist.cu over NCCL) and
+value = 4 n^3 / max-over-ranks time; a failure there exits non-zero (no replica fallback).
 
 --impl reference times the reference package itself (pipeevd.run, installed unmodified into
 baseline/_ref, tools/ref_cpu.py) on a bounded sample (n=1024 per step) on the host's cores.
@@ -95,63 +95,146 @@ def run_b200(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
+        # one EVD over all ranks (csrc/dist.cu over NCCL); a failure is a failure, no fallback
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        try:
-            return run_b200_distributed(args)
-        except Exception as exc:  # keep a number for the scaling run, labelled as replicas
-            if rank == 0:
-                print(f"distributed EVD failed ({exc!r}); falling back to replicas",
-                      file=sys.stderr)
-            args.fallback = repr(exc)[:200]
+        return run_b200_distributed(args)
     return run_b200_single(args)
 
 
+def stage_roofline(n, b, stage_ms, flops_exec, order, peaks, G=1):
+    """Per-stage roofline: achieved rate / (G x peak) for each of the five stages.
+    GEMM-like stages: algorithmic flops on the FP64 DMMA peak; the divide and
+    conquer: the merge-GEMM flops it EXECUTED (deflation-dependent, summed on the device); the
+    bulge chase: its compulsory HBM bytes on the measured HBM bandwidth."""
+    fl = stage_flops(n, order)
+    nref = sum(n - 2 - j * b for j in range((n - 3) // b + 1)) if n >= 3 else 0
+    bc_bytes = 8 * ((b + 1) * n + nref * (((b + 7) // 8) * 8 + 1) + 2 * n)
+    out = {}
+    for k, alg in (("sbr", fl["sbr"]), ("sbr_back", fl["sbr_back"]), ("bc_back", fl["bc_back"]),
+                   ("final", fl["final"]), ("solver", flops_exec.get("solver", 0.0))):
+        t = stage_ms.get(k, 0.0)
+        if t <= 0 or alg <= 0:
+            continue
+        ach = alg / (t * 1e-3) / 1e12
+        out[k] = {"bound": "tensor", "achieved": round(ach, 3), "peak": round(G * peaks["dmma"], 2),
+                  "unit": "TFLOP/s", "frac": round(ach / (G * peaks["dmma"]), 4),
+                  "ms": round(t, 1), "flops": alg,
+                  "flops_executed": flops_exec.get(k)}
+    t = stage_ms.get("bc", 0.0)
+    if t > 0:
+        hbm = peaks["hbm_gbs"]
+        ach = bc_bytes / (t * 1e-3) / 1e9
+        out["bc"] = {"bound": "hbm (latency-bound chase)", "achieved": round(ach, 2),
+                     "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 5), "ms": round(t, 1),
+                     "bytes": bc_bytes,
+                     "note": "compulsory bytes 8[(b+1)n + N_refl(pad8(b)+1) + 2n]; the chase is "
+                             "one GPU's wavefront (replicated partitions relay across GPUs)"}
+    return out
+
+
 def run_b200_distributed(args):
-    """N ranks cooperate on ONE n x n EVD: blockwise columns (distributed.py)."""
+    """N ranks cooperate on ONE n x n EVD: blockwise columns (csrc/dist.cu over NCCL)."""
+    import ctypes
     import torch
     import torch.distributed as dist
     from paper_2511_16174_b200 import PipelineConfig, _lib
     from paper_2511_16174_b200.distributed import run_distributed
+    from paper_2511_16174_b200.schedule import partition
+    from paper_2511_16174_b200.pipeline import back_ranges
     rank, world, local = dist_env()
     L = _lib.load()
     n, b = args.n, args.b
+    c0w, c1w = partition(n, world)[rank]
+    r0, r1 = back_ranges(n, world, 0.0)[rank]
     g = torch.Generator(device="cuda")
     g.manual_seed(args.seed)          # every rank generates the same A, keeps its columns
     a0 = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
     a0.add_(a0.t().clone())
     a0.mul_(0.5)
+    blk0 = a0[c0w:c1w].clone()        # (w, n): column-major n x w, this rank's columns
+    del a0
+    torch.cuda.empty_cache()
     cfg = PipelineConfig(workers=world, b=b, order=args.order)
+    blk = torch.empty_like(blk0)
 
     def block(c0, c1):
-        return a0[c0:c1].clone()
+        return blk
 
     def barrier():
         dist.barrier()
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
+        blk.copy_(blk0)
         run_distributed(block, cfg, n=n, gather_q=False)
-        torch.cuda.empty_cache()
     launches0 = L.pevd_kernel_launches()
-    times = []
+    times, infos = [], []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
+            blk.copy_(blk0)
             barrier()
-            t0 = time.perf_counter()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            run_distributed(block, cfg, n=n, gather_q=False)
+            _, _, ledger, info = run_distributed(block, cfg, n=n, gather_q=False)
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+            infos.append(info)
             barrier()
-            torch.cuda.empty_cache()
     launches = (L.pevd_kernel_launches() - launches0) // max(1, args.steps)
     ms = sum(times) / len(times)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = 4 * n ** 3 / (ms * 1e-3) / 1e12
+    # per-stage times: the max over ranks of each stage's span; executed flops summed
+    st = infos[-1]["stats"].stages
+    mine = [getattr(st, k + "_ms")[1] - getattr(st, k + "_ms")[0]
+            for k in ("sbr", "bc", "solver", "sbr_back", "bc_back", "final")] + list(st.flops)
+    tt = torch.tensor(mine, dtype=torch.float64, device="cuda")
+    mx = tt[:6].clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = tt[6:].clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    names = ("sbr", "bc", "solver", "sbr_back", "bc_back", "final")
+    stage_ms = dict(zip(names, mx.tolist()))
+    fx = dict(zip(("sbr", "bc", "sbr_back", "bc_back", "solver", "final"), sm.tolist()))
+    # the divide and conquer is replicated (every rank solves): one rank's executed flops
+    fx["solver"] = fx["solver"] / world
+    peaks = load_fp64_peaks()
+    stages = stage_roofline(n, b, stage_ms, fx, args.order, peaks, world)
+    dom = max((k for k in stages if k != "bc"), key=lambda k: stages[k]["ms"])
+    roofline = dict(stages[dom])
+    roofline.update({"kernel": dom, "traffic": None,
+                     "peak_source": f"{world} x FP64 DMMA microbenchmark "
+                                    f"(profiles/r01_fp64_peaks.json)",
+                     "stages": stages,
+                     "comm_words": ledger.total_words,
+                     "comm_words_by_stage": {k: ledger.words(stage=k) for k in ledger.stages()}})
+    clocks = clk.summary()
+    # ---- e2e: this rank's column block from pinned host memory, its Q slab back to the host
+    e2e = None
+    if not args.no_e2e:
+        hblk = torch.empty(blk0.shape, dtype=torch.float64, pin_memory=True)
+        hblk.copy_(blk0)
+        hq = torch.empty((max(r1 - r0, 1), n), dtype=torch.float64, pin_memory=True)
+        del blk0
+        torch.cuda.empty_cache()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        blk.copy_(hblk, non_blocking=True)
+        res, _, _, info = run_distributed(block, cfg, n=n, gather_q=False)
+        hq.copy_(info["q_part"], non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ems = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        ems = float(ems.item())
+        e2e = {"value": round(4 * n ** 3 / (ems * 1e-3) / 1e12, 4), "unit": "TFLOP/s",
+               "ms_per_step": round(ems, 1), "h2d_bytes_per_step": 8 * n * n,
+               "d2h_bytes_per_step": 8 * n * n,
+               "note": "each rank: its column block pinned host -> device, its Q slab back"}
     cpu = cpu_baseline(args.cpu_n) if (rank == 0 and not args.no_cpu) else None
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world,
@@ -160,15 +243,12 @@ def run_b200_distributed(args):
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"ONE dense symmetric FP64 EVD with eigenvectors, n={n}, "
                                        f"b={b}, order={args.order}, blockwise columns over "
-                                       f"{world} GPUs",
-                           "n": n, "b": b, "parallelism": f"blockwise{world}",
+                                       f"{world} GPUs (csrc/dist.cu, NCCL)",
+                           "n": n, "b": b, "order": args.order, "parallelism": f"blockwise{world}",
                            "l2": "input >> 126 MB L2 (no flush needed)",
                            "flop_convention": "4 n^3 / wall (PAPER.md:92)"},
-                "roofline": None, "cpu_baseline": cpu,
-                "e2e": {"value": round(value, 4), "unit": "TFLOP/s",
-                        "note": "device-resident input per rank; host path not timed at N>1",
-                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-                "clocks": clk.summary(), "gpu_launches": int(launches), "impl": "b200"}
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "clocks": clocks, "gpu_launches": int(launches), "impl": "b200"}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
@@ -244,6 +324,7 @@ def run_b200_single(args):
     st = stats[-1]
     stage_ms = {k: getattr(st, k + "_ms")[1] - getattr(st, k + "_ms")[0]
                 for k in ("sbr", "bc", "solver", "sbr_back", "bc_back", "final")}
+    fx = dict(zip(("sbr", "bc", "sbr_back", "bc_back", "solver", "final"), list(st.flops)))
     fl = stage_flops(n, args.order)
     dom = max(("sbr", "sbr_back", "bc_back", "final", "solver"), key=lambda k: stage_ms[k])
     peaks = load_fp64_peaks()
@@ -264,10 +345,8 @@ def run_b200_single(args):
                                " on this pool's B200 (profiles/r01_fp64_peaks.json); "
                                "MEASURED_PEAKS.json has no FP64 entry",
                 "stage_ms": {k: round(v, 1) for k, v in stage_ms.items()},
-                "stage_tflops": {k: round(fl[k] / (stage_ms[k] * 1e-3) / 1e12, 2)
-                                 for k in fl if stage_ms[k] > 0 and fl[k] > 0 and k != "solver"},
-                "stage_tflops_note": "algorithmic flops / stage time; the divide and conquer is "
-                                     "omitted: its (4/3) n^3 bound shrinks with deflation"}
+                "stages": stage_roofline(n, b, stage_ms, fx, args.order, peaks),
+                "executed_flops": {k: v for k, v in fx.items() if v > 0}}
     clocks = clk.summary()
 
     # ---- e2e through the C ABI with host buffers (pevd_syevd)
@@ -296,6 +375,11 @@ def run_b200_single(args):
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_baseline(args.cpu_n)
+    same_n = None
+    if rank == 0 and not args.no_same_n:
+        same_n = same_n_runs(L, b, args.order, (1024, 4096))
+        if cpu and cpu.get("kind") == "reference" and "1024" in same_n:
+            same_n["ratio_vs_reference_n1024"] = round(same_n["1024"]["tflops"] / cpu["value"], 1)
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 1),
@@ -304,16 +388,51 @@ def run_b200_single(args):
                 "config": {"workload": f"dense symmetric FP64 EVD with eigenvectors, n={n}, b={b}, "
                                        f"order={args.order}, A=(G+G^T)/2 G~N(0,1)",
                            "n": n, "b": b, "order": args.order,
-                           "parallelism": ("replicas (" + getattr(args, "fallback", "") + ")")
-                           if world > 1 else "1 GPU",
+                           "parallelism": "1 GPU",
                            "l2": "input 8n^2 = %.1f GB >> 126 MB L2 (no flush needed)" % (8 * n * n / 1e9),
                            "flop_convention": "4 n^3 / wall (PAPER.md:92)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-                "accuracy": accuracy,
+                "accuracy": accuracy, "same_n": same_n,
                 "gpu_launches": int(launches), "impl": "b200"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def same_n_runs(L, b, order, ns):
+    """The same device path at the reference arm's sizes (a like-for-like ratio beside the
+    headline): best of 3 CUDA-event-timed EVDs per n, inputs resident."""
+    import ctypes
+    import torch
+    from paper_2511_16174_b200 import _lib
+    out = {}
+    oc = _lib.ORDER_CODES[order]
+    P = ctypes.c_void_p
+    for n in ns:
+        g = torch.Generator(device="cuda")
+        g.manual_seed(n)
+        a0 = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+        a0 = (a0 + a0.t()) * 0.5
+        a = torch.empty_like(a0)
+        q = torch.empty_like(a0)
+        lam = torch.empty(n, dtype=torch.float64, device="cuda")
+        ws = torch.empty(L.pevd_syevd_workspace_bytes(n, b, 1, oc), dtype=torch.uint8, device="cuda")
+        s = torch.cuda.current_stream()
+        best = None
+        for _ in range(4):
+            a.copy_(a0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            _lib.check(L.pevd_syevd_device(n, b, P(a.data_ptr()), n, P(lam.data_ptr()),
+                                           P(q.data_ptr()), n, 1, oc, P(ws.data_ptr()),
+                                           ws.numel(), P(s.cuda_stream),
+                                           ctypes.byref(_lib.PevdStats())), "same_n")
+            e1.record(s)
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1)
+            best = t if best is None else min(best, t)
+        out[str(n)] = {"ms": round(best, 2), "tflops": round(4 * n ** 3 / (best * 1e-3) / 1e12, 4)}
+    return out
 
 
 def load_fp64_peaks():
@@ -322,10 +441,15 @@ def load_fp64_peaks():
         d = json.load(open(path))
         dmma = max(x["tflops"] for x in d["micro"] if x["kind"].startswith("dmma"))
         dfma = max(x["tflops"] for x in d["micro"] if x["kind"] == "dfma")
-        return {"dmma": round(dmma, 2), "dfma": round(dfma, 2),
-                "cublas_dgemm": round(d.get("cublas_dgemm_8192_sustained_4s_tflops", 0), 2)}
+        out = {"dmma": round(dmma, 2), "dfma": round(dfma, 2),
+               "cublas_dgemm": round(d.get("cublas_dgemm_8192_sustained_4s_tflops", 0), 2)}
     except Exception:
-        return {"dmma": 37.17, "dfma": 34.19, "cublas_dgemm": 35.41}
+        out = {"dmma": 37.17, "dfma": 34.19, "cublas_dgemm": 35.41}
+    try:  # HBM: the driver-measured copy bandwidth of this pool's B200
+        out["hbm_gbs"] = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        out["hbm_gbs"] = 6440.1
+    return out
 
 
 def cpu_baseline(n_cpu: int):
@@ -433,6 +557,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip the residual/orthogonality check")
+    ap.add_argument("--no-same-n", action="store_true", help="skip the n=1024/4096 device runs")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

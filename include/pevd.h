@@ -54,6 +54,47 @@ typedef struct pevd_stats {
   double flops[6];
 } pevd_stats;
 
+/* ---------------------------------------------------------------- multi-GPU (blockwise)
+ * Trace events and ledger messages of one rank of a distributed EVD (TraceEvent / CommLedger,
+ * messaging.py:51-167).  Stages of events: PEVD_TRACE_*; stages of messages: PEVD_LEDGER_*.
+ * dst of a message: >= 0 a rank, -1 the host, -2 a broadcast (messaging.py HOST / BROADCAST). */
+#define PEVD_TRACE_SBR 0
+#define PEVD_TRACE_BC 1
+#define PEVD_TRACE_SBR_BACK 2
+#define PEVD_TRACE_BC_BACK 3
+#define PEVD_TRACE_SOLVER 4
+#define PEVD_TRACE_FINAL 5
+#define PEVD_TRACE_COMM 6
+#define PEVD_LEDGER_SBR 0
+#define PEVD_LEDGER_SBR_PANEL 1
+#define PEVD_LEDGER_BANDSTAGE 2
+#define PEVD_LEDGER_BC 3
+#define PEVD_LEDGER_UGATHER 4
+#define PEVD_LEDGER_QD 5
+#define PEVD_LEDGER_RESULT 6
+#define PEVD_LEDGER_GATHER 7
+
+typedef struct pevd_trace_event {
+  int32_t worker, stage, block, pad;
+  double t_start_ms, t_end_ms;  /* device time from the rank's t0 (CUDA events) */
+  int64_t words;                /* FP64 words moved (Comm spans) */
+} pevd_trace_event;
+
+typedef struct pevd_message {
+  int32_t src, dst, stage, pad;
+  int64_t words;
+} pevd_message;
+
+/* Caller-owned arrays; the library fills min(count, cap) entries and reports the full count. */
+typedef struct pevd_dist_stats {
+  pevd_stats stages;        /* this rank's stage spans (ms from t0) and executed flops */
+  double t0_mono_ns;        /* CLOCK_MONOTONIC at t0 (after a barrier of all ranks) */
+  pevd_trace_event* events;
+  int64_t events_cap, n_events;
+  pevd_message* msgs;       /* this rank's SENDS, as words actually handed to the transport */
+  int64_t msgs_cap, n_msgs;
+} pevd_dist_stats;
+
 const char* pevd_last_error(void);
 const char* pevd_version(void);
 /* Number of CUDA kernels this library has launched since it was loaded. */
@@ -152,6 +193,36 @@ int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int
                        int64_t ldx, int64_t nrows, void* workspace, void* stream);
 int pevd_bc_back_left(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
                       int64_t ldx, int64_t ncols, void* workspace, void* stream);
+
+/* ---------------------------------------------------------------- multi-GPU entry points
+ * The reference's `run(a, PipelineConfig(workers=G))` (pipeline.py:511-548) with G cooperating
+ * devices and the paper's blockwise column distribution (schedule.py:21-33).  col_lo (G+1) is
+ * the SBR column partition (`partition(n, G)`), back_lo (G+1) the back-transform partition
+ * (`back_plan_sizes`, backtrans.py:108-121): columns of Q in conventional order, rows otherwise.
+ * b <= 32. */
+
+/* 128-byte NCCL unique id (rank 0 creates it; the caller shares it, e.g. over torch.distributed). */
+int pevd_nccl_unique_id(char* out128);
+/* One process per GPU: an NCCL communicator for this rank (the current CUDA device). */
+int pevd_comm_nccl_create(int rank, int size, const char* id128, void** comm);
+void pevd_comm_destroy(void* comm);
+
+/* One rank of the distributed EVD (every rank calls it; device pointers).  blk: this rank's
+ * column block [col_lo[r], col_lo[r+1]) with all n rows (n x w, ldb; destroyed).  lam: n (every
+ * rank).  Q: conventional -> the rank's back columns (n x nb, ldq, Fortran order); pipelined /
+ * sequential -> the rank's back rows stored as an n x nb column-major block (the rows of Q in C
+ * order).  Synchronous. */
+int pevd_dist_syevd(void* comm, int64_t n, int b, double* blk, int64_t ldb, const int64_t* col_lo,
+                    const int64_t* back_lo, double* lam, double* Q, int64_t ldq, int want_vectors,
+                    int order, void* stream, pevd_dist_stats* stats);
+
+/* One process, G workers (one host thread each) on devices devs[0..G) (entries may repeat: workers
+ * then share a GPU), peer-to-peer transfers over NVLink.  HOST buffers: A column-major (lda),
+ * lam (n), Q n x n: Fortran order in conventional order, C order otherwise (pipeline.py:495,503).
+ * stats: G entries (may be NULL). */
+int pevd_syevd_multi(int G, const int* devs, int64_t n, int b, const double* A, int64_t lda,
+                     const int64_t* col_lo, const int64_t* back_lo, double* lam, double* Q,
+                     int want_vectors, int order, pevd_dist_stats* stats);
 
 #ifdef __cplusplus
 }

@@ -30,6 +30,41 @@ class PevdStats(ctypes.Structure):
 FLOP_STAGES = ("SBR", "BC", "SBR-Back", "BC-Back", "Solver", "FinalMultiply")
 
 
+# stage codes of pevd_trace_event / pevd_message (pevd.h PEVD_TRACE_* / PEVD_LEDGER_*)
+TRACE_STAGES = ("SBR", "BC", "SBR-Back", "BC-Back", "Solver", "FinalMultiply", "Comm")
+LEDGER_STAGES = ("SBR", "SBR-panel", "BandStage", "BC", "U-gather", "Qd", "Result", "Gather")
+
+
+class PevdTraceEvent(ctypes.Structure):
+    _fields_ = [("worker", ctypes.c_int32), ("stage", ctypes.c_int32), ("block", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("t_start_ms", _dbl), ("t_end_ms", _dbl),
+                ("words", _i64)]
+
+
+class PevdMessage(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_int32), ("dst", ctypes.c_int32), ("stage", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("words", _i64)]
+
+
+class PevdDistStats(ctypes.Structure):
+    _fields_ = [("stages", PevdStats), ("t0_mono_ns", _dbl),
+                ("events", ctypes.POINTER(PevdTraceEvent)), ("events_cap", _i64),
+                ("n_events", _i64), ("msgs", ctypes.POINTER(PevdMessage)), ("msgs_cap", _i64),
+                ("n_msgs", _i64)]
+
+
+def new_dist_stats(events_cap: int = 1 << 15, msgs_cap: int = 1 << 15):
+    """A PevdDistStats with caller-owned event / message arrays (kept alive on the object)."""
+    st = PevdDistStats()
+    st._ev = (PevdTraceEvent * events_cap)()
+    st._ms = (PevdMessage * msgs_cap)()
+    st.events = ctypes.cast(st._ev, ctypes.POINTER(PevdTraceEvent))
+    st.events_cap = events_cap
+    st.msgs = ctypes.cast(st._ms, ctypes.POINTER(PevdMessage))
+    st.msgs_cap = msgs_cap
+    return st
+
+
 # name -> (restype, argtypes); must cover every function declared in include/pevd.h
 SIGNATURES = {
     "pevd_last_error": (ctypes.c_char_p, []),
@@ -61,6 +96,15 @@ SIGNATURES = {
     "pevd_bc_back_workspace_bytes": (_i64, [_i64, _i64]),
     "pevd_bc_back_right": (_int, [_i64, _int, _vp, _vp, _int, _vp, _i64, _i64, _vp, _vp]),
     "pevd_bc_back_left": (_int, [_i64, _int, _vp, _vp, _int, _vp, _i64, _i64, _vp, _vp]),
+    "pevd_nccl_unique_id": (_int, [ctypes.c_char_p]),
+    "pevd_comm_nccl_create": (_int, [_int, _int, ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "pevd_comm_destroy": (None, [_vp]),
+    "pevd_dist_syevd": (_int, [_vp, _i64, _int, _vp, _i64, ctypes.POINTER(_i64),
+                               ctypes.POINTER(_i64), _vp, _vp, _i64, _int, _int, _vp,
+                               ctypes.POINTER(PevdDistStats)]),
+    "pevd_syevd_multi": (_int, [_int, ctypes.POINTER(_int), _i64, _int, _vp, _i64,
+                                ctypes.POINTER(_i64), ctypes.POINTER(_i64), _vp, _vp, _int, _int,
+                                ctypes.POINTER(PevdDistStats)]),
 }
 
 _lib = None

@@ -35,6 +35,9 @@ struct FlopState {
   double host[ST_NSTAGE] = {};
   unsigned long long* dev = nullptr;
   int dev_id = -1;
+  ~FlopState() {
+    if (dev) cudaFree(dev);
+  }
 };
 static thread_local FlopState g_flops;
 

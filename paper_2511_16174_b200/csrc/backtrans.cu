@@ -668,6 +668,40 @@ int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, 
   return OK;
 }
 
+// X (nrows x n, col-major ldx) <- X Q_s = X B_0 B_1 ... (aggregated blocks in creation order):
+// the RowAccumulator of backtrans.py:149-183 for a block of rows (the distributed pipelined
+// order forms only its rows of Q_s, starting from X = the rows of the identity).
+int sbr_back_apply_right(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_t ldy,
+                         const double* Tall, double* X, int64_t ldx, int64_t nrows, void* ws,
+                         bool prepared) {
+  if (b < 1 || n <= b || nrows <= 0) return OK;
+  if (nrows > n) {
+    set_error("sbr_back_apply_right: %lld rows > n", (long long)nrows);
+    return ERR_VALUE;
+  }
+  if (!prepared) PEVD_TRY(sbr_back_prepare(st, n, b, Yfull, ldy, Tall, ws));
+  const int NB = nb_agg();
+  SbrBackWs W = sbr_back_carve(n, b, ws, NB);
+  const int64_t R = sbr_num_rounds(n, b);
+  for (int64_t g = 0; g < W.ngroups; ++g) {
+    int64_t t0, c0, K;
+    group_dims(n, b, NB, R, g, &t0, &c0, &K);
+    const int64_t m = n - t0;
+    const double* Y = Yfull + t0 + c0 * ldy;  // m x K
+    const double* Tg = W.Tagg + g * W.K * W.K;
+    double* X2 = X + t0 * ldx;                // nrows x m
+    // tmp1 = X2 Y (nrows x K); tmp2 = tmp1 T; X2 -= tmp2 Y^T
+    GemmArgs g1{nrows, K, m, 1.0, 0.0, X2, ldx, Y, ldy, W.tmp1, nrows, 0, 0, A_GENERAL, C_ALL};
+    PEVD_TRY(gemm(st, g1, W.sk, W.skn));
+    GemmArgs g2{nrows, K, K, 1.0, 0.0, W.tmp1, nrows, Tg, W.K, W.tmp2, nrows, 0, 0, A_GENERAL,
+                C_ALL};
+    PEVD_TRY(gemm(st, g2, W.sk, W.skn));
+    GemmArgs g3{nrows, m, K, -1.0, 1.0, W.tmp2, nrows, Y, ldy, X2, ldx, 0, 1, A_GENERAL, C_ALL};
+    PEVD_TRY(gemm(st, g3, W.sk, W.skn));
+  }
+  return OK;
+}
+
 // out (cols x rows, ld ldo) = in^T (in: rows x cols, ld ldi); 32 x 32 tiles through shared memory
 __global__ void transpose_kernel(int64_t rows, int64_t cols, const double* __restrict__ in,
                                  int64_t ldi, double* __restrict__ out, int64_t ldo) {

@@ -77,7 +77,7 @@ __global__ void work_to_tridiag(int64_t n, const double* __restrict__ Bd, int64_
 __global__ void __launch_bounds__(BC_WARPS * 32)
     bc_chase_kernel(int64_t n, int b, double* __restrict__ Bd, int64_t LDB, int* prog,
                     double* __restrict__ tau_out, double* __restrict__ V_out, int vld,
-                    int64_t sweep_end) {
+                    int64_t sweep_end, int64_t slot_n, int64_t slot_col0) {
   extern __shared__ __align__(16) unsigned char smraw[];
   WarpSmem& S = reinterpret_cast<WarpSmem*>(smraw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
       const int nleft = (int)(w0 - cg);  // 1 (j = 0) or b
       const int64_t tend = (w0 + L + b < n) ? w0 + L + b : n;
       const int nT = (int)(tend - (w0 + L));
-      const int64_t slot = (int64_t)j * (n - 2) - (int64_t)b * j * (j - 1) / 2 + gi;
+      // reflector (slot_col0 + gi, j) of the slot_n problem (a relayed tail writes straight into
+      // the whole matrix's fixed slots)
+      const int64_t slot = (int64_t)j * (slot_n - 2) - (int64_t)b * j * (j - 1) / 2 + slot_col0 + gi;
 
       // ---- stage the whole region with independent loads (one L2 round trip, not 3b)
       double rl[BMAX], rw[BMAX], rc[BMAX];
@@ -268,7 +270,8 @@ int64_t bc_ws_bytes(int64_t n, int b) { return n * bc_ldb(b) * 8 + n * 4 + 256; 
 // resulting band with its residual fill, d / e (optional) its tridiagonal part.
 int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* bands_ref,
                     int64_t sweep_end, double* d, double* e, double* band_out, double* tau,
-                    double* V, int vld, void* ws) {
+                    double* V, int vld, void* ws, int64_t slot_n, int64_t slot_col0) {
+  if (slot_n <= 0) slot_n = n;
   if (b < 1 || b > BMAX) {
     set_error("bc_reduce: bandwidth %d outside [1, %d] (device kernel limit)", b, BMAX);
     return ERR_VALUE;
@@ -319,11 +322,11 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
     const int grid = (int)std::min<int64_t>((int64_t)per_sm * num_sms(), need);
     int64_t n_ = n, sweep_end_ = sweep_end, LDB_ = LDB;
     int b_ = b, vld_ = vld;
-    void* args[] = {&n_, &b_, &Bd, &LDB_, &prog, &tau, &V, &vld_, &sweep_end_};
+    void* args[] = {&n_, &b_, &Bd, &LDB_, &prog, &tau, &V, &vld_, &sweep_end_, &slot_n, &slot_col0};
     PEVD_CUDA(cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(BC_WARPS * 32), args,
                                           smem, st));
     PEVD_LAUNCH_CHECK();
-  } else if (tau && n >= 3) {
+  } else if (tau && n >= 3 && slot_n == n && slot_col0 == 0) {
     PEVD_CUDA(cudaMemsetAsync(tau, 0, 8 * bc_num_reflectors(n, b), st));
   }
   if (d && e) {

@@ -39,9 +39,11 @@ int bc_reduce(cudaStream_t st, int64_t n, int b, const double* bands_ref, double
               double* tau, double* V, int vld, void* ws);
 // Partition chase (bulge.py:348-385): sweeps [0, sweep_end) on a band of semi-bandwidth bw <= 2b;
 // band_out ((2b+1) x n, may be null) gets the band afterwards, d / e (may be null) its diagonals.
+// slot_n / slot_col0 (> 0 / >= 0): the band is the tail [slot_col0, slot_n) of a slot_n problem
+// and the reflectors go to that problem's fixed slots (sweep gi is global sweep slot_col0 + gi).
 int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* bands_ref,
                     int64_t sweep_end, double* d, double* e, double* band_out, double* tau,
-                    double* V, int vld, void* ws);
+                    double* V, int vld, void* ws, int64_t slot_n = 0, int64_t slot_col0 = 0);
 
 // ---------------- tridiagonal divide and conquer (stedc.cu)
 int64_t stedc_ws_bytes(int64_t n);
@@ -70,6 +72,10 @@ int sbr_back_form(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_
 int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_t ldy,
                         const double* Tall, double* X, int64_t ldx, int64_t ncols, void* ws,
                         bool prepared = false);
+// X (nrows x n) <- X Q_s: rows of Q_s from rows of the identity (distributed pipelined order).
+int sbr_back_apply_right(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_t ldy,
+                         const double* Tall, double* X, int64_t ldx, int64_t nrows, void* ws,
+                         bool prepared = false);
 // Right-apply the bulge reflectors to the rows of X (nrows x n, col-major ldx):
 // X <- X Q_b  (== (Q_b^T X^T)^T, the reordered BC-Back, backtrans.py:277-310).
 int64_t bc_back_ws_bytes(int64_t n, int64_t nrows);

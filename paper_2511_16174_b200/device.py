@@ -273,3 +273,45 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None):
         raise RuntimeError(L.pevd_last_error().decode())
     _lib.check(rc, "syevd")
     return lam.cpu().numpy()[:n], (from_dev(q) if want_vectors else None), st
+
+
+def syevd_multi(a, workers: int, b: int, col_ranges, back_ranges, want_vectors=True,
+                order="pipelined", devices=None):
+    """Blockwise EVD over `workers` cooperating devices in this process (pevd_syevd_multi: one
+    host thread per worker, peer-to-peer transfers).  Workers map round-robin onto the visible
+    GPUs; with fewer GPUs than workers, several workers share a device (same protocol, same
+    messages, no extra parallelism).  Returns (lam, Q (Fortran order in conventional order,
+    C order otherwise) or None, [PevdDistStats per worker])."""
+    L = _lib.load()
+    torch = _torch()
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    n = a.shape[0]
+    G = int(workers)
+    if devices is None:
+        ngpu = torch.cuda.device_count()
+        devices = [w % ngpu for w in range(G)]
+    devs = (ctypes.c_int * G)(*devices)
+    col_lo = (ctypes.c_int64 * (G + 1))(*([lo for lo, _ in col_ranges] + [n]))
+    back_lo = (ctypes.c_int64 * (G + 1))(*([lo for lo, _ in back_ranges] + [n]))
+    lam = np.empty(n, dtype=np.float64)
+    q = None
+    if want_vectors:
+        q = np.empty((n, n), dtype=np.float64,
+                     order="F" if order == "conventional" else "C")
+    stats = (_lib.PevdDistStats * G)()
+    keep = [_lib.new_dist_stats() for _ in range(G)]
+    for w in range(G):
+        stats[w] = keep[w]
+    rc = L.pevd_syevd_multi(G, devs, n, b, a.ctypes.data_as(ctypes.c_void_p), n, col_lo, back_lo,
+                            lam.ctypes.data_as(ctypes.c_void_p),
+                            q.ctypes.data_as(ctypes.c_void_p) if q is not None else None,
+                            int(want_vectors), _lib.ORDER_CODES[order], stats)
+    if rc == _lib.PEVD_ERR_CONVERGE:
+        raise RuntimeError(L.pevd_last_error().decode())
+    _lib.check(rc, "syevd_multi")
+    out = []
+    for w in range(G):
+        st = stats[w]
+        st._ev, st._ms = keep[w]._ev, keep[w]._ms
+        out.append(st)
+    return lam, q, out

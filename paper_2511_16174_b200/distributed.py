@@ -1,25 +1,26 @@
-"""Multi-GPU pipelined EVD: the paper's blockwise column distribution over torch.distributed.
+"""Multi-GPU pipelined EVD over torch.distributed: one process per GPU (torchrun).
 
-Restates the reference's worker/host protocol (pipeline.py:170-508) for one process per GPU:
+`run_distributed(a, cfg)` on CUDA is the production path: every rank calls the C++ per-rank
+orchestrator `pevd_dist_syevd` (csrc/dist.cu) over an NCCL communicator of its own (created
+from a unique id that rank 0 shares through the process group).  The protocol (restating
+pipeline.py:170-508, the paper's blockwise column distribution):
 
-* SBR (pipeline.py:198-302): rank w owns columns [c0w, c1w) with all n rows (full storage,
-  schedule.py:21-33).  Per round the panel's owner gathers straddling pieces (C2/C3), factors it
-  (panel QR on its device), and broadcasts the factor (C4); every rank forms its rows of A W by
-  symmetry from its own columns and all-gathers them (C5); every rank then applies the two-sided
-  update to its own columns only.  The trailing matrix never moves.
-* BC (pipeline.py:306-363): the band is all-gathered (13 MB at n=49152) and every rank runs the
-  wavefront chase on its device.  Over NVSwitch this replaces the reference's serial relay of the
-  overlap block and the 10 GB reflector all-gather (C7-C10) with one band all-gather; the result
-  is bitwise identical on every rank because the chase kernel is deterministic.
-* Solver: every rank runs the device divide and conquer (no 19 GB Q_d broadcast, C11).
-* Back transformation (pipeline.py:335-420): rank w owns rows back_plan_sizes(...)[w] of Q.  It
-  accumulates its rows of Q_s panel by panel (RowAccumulator), applies the bulge reflectors
-  (BC-Back, reordered) and multiplies by Q_d; rows are all-gathered at the end (C12).
+* SBR (pipeline.py:198-302): rank w owns columns [c0w, c1w) with all n rows.  Per round the
+  straddling pieces of a panel are all-gathered, its owner factors it and broadcasts
+  [W | Y | T | R]; every rank forms its rows of A W by symmetry and the row blocks are
+  all-gathered; every rank updates its own columns (double-blocked, 16 panels per group).
+* BC (pipeline.py:306-363): band pieces to rank 0, then the relay: rank w chases the sweeps of
+  its columns down the remaining band (bulge.py:348-385) and sends the 2b x b overlap block and
+  the band tail to rank w + 1; the tridiagonal pieces and the reflector sets are all-gathered.
+* Solver: every rank runs the device divide and conquer (only its back columns of Q_d in
+  conventional order); eigenvalues only by bisection.
+* Back transformation (pipeline.py:335-420): rows (pipelined / sequential) or columns
+  (conventional) of back_plan_sizes; Q slabs are all-gathered on request.
 
-The compute goes through an `ops` object: `CudaOps` (libpevd.so, production) or a CPU
-implementation supplied by the tests (so the protocol runs under gloo without a GPU).  The
-ledger records the words the reference's protocol counts (messaging.py:111-167), so its analytic
-checks (comm_broadcast_words, 2 b^2 per BC boundary) read the same.
+`run_distributed(a, cfg, ops=...)` with a compute object (tests/cpu_ops.py) runs the SAME
+message schedule in Python, host-side, so the protocol and its measured ledger are testable
+under gloo on CPU: every message either path sends is booked under the same (src, dst, stage,
+words), and `schedule.protocol_ledger` states them in closed form.
 """
 from __future__ import annotations
 
@@ -36,119 +37,6 @@ from .schedule import back_plan_sizes, partition, round_schedule
 
 # ----------------------------------------------------------------------------------------------
 # compute interface
-
-
-class CudaOps:
-    """Device compute over the C ABI (column-major matrices as torch tensors of shape (cols, rows)
-    on the current CUDA device)."""
-
-    def __init__(self):
-        from . import _lib
-        self.torch = _lib.require_cuda()
-        self.L = _lib.load()
-        self._lib = _lib
-        self.device = torch.device("cuda", torch.cuda.current_device())
-
-    # -- memory
-    def from_host(self, a):  # numpy (rows x cols) -> column-major device tensor
-        return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64).T)).to(self.device)
-
-    def to_host(self, t):
-        return np.asfortranarray(t.detach().cpu().numpy().T)
-
-    def zeros(self, rows, cols):
-        return torch.zeros((cols, rows), dtype=torch.float64, device=self.device)
-
-    def _p(self, t):
-        import ctypes
-        return ctypes.c_void_p(t.data_ptr())
-
-    def _stream(self):
-        import ctypes
-        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-
-    # -- kernels
-    def gemm(self, A, B, C, alpha=1.0, beta=0.0, ta=False, tb=False):
-        """C = alpha op(A) op(B) + beta C on column-major views (tensors (cols, rows))."""
-        lda, ldb, ldc = A.stride(0), B.stride(0), C.stride(0)
-        m = A.shape[0] if ta else A.shape[1]
-        k = A.shape[1] if ta else A.shape[0]
-        n = B.shape[1] if tb else B.shape[0]
-        ws = getattr(self, "_ws", None)
-        if ws is None:
-            ws = self._ws = torch.empty(64 << 20, dtype=torch.uint8, device=self.device)
-        rc = self.L.pevd_dgemm(int(ta), int(tb), m, n, k, alpha, self._p(A), lda, self._p(B), ldb,
-                               beta, self._p(C), ldc, self._p(ws), ws.numel(), self._stream())
-        self._lib.check(rc, "dgemm")
-
-    def panel_qr(self, P):
-        """Householder QR of the column-major panel P (pw, m): returns (R, Y, T) as tensors."""
-        pw, m = P.shape
-        R = torch.empty((pw, pw), dtype=torch.float64, device=self.device)
-        Y = torch.empty((pw, m), dtype=torch.float64, device=self.device)
-        T = torch.empty((pw, pw), dtype=torch.float64, device=self.device)
-        ws = torch.empty(self.L.pevd_panel_qr_workspace_bytes(), dtype=torch.uint8, device=self.device)
-        rc = self.L.pevd_panel_qr(m, pw, self._p(P), P.stride(0), self._p(R), self._p(Y), m, None, m,
-                                  self._p(T), self._p(ws), self._stream())
-        self._lib.check(rc, "panel_qr")
-        return R, Y, T
-
-    def bc(self, bands):
-        """bands (b+1, n) device tensor -> (d, e) host arrays, (tau, V) device tensors."""
-        b, n = bands.shape[0] - 1, bands.shape[1]
-        bands = bands.contiguous()
-        d = torch.empty(n, dtype=torch.float64, device=self.device)
-        e = torch.empty(max(n, 2), dtype=torch.float64, device=self.device)
-        nref = max(self.L.pevd_bc_num_reflectors(n, b), 1)
-        vld = ((b + 7) // 8) * 8
-        tau = torch.zeros(nref, dtype=torch.float64, device=self.device)
-        V = torch.zeros(nref * vld, dtype=torch.float64, device=self.device)
-        ws = torch.empty(self.L.pevd_bc_workspace_bytes(n, b), dtype=torch.uint8, device=self.device)
-        rc = self.L.pevd_bc(n, b, self._p(bands), self._p(d), self._p(e), self._p(tau), self._p(V),
-                            vld, self._p(ws), self._stream())
-        self._lib.check(rc, "bc")
-        return d, e[: n - 1], tau, (V, vld)
-
-    def stedc(self, d, e, cols=None):
-        """Device divide and conquer on (d, e) device tensors -> (lam host, Q_d device); with
-        cols = (c0, c1) only those eigenvector columns are formed (the rest stays zero)."""
-        n = d.shape[0]
-        dd = d.clone()
-        ee = e.clone() if n > 1 else torch.zeros(1, dtype=torch.float64, device=self.device)
-        Q = torch.empty((n, n), dtype=torch.float64, device=self.device)
-        ws = torch.empty(self.L.pevd_stedc_workspace_bytes(n), dtype=torch.uint8, device=self.device)
-        if cols is None:
-            rc = self.L.pevd_stedc(n, self._p(dd), self._p(ee), self._p(Q), n, self._p(ws),
-                                   self._stream())
-        else:
-            rc = self.L.pevd_stedc_cols(n, self._p(dd), self._p(ee), self._p(Q), n, int(cols[0]),
-                                        int(cols[1]), self._p(ws), self._stream())
-        if rc == self._lib.PEVD_ERR_CONVERGE:
-            raise RuntimeError(self.L.pevd_last_error().decode())
-        self._lib.check(rc, "stedc")
-        return dd.cpu().numpy(), Q
-
-    def bc_back_left(self, n, b, tau, Vpack, X):
-        """X (column-major n x cols device tensor) <- Q_b X in place (conventional BC-Back)."""
-        V, vld = Vpack
-        cols = X.shape[0]
-        ws = torch.empty(self.L.pevd_bc_back_workspace_bytes(n, cols), dtype=torch.uint8,
-                         device=self.device)
-        rc = self.L.pevd_bc_back_left(n, b, self._p(tau), self._p(V), vld, self._p(X),
-                                      X.stride(0), cols, self._p(ws), self._stream())
-        self._lib.check(rc, "bc_back_left")
-        return X
-
-    def bc_back_right(self, n, b, tau, Vpack, X):
-        """X (column-major rows x n device tensor) <- X Q_b in place."""
-        V, vld = Vpack
-        rows = X.shape[1]
-        ws = torch.empty(self.L.pevd_bc_back_workspace_bytes(n, rows), dtype=torch.uint8,
-                         device=self.device)
-        rc = self.L.pevd_bc_back_right(n, b, self._p(tau), self._p(V), vld, self._p(X),
-                                       X.stride(0), rows, self._p(ws), self._stream())
-        self._lib.check(rc, "bc_back_right")
-        return X
 
 
 # ----------------------------------------------------------------------------------------------
@@ -171,6 +59,16 @@ def _recv(t, src, group):
         t.copy_(h)
     else:
         dist.recv(t, src=src, group=group)
+
+
+def _p2p(t, src, dst, group):
+    """Point to point src -> dst; returns the received tensor on dst (t elsewhere)."""
+    rank = dist.get_rank(group)
+    if rank == src:
+        _send(t.contiguous(), dst, group)
+    elif rank == dst:
+        _recv(t, src, group)
+    return t
 
 
 def _bcast(t, src, group):
@@ -232,17 +130,135 @@ def _aggregate(ops, group, n):
     return t0, Y, T
 
 
+# ----------------------------------------------------------------------------------------------
+# production: the C++ per-rank orchestrator over NCCL
+
+
+_COMMS: dict = {}
+
+
+def nccl_comm(group=None):
+    """This rank's NCCL communicator for pevd_dist_syevd (created once per process group from a
+    unique id that rank 0 shares through the group)."""
+    import ctypes
+    from . import _lib
+    L = _lib.load()
+    rank, G = dist.get_rank(group), dist.get_world_size(group)
+    key = (id(group), rank, G, torch.cuda.current_device())
+    if key not in _COMMS:
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _lib.check(L.pevd_nccl_unique_id(uid), "nccl unique id")
+        box = [bytes(uid.raw)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        h = ctypes.c_void_p()
+        _lib.check(L.pevd_comm_nccl_create(rank, G, box[0], ctypes.byref(h)), "nccl comm")
+        _COMMS[key] = h
+    return _COMMS[key]
+
+
+def _gather_outputs(st, group):
+    """Every rank's events / messages / flops, merged into the run's TraceEvents, measured
+    CommLedger and executed FlopCounter (the same on every rank)."""
+    from . import _lib
+    mine = {"t0": float(st.t0_mono_ns),
+            "events": [(e.worker, e.stage, e.block, e.t_start_ms, e.t_end_ms, e.words)
+                       for e in st.events[:min(int(st.n_events), int(st.events_cap))]],
+            "msgs": [(m.src, m.dst, m.stage, m.words)
+                     for m in st.msgs[:min(int(st.n_msgs), int(st.msgs_cap))]],
+            "flops": list(st.stages.flops)}
+    G = dist.get_world_size(group)
+    allp = [None] * G
+    dist.all_gather_object(allp, mine, group=group)
+    from .core import FlopCounter
+    trace, ledger, counter = TraceLog(), CommLedger(), FlopCounter()
+    for p in allp:
+        for (w, sg, blk, t0, t1, words) in p["events"]:
+            trace.add(w, _lib.TRACE_STAGES[sg], blk, int(round(p["t0"] + t0 * 1e6)),
+                      int(round(p["t0"] + t1 * 1e6)), words)
+        for (src, dst, sg, words) in p["msgs"]:
+            ledger.record(src, dst, _lib.LEDGER_STAGES[sg], words)
+        for k, name in enumerate(_lib.FLOP_STAGES):
+            if p["flops"][k] > 0:
+                counter.add(name, int(round(p["flops"][k] / 2)))
+    return trace, ledger, counter
+
+
+def _run_device(a, cfg, group, n, gather_q):
+    """pevd_dist_syevd on this rank's GPU (csrc/dist.cu) over NCCL."""
+    import ctypes
+    from . import _lib
+    from .pipeline import back_ranges
+    torch_ = _lib.require_cuda()
+    L = _lib.load()
+    rank, G = dist.get_rank(group), dist.get_world_size(group)
+    if callable(a):
+        dense = None
+        assert n is not None
+    else:
+        dense = a.data if isinstance(a, SymmetricMatrix) else \
+            SymmetricMatrix.from_dense(np.asarray(a, dtype=np.float64)).data
+        n = dense.shape[0]
+    b = min(cfg.b, n - 1)
+    if b > 32:
+        raise ValueError(f"bandwidth b={b} > 32 is not supported by the device kernels")
+    cols = partition(n, G)
+    backs = back_ranges(n, G, cfg.back_skew)
+    c0w, c1w = cols[rank]
+    r0, r1 = backs[rank]
+    dev = torch_.device("cuda", torch_.cuda.current_device())
+    if dense is None:
+        blk = a(c0w, c1w)              # (w, n): column-major n x w
+    else:
+        blk = torch_.from_numpy(np.ascontiguousarray(dense[:, c0w:c1w].T)).to(dev)
+    lam = torch_.empty(n, dtype=torch_.float64, device=dev)
+    nb = r1 - r0
+    qpart = torch_.empty((max(nb, 1), n), dtype=torch_.float64, device=dev) \
+        if cfg.want_vectors else None
+    col_lo = (ctypes.c_int64 * (G + 1))(*([lo for lo, _ in cols] + [n]))
+    back_lo = (ctypes.c_int64 * (G + 1))(*([lo for lo, _ in backs] + [n]))
+    st = _lib.new_dist_stats()
+    comm = nccl_comm(group)
+    P = ctypes.c_void_p
+    rc = L.pevd_dist_syevd(comm, n, b, P(blk.data_ptr()), blk.stride(0), col_lo, back_lo,
+                           P(lam.data_ptr()), P(qpart.data_ptr()) if qpart is not None else None,
+                           n, int(cfg.want_vectors), _lib.ORDER_CODES[cfg.order],
+                           P(torch_.cuda.current_stream().cuda_stream), ctypes.byref(st))
+    if rc == _lib.PEVD_ERR_CONVERGE:
+        raise RuntimeError(L.pevd_last_error().decode())
+    _lib.check(rc, f"rank {rank}: pevd_dist_syevd")
+    trace, ledger, counter = _gather_outputs(st, group)
+    info = {"counter": counter, "stats": st, "cols": (c0w, c1w), "back": (r0, r1),
+            "q_part": qpart}
+    res = EigenResult(lam=lam.cpu().numpy())
+    if cfg.want_vectors and gather_q:
+        # (n x nb column-major slabs: Fortran-order columns in conventional order, C-order rows
+        #  otherwise) all-gathered over the NCCL process group
+        sizes = [hi - lo for lo, hi in backs]
+        full = _allgather_uneven(qpart[:nb], sizes, group, (n,))
+        for w in range(G):
+            ledger.record(w, HOST, "Result", sizes[w] * n)
+        qh = full.cpu().numpy()
+        res = EigenResult(lam=res.lam, Q=np.asfortranarray(qh.T) if cfg.order == "conventional"
+                          else np.ascontiguousarray(qh), vectors_computed=True)
+    return res, trace.events(), ledger, info
+
+
 def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
     """Blockwise multi-process EVD.
 
     `a` is either the full matrix (every rank passes the same one; validated like the reference)
     or, for device-resident runs, a callable ``a(c0, c1)`` returning this rank's column block as
     a column-major device tensor of shape (c1 - c0, n) (then `n` must be given).  Every rank gets
-    the eigenvalues; with gather_q the full Q (C order) too, else only its row block.
+    the eigenvalues; with gather_q the full Q too.
+
+    ops=None: the production path on this rank's GPU (csrc/dist.cu over NCCL).  With a compute
+    object (tests/cpu_ops.py) the same protocol runs host-side in Python (gloo, CPU tests).
 
     Returns (EigenResult, events, ledger, info dict)."""
     if ops is None:
-        ops = CudaOps()
+        return _run_device(a, cfg, group, n, gather_q)
+
     rank = dist.get_rank(group)
     G = dist.get_world_size(group)
     if callable(a):
@@ -275,50 +291,50 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
     panels = []  # (c0, pw, t0, Y (pw, m) col-major, T (pw, pw))
     t_sbr0 = now()
 
+    sbr_span = [None, None]   # the rounds this rank owns (its trace SBR event)
+
     def factor(c0, pw, t0):
-        """Gather the panel at its owner (pieces of straddling panels, C2), factor it there,
-        return the R pieces (C3) and broadcast the factor (C4).  Returns (Y, T)."""
+        """The panel's straddling pieces are all-gathered, its owner factors it and broadcasts
+        [W | Y | T | R] (booked as the reference books (W, Y), pipeline.py:236, plus T, R);
+        every rank owning panel columns writes [R; 0] into them.  Returns (Y, W, T)."""
         m = n - t0
         owner = owner_of(c0)
+        if rank == owner and sbr_span[0] is None:
+            sbr_span[0] = now()
+        ov = [max(0, min(c0 + pw, ranges[x][1]) - max(c0, ranges[x][0])) for x in range(G)]
+        plo, phi = max(c0, c0w), min(c0 + pw, c1w)
+        if ov[owner] < pw:  # straddling panel
+            for x in range(G):
+                if ov[x]:
+                    ledger.record(x, BROADCAST, "SBR-panel", ov[x] * m)
+            mine = blk[plo - c0w: phi - c0w, t0:] if plo < phi else \
+                torch.zeros((0, m), dtype=torch.float64, device=blk.device)
+            P = _allgather_uneven(mine.contiguous(), ov, group, (m,))
+        elif rank == owner:
+            P = blk[c0 - c0w: c0 + pw - c0w, t0:]
+        buf = torch.empty(2 * m * pw + 2 * pw * pw, dtype=torch.float64, device=blk.device)
         if rank == owner:
-            P = ops.zeros(m, pw)
-            hi = min(c0 + pw, c1w)
-            P[: hi - c0] = blk[c0 - c0w: hi - c0w, t0:]
-        for x in range(G):
-            xlo, xhi = max(c0, ranges[x][0]), min(c0 + pw, ranges[x][1])
-            if x == owner or xlo >= xhi:
-                continue
-            ledger.record(x, owner, "SBR-panel", (xhi - xlo) * m)
-            if rank == x:
-                _send(blk[xlo - c0w: xhi - c0w, t0:].contiguous(), owner, group)
-            elif rank == owner:
-                piece = torch.empty((xhi - xlo, m), dtype=torch.float64, device=blk.device)
-                _recv(piece, x, group)
-                P[xlo - c0: xhi - c0] = piece
-        if rank == owner:
-            R, Y, T = ops.panel_qr(P)
+            R, Y, T = ops.panel_qr(P.contiguous() if ov[owner] < pw else P.clone())
+            W = ops.zeros(m, pw)
+            ops.gemm(Y, T, W)
+            buf[: m * pw] = W.reshape(-1)
+            buf[m * pw: 2 * m * pw] = Y.reshape(-1)
+            buf[2 * m * pw: 2 * m * pw + pw * pw] = T.reshape(-1)
+            buf[2 * m * pw + pw * pw:] = R.reshape(-1)
+        ledger.record(owner, BROADCAST, "SBR", 2 * m * pw)        # every rank books every message
+        ledger.record(owner, BROADCAST, "SBR-panel", 2 * pw * pw)
+        _bcast(buf, owner, group)
+        W = buf[: m * pw].reshape(pw, m)
+        Y = buf[m * pw: 2 * m * pw].reshape(pw, m)
+        T = buf[2 * m * pw: 2 * m * pw + pw * pw].reshape(pw, pw)
+        R = buf[2 * m * pw + pw * pw:].reshape(pw, pw)
+        if plo < phi:
             Rfull = torch.zeros((pw, m), dtype=torch.float64, device=blk.device)
             Rfull[:, :pw] = R  # panel rows t0.. become [R; 0]
-            hi = min(c0 + pw, c1w)
-            blk[c0 - c0w: hi - c0w, t0:] = Rfull[: hi - c0]
-        else:
-            Y = torch.empty((pw, m), dtype=torch.float64, device=blk.device)
-            T = torch.empty((pw, pw), dtype=torch.float64, device=blk.device)
-        for x in range(G):
-            xlo, xhi = max(c0, ranges[x][0]), min(c0 + pw, ranges[x][1])
-            if x == owner or xlo >= xhi:
-                continue
-            ledger.record(owner, x, "SBR-panel", (xhi - xlo) * m)
-            if rank == owner:
-                _send(Rfull[xlo - c0: xhi - c0].contiguous(), x, group)
-            elif rank == x:
-                piece = torch.empty((xhi - xlo, m), dtype=torch.float64, device=blk.device)
-                _recv(piece, owner, group)
-                blk[xlo - c0w: xhi - c0w, t0:] = piece
-        _bcast(Y, owner, group)
-        _bcast(T, owner, group)
-        ledger.record(owner, BROADCAST, "SBR", 2 * m * pw)  # the reference ships (W, Y)
-        return Y, T
+            blk[plo - c0w: phi - c0w, t0:] = Rfull[plo - c0: phi - c0]
+        if rank == owner:
+            sbr_span[1] = now()
+        return Y, W, T
 
     def form_z(t0, pw, Y, W, corr=None):
         """A W from our columns by symmetry (C5; `corr` subtracts the block's pending
@@ -351,9 +367,7 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
         c0, pw, t0 = sched[x]
         if pw < b:
             # ---- the ragged last round, one panel (sbr.py:175-182) ----
-            Y, T = factor(c0, pw, t0)
-            W = ops.zeros(n - t0, pw)
-            ops.gemm(Y, T, W)  # W = Y T
+            Y, W, T = factor(c0, pw, t0)
             Z = form_z(t0, pw, Y, W)
             rlo = max(t0, c0w)
             if rlo < c1w:   # two-sided update of our columns (rows t0..n)
@@ -389,9 +403,7 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
                 if lo < hi:
                     ops.gemm(P1[: 2 * ri, ri - b:], P2[: 2 * ri, lo - t0: hi - t0],
                              blk[lo - c0w: hi - c0w, ci:], alpha=-1.0, beta=1.0, tb=True)
-            Y, T = factor(ci, b, ti)
-            W = ops.zeros(n - ti, b)
-            ops.gemm(Y, T, W)
+            Y, W, T = factor(ci, b, ti)
             corr = None
             if i:
                 tv = ops.zeros(2 * ri, b)
@@ -413,9 +425,10 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
             ops.gemm(P1[:, ru:], P2[:, lo - t0: c1w - t0], blk[lo - c0w:, tl:], alpha=-1.0,
                      beta=1.0, tb=True)
         x += nbl
-    trace.add(rank, "SBR", rank, t_sbr0, now())
+    if sbr_span[0] is not None:
+        trace.add(rank, "SBR", rank, sbr_span[0], sbr_span[1])
 
-    # ---- band: our columns' diagonals, all-gathered (replaces C6/C7) ----
+    # ---- band pieces to rank 0 (BandStage) ----
     width = c1w - c0w
     own_bands = torch.zeros((width, b + 1), dtype=torch.float64, device=blk.device)
     for d in range(b + 1):
@@ -424,24 +437,61 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
             j = torch.arange(nv, device=blk.device)
             own_bands[:nv, d] = blk[j, c0w + d + j]
     counts = [hi - lo for lo, hi in ranges]
+    for w in range(1, G):
+        ledger.record(w, 0, "BandStage", (b + 1) * counts[w])
     bands_rows = _allgather_uneven(own_bands, counts, group, (b + 1,))  # (n, b+1)
-    for w in range(G):
-        ledger.record(w, HOST, "BandStage", (b + 1) * counts[w])
     bands = bands_rows.t().contiguous()                                # (b+1, n)
-    # ---- BC on every rank (deterministic wavefront chase) ----
-    t_bc = now()
-    d, e, tau, V = ops.bc(bands)
-    trace.add(rank, "BC", rank, t_bc, now())
-    for w in range(G - 1):
-        ledger.record(w, w + 1, "BC", 2 * b * b)  # the overlap-block hand-off of the relay
+    # ---- the relayed chase (bulge.py:348-385): rank x chases the sweeps of its columns down
+    #      the remaining band and hands the overlap block and the tail to rank x + 1 ----
+    tail = bands if rank == 0 else None
+    parts = None
+    for x in range(G):
+        c0x = ranges[x][0]
+        last = x == G - 1
+        pend = n if last else ranges[x + 1][0]
+        mr = n - pend
+        bwo = min(2 * b, max(mr - 1, 0))
+        if rank == x:
+            t_bc = now()
+            parts = ops.bc_partition(tail, b, c0x, pend, n)
+            trace.add(rank, "BC", rank, t_bc, now())
+        if not last:
+            ledger.record(x, x + 1, "BC", 2 * b * b)
+            ledger.record(x, x + 1, "BandStage", (bwo + 1) * mr)
+            shape = (bwo + 1, mr)
+            t = parts["tail"] if rank == x else torch.empty(shape, dtype=torch.float64)
+            t = _p2p(t, x, x + 1, group)
+            if rank == x + 1:
+                tail = t
+    # tridiagonal pieces and reflector sets to every rank
+    dcnt = [(n if x == G - 1 else ranges[x + 1][0]) - ranges[x][0] for x in range(G)]
+    ecnt = [min(ranges[x][0] + dcnt[x], n - 1) - ranges[x][0] for x in range(G)]
+    for x in range(G):
+        ledger.record(x, BROADCAST, "Gather", dcnt[x])
+        ledger.record(x, BROADCAST, "Gather", ecnt[x])
+    d = _allgather_uneven(torch.as_tensor(parts["d"]), dcnt, group, ()).numpy()
+    e = _allgather_uneven(torch.as_tensor(parts["e"]), ecnt, group, ()).numpy()
+    refl = None
+    if cfg.want_vectors:
+        sets = [None] * G
+        dist.all_gather_object(sets, parts["refl"], group=group)
+        vld = ((b + 7) // 8) * 8
+        for x in range(G):
+            ledger.record(x, BROADCAST, "U-gather", len(sets[x]["tau"]) * (1 + vld))
+        refl = ops.merge_reflectors(sets)
+    d = torch.as_tensor(d)
+    e = torch.as_tensor(e)
     # ---- solver ----
+    sizes = back_plan_sizes(n, G, cfg.back_skew)
+    bounds = np.cumsum([0] + sizes)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
     t_s = now()
-    # (conventional order: each rank forms only its own columns of Q_d)
+    # (conventional order: each rank forms only its own back columns of Q_d)
     if cfg.order == "conventional" and cfg.want_vectors:
-        lam, Qd = ops.stedc(d, e, cols=(c0w, c1w))
+        lam, Qd = ops.stedc(d, e, cols=(r0, r1))
     else:
-        lam, Qd = ops.stedc(d, e)  # lam on the host, Q_d column-major (device for CudaOps)
-    trace.add(HOST, "Solver", 0, t_s, now())
+        lam, Qd = ops.stedc(d, e)
+    trace.add(rank, "Solver", rank, t_s, now())
     if not cfg.want_vectors:
         return EigenResult(lam=lam), trace.events(), ledger, {}
     if cfg.order == "conventional":
@@ -449,8 +499,8 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
         #      already holds Q_d, the bulge reflectors and the SBR panels, so the column blocks
         #      are independent: no Q_d / U broadcasts, no final GEMM (pipeline.py:367-387) ----
         t_bb = now()
-        X = Qd[c0w:c1w].clone()                       # column-major n x (c1w - c0w)
-        X = ops.bc_back_left(n, b, tau, V, X)         # Q_b X
+        X = Qd[r0:r1].clone()                         # column-major n x (r1 - r0)
+        X = ops.bc_back_left(n, b, refl, None, X)     # Q_b X
         trace.add(rank, "BC-Back", rank, t_bb, now())
         t_sb = now()
         groups = [panels[g0:g0 + SBR_BACK_AGG] for g0 in range(0, len(panels), SBR_BACK_AGG)]
@@ -458,26 +508,22 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
             t0, Yg, Tg = _aggregate(ops, grp, n)
             K = Tg.shape[0]
             X2 = X[:, t0:]                            # rows t0.. of our columns
-            P1 = ops.zeros(K, c1w - c0w)
+            P1 = ops.zeros(K, r1 - r0)
             ops.gemm(Yg, X2, P1, ta=True)             # Y^T X
-            P2 = ops.zeros(K, c1w - c0w)
+            P2 = ops.zeros(K, r1 - r0)
             ops.gemm(Tg, P1, P2)                      # T (Y^T X)
             ops.gemm(Yg, P2, X2, alpha=-1.0, beta=1.0)  # X -= Y T Y^T X
         trace.add(rank, "SBR-Back", rank, t_sb, now())
         if not gather_q:
             return (EigenResult(lam=lam), trace.events(), ledger,
-                    {"cols": (c0w, c1w), "q_cols": X})
-        counts = [hi - lo for lo, hi in ranges]
-        Qc = _allgather_uneven(X, counts, group, (n,))   # (n cols, n rows): column-major Q
+                    {"cols": (r0, r1), "q_cols": X})
+        Qc = _allgather_uneven(X, sizes, group, (n,))    # (n cols, n rows): column-major Q
         for w in range(G):
-            ledger.record(w, HOST, "Result", counts[w] * n)
+            ledger.record(w, HOST, "Result", sizes[w] * n)
         return (EigenResult(lam=lam, Q=np.asfortranarray(Qc.cpu().numpy().T),
                             vectors_computed=True),
-                trace.events(), ledger, {"cols": (c0w, c1w)})
+                trace.events(), ledger, {"cols": (r0, r1)})
     # ---- back transformation of our rows ----
-    sizes = back_plan_sizes(n, G, cfg.back_skew)
-    bounds = np.cumsum([0] + sizes)
-    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
     t_sb = now()
     Mt = ops.zeros(r1 - r0, n)               # column-major (r x n): rows r0..r1 of I
     ir = torch.arange(r1 - r0, device=Mt.device)
@@ -491,10 +537,11 @@ def run_distributed(a, cfg, ops=None, group=None, n=None, gather_q=True):
         P2 = ops.zeros(r1 - r0, K)
         ops.gemm(P1, Tg, P2)                  # (M Y) T
         ops.gemm(P2, Yg, Ms, alpha=-1.0, beta=1.0, tb=True)  # -= (M Y T) Y^T
-    trace.add(rank, "SBR-Back", rank, t_sb, now())
+    trace.add(HOST if cfg.order == "pipelined" else rank, "SBR-Back", rank, t_sb, now())
     t_bb = now()
-    Msb = ops.bc_back_right(n, b, tau, V, Mt)   # rows of Q_s Q_b (in place)
-    trace.add(rank, "BC-Back", rank, t_bb, now())
+    Msb = ops.bc_back_right(n, b, refl, None, Mt)   # rows of Q_s Q_b (in place)
+    trace.add(HOST if cfg.order == "pipelined" else rank, "BC-Back", rank, t_bb, now())
+    dist.barrier(group)  # Q_d complete everywhere before any final multiply (dist.cu does the same)
     t_f = now()
     Qrows_t = ops.zeros(r1 - r0, n)
     ops.gemm(Msb, Qd, Qrows_t)

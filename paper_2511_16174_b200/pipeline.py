@@ -8,13 +8,21 @@ reflectors applied to Q_d from the left ("conventional").  The returned 4-tuple 
 reference's contract: EigenResult, time-sorted TraceEvents (device CUDA-event stage times),
 CommLedger, FlopCounter (MACs).
 
-Trace lanes: worker 0 is the main stream (SBR, BC, Solver, FinalMultiply); the back-transform
-stream (SBR-Back, BC-Back), which overlaps the chase and the solver, is reported as the
-concurrent helper lane HOST (-1), the role the reference's host thread plays.
+Workers: workers = 1 runs the fused single-GPU orchestrator.  workers = G > 1 runs the paper's
+blockwise protocol over G cooperating devices -- in this process (pevd_syevd_multi: one host
+thread per worker, peer-to-peer copies over NVLink; workers map round-robin onto the visible
+GPUs, so a 1-GPU box runs G workers on one device) or, under torchrun, one process per GPU over
+NCCL (distributed.py).
 
-Ledger: one GPU moves no messages; the ledger records the words the reference's blockwise
-protocol exchanges between `cfg.workers` devices (pipeline.py:236-502), so analytic checks
-(schedule.comm_broadcast_words, 2 b^2 per BC boundary) hold for any worker count.
+Trace lanes: a worker's main stream (SBR rounds it owns, its BC partition, Solver,
+FinalMultiply; Comm spans on its comm stream); the back-transform stream, which overlaps the
+chase and the solver in pipelined order, is the concurrent helper lane HOST (-1), the role the
+reference's host thread plays.
+
+Ledger and counter are MEASURED: every message is booked with the words actually handed to the
+transport (schedule.protocol_ledger states them in closed form; the SBR words equal
+comm_broadcast_words and each BC boundary carries one 2b x b overlap block, as in the
+reference), and the FlopCounter holds the executed multiply-adds per stage (PevdStats.flops).
 """
 from __future__ import annotations
 
@@ -26,8 +34,7 @@ import numpy as np
 from . import _lib
 from .core import EigenResult, FlopCounter, SymmetricMatrix
 from .messaging import BROADCAST, HOST, CommLedger, TraceLog
-from .schedule import (back_plan_sizes, bc_back_macs, bc_back_macs_fast, bc_macs, bc_macs_fast,
-                       partition, round_schedule, sbr_macs)
+from .schedule import back_plan_sizes, partition
 
 ORDERS = ("pipelined", "sequential", "conventional")
 
@@ -59,48 +66,45 @@ class PipelineConfig:
             raise ValueError(f"back_skew {self.back_skew} outside [0, 0.05]")
 
 
-def _ledger_for(n: int, b: int, cfg: PipelineConfig, nref: int) -> CommLedger:
-    """Words of the blockwise protocol for cfg.workers devices (pipeline.py:236-502)."""
-    led = CommLedger()
-    W = cfg.workers
-    if b < 1:
-        return led
-    ranges = partition(n, W)
-    owner = [next(w for w, (lo, hi) in enumerate(ranges) if lo <= c0 < hi)
-             for c0, _, _ in round_schedule(n, b)]
-    for idx, (c0, pw, t0) in enumerate(round_schedule(n, b)):
-        m = n - t0
-        led.record(owner[idx], BROADCAST, "SBR", 2 * m * pw)     # ("wy", idx): W and Y
-        for x, (lo, hi) in enumerate(ranges):
-            rlo = max(t0, lo)
-            if rlo < hi:
-                led.record(x, BROADCAST, "SBR", (hi - rlo) * pw)  # ("aw", idx) row block
-    for w in range(W):
-        led.record(w, HOST, "BandStage", (b + 1) * (ranges[w][1] - ranges[w][0]))
-    for w in range(W - 1):
-        led.record(w, w + 1, "BC", 2 * b * b)                   # the 2b x b overlap block
-    if cfg.want_vectors:
-        stride = ((b + 7) // 8) * 8
-        led.record(HOST, BROADCAST, "U-gather", 4 * nref + nref + nref * stride)
-        if cfg.order != "conventional":
-            led.record(HOST, BROADCAST, "Qd", n * n)
-    return led
+def dist_outputs(stats, workers: int):
+    """TraceEvents, the measured CommLedger and the executed-flop FlopCounter (MACs) of a
+    distributed run, from the per-rank PevdDistStats (pevd.h).  Event times are CLOCK_MONOTONIC
+    ns (time.perf_counter_ns's clock): each rank's t0 is taken after a barrier of all ranks."""
+    trace, ledger, counter = TraceLog(), CommLedger(), FlopCounter()
+    for st in stats:
+        t0 = float(st.t0_mono_ns)
+        for i in range(min(int(st.n_events), int(st.events_cap))):
+            e = st.events[i]
+            trace.add(e.worker, _lib.TRACE_STAGES[e.stage], e.block,
+                      int(round(t0 + e.t_start_ms * 1e6)), int(round(t0 + e.t_end_ms * 1e6)),
+                      e.words)
+        for i in range(min(int(st.n_msgs), int(st.msgs_cap))):
+            m = st.msgs[i]
+            ledger.record(m.src, m.dst, _lib.LEDGER_STAGES[m.stage], m.words)
+        for k, name in enumerate(_lib.FLOP_STAGES):
+            if st.stages.flops[k] > 0:
+                counter.add(name, int(round(st.stages.flops[k] / 2)))
+    return trace, ledger, counter
 
 
-def _macs(n: int, b: int, cfg: PipelineConfig) -> FlopCounter:
+def _macs(st) -> FlopCounter:
+    """Executed multiply-adds per stage of a single-GPU run (PevdStats.flops / 2)."""
     c = FlopCounter()
-    if n < 2 or b < 1:
-        return c
-    c.add("SBR", sbr_macs(n, b))
-    c.add("BC", bc_macs(n, b) if n <= 4096 else bc_macs_fast(n, b))
-    # D&C merge GEMMs without deflation: sum over levels of (n1^2 + n2^2) s ~ (2/3) n^3 MACs
-    c.add("Solver", max(1, (2 * n ** 3) // 3))
-    if cfg.want_vectors:
-        c.add("SBR-Back", max(1, (2 * n ** 3) // 3))
-        c.add("BC-Back", bc_back_macs(n, b, n) if n <= 2048 else bc_back_macs_fast(n, b, n))
-        if cfg.order != "conventional":
-            c.add("FinalMultiply", n ** 3)
+    for k, name in enumerate(_lib.FLOP_STAGES):
+        if st.flops[k] > 0:
+            c.add(name, int(round(st.flops[k] / 2)))
     return c
+
+
+def back_ranges(n: int, workers: int, back_skew: float):
+    """Row (pipelined / sequential) or column (conventional) blocks of the back transform
+    (pipeline.py:97-102, backtrans.py:108-121)."""
+    sizes = back_plan_sizes(n, workers, back_skew)
+    out, at = [], 0
+    for s in sizes:
+        out.append((at, at + s))
+        at += s
+    return out
 
 
 def run(a, cfg: PipelineConfig):
@@ -114,17 +118,21 @@ def run(a, cfg: PipelineConfig):
     b = min(cfg.b, n - 1) if n > 1 else 0
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1 and n > 2:
-        # one process per GPU: the blockwise protocol (distributed.py)
+        # one process per GPU (torchrun): every rank runs the C++ per-rank orchestrator over NCCL
+        if cfg.workers != dist.get_world_size():
+            raise ValueError(f"PipelineConfig.workers={cfg.workers} but the process group has "
+                             f"{dist.get_world_size()} ranks (one worker per rank)")
         from .distributed import run_distributed
-        from .core import FlopCounter as _FC
-        res, events, ledger, _ = run_distributed(dense, cfg)
+        res, events, ledger, info = run_distributed(dense, cfg)
         if cfg.trace_path:
             log = TraceLog()
             for ev in events:
                 log.add(ev.worker, ev.stage, ev.block, ev.t_start, ev.t_end, ev.words)
             log.to_ndjson(cfg.trace_path)
-        return res, events, ledger, _macs(n, b, cfg)
+        return res, events, ledger, info["counter"]
     from . import device  # imports torch lazily; fails loudly without CUDA / libpevd.so
+    if cfg.workers > 1 and n >= 3:
+        return _run_multi(dense, n, b, cfg, device)
     t0 = time.perf_counter_ns()
     try:
         lam, q, st = device.syevd(dense, max(b, 1), cfg.want_vectors, cfg.order)
@@ -145,15 +153,40 @@ def run(a, cfg: PipelineConfig):
             trace.add(back, "SBR-Back", 0, ns(st.sbr_back_ms[0]), ns(st.sbr_back_ms[1]))
             trace.add(back, "BC-Back", 0, ns(st.bc_back_ms[0]), ns(st.bc_back_ms[1]))
             trace.add(0, "FinalMultiply", 0, ns(st.final_ms[0]), ns(st.final_ms[1]))
-    nref = int(st.n_reflectors)
-    ledger = _ledger_for(n, b, cfg, nref) if n > 1 else CommLedger()
-    counter = _macs(n, b, cfg)
+    ledger = CommLedger()  # one GPU: nothing moves between devices
+    counter = _macs(st)
     result = EigenResult(lam=lam, Q=q if cfg.want_vectors else None,
                          vectors_computed=bool(cfg.want_vectors))
     if cfg.want_vectors and cfg.order == "conventional":
         result.Q = np.asfortranarray(result.Q)
     elif cfg.want_vectors:
         result.Q = np.ascontiguousarray(result.Q)  # pipeline.py:503 (C order)
+    if cfg.trace_path:
+        trace.to_ndjson(cfg.trace_path)
+    return result, trace.events(), ledger, counter
+
+
+def _run_multi(dense, n: int, b: int, cfg: PipelineConfig, device):
+    """cfg.workers cooperating devices in this process (pevd_syevd_multi): the blockwise
+    protocol with one host thread per worker and peer-to-peer transfers.  Workers map
+    round-robin onto the visible GPUs; on a box with fewer GPUs than workers several workers
+    share one device (the same protocol and messages, without the extra parallelism)."""
+    if b > 32:
+        raise ValueError(f"bandwidth b={b} > 32 is not supported by the device kernels")
+    cols = partition(n, cfg.workers)
+    backs = back_ranges(n, cfg.workers, cfg.back_skew)
+    try:
+        lam, q, stats = device.syevd_multi(dense, cfg.workers, max(b, 1), cols, backs,
+                                           cfg.want_vectors, cfg.order)
+    except ValueError:
+        raise
+    except RuntimeError as exc:
+        if "did not converge" in str(exc):
+            raise
+        raise PipelineError(f"distributed EVD failed: {exc}") from exc
+    trace, ledger, counter = dist_outputs(stats, cfg.workers)
+    result = EigenResult(lam=lam, Q=q if cfg.want_vectors else None,
+                         vectors_computed=bool(cfg.want_vectors))
     if cfg.trace_path:
         trace.to_ndjson(cfg.trace_path)
     return result, trace.events(), ledger, counter
@@ -179,12 +212,7 @@ def run_auto_skew(a, cfg: PipelineConfig):
 
 def back_rows(n: int, cfg: PipelineConfig):
     """Row blocks of the back transform per worker (pipeline.py:97-102)."""
-    sizes = back_plan_sizes(n, cfg.workers, cfg.back_skew)
-    out, at = [], 0
-    for s in sizes:
-        out.append((at, at + s))
-        at += s
-    return out
+    return back_ranges(n, cfg.workers, cfg.back_skew)
 
 
 __all__ = ["PipelineConfig", "PipelineError", "run", "run_auto_skew", "ORDERS", "_lib"]

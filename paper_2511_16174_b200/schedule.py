@@ -249,3 +249,61 @@ def mean_idle_fraction(events, workers: int) -> float:
         return 0.0
     return sum(1.0 - sum(e.duration for e in spans if e.worker == w) / (t1 - t0)
                for w in range(workers)) / workers
+
+
+# ------------------------------------------------------------------ the measured protocol
+def protocol_ledger(n: int, b: int, workers: int, want_vectors: bool = True,
+                    back_skew: float = 0.0, result: bool = True) -> list:
+    """Every message of the blockwise protocol (csrc/dist.cu, distributed.py) as
+    (src, dst, stage, words), in closed form from the schedule -- the ledger a run measures.
+    dst -1 = host, -2 = broadcast (messaging.py).  `result`: the Q slabs gathered to the caller.
+      SBR        per round: owner broadcasts (W, Y) 2 m pw (pipeline.py:236); every rank its
+                 A W row block (pipeline.py:251-271) -> sum = comm_broadcast_words(n, b)
+      SBR-panel  T and R of the factor (2 pw^2); straddling pieces (overlap x m per holder)
+      BandStage  band pieces to rank 0; the band tail rank x -> x + 1 ((bw + 1) x rest)
+      BC         the 2b x b overlap block rank x -> x + 1 (bulge.py:144-167)
+      Gather     each partition's d and e pieces
+      U-gather   each partition's reflectors, (1 + pad8(b)) words each
+      Result     the Q slab of each worker (n x back block)"""
+    G = workers
+    if G < 2:
+        return []  # one worker moves nothing between devices
+    ranges = partition(n, G)
+    msgs = []
+
+    def owner(c):
+        return next(x for x, (lo, hi) in enumerate(ranges) if lo <= c < hi)
+
+    for c0, pw, t0 in round_schedule(n, b):
+        m = n - t0
+        o = owner(c0)
+        ov = [max(0, min(c0 + pw, hi) - max(c0, lo)) for lo, hi in ranges]
+        if ov[o] < pw:
+            msgs += [(x, -2, "SBR-panel", ov[x] * m) for x in range(G) if ov[x]]
+        msgs.append((o, -2, "SBR", 2 * m * pw))
+        msgs.append((o, -2, "SBR-panel", 2 * pw * pw))
+        for x, (lo, hi) in enumerate(ranges):
+            c = hi - max(t0, lo)
+            if c > 0:
+                msgs.append((x, -2, "SBR", c * pw))
+    for x in range(1, G):
+        msgs.append((x, 0, "BandStage", (b + 1) * (ranges[x][1] - ranges[x][0])))
+    J = (n - 3) // b + 1 if n >= 3 else 0
+    vld = ((b + 7) // 8) * 8
+    for x in range(G):
+        c0 = ranges[x][0]
+        pend = n if x == G - 1 else ranges[x + 1][0]
+        if x < G - 1:
+            mr = n - pend
+            msgs.append((x, x + 1, "BC", 2 * b * b))
+            msgs.append((x, x + 1, "BandStage", (min(2 * b, max(mr - 1, 0)) + 1) * mr))
+        msgs.append((x, -2, "Gather", pend - c0))
+        msgs.append((x, -2, "Gather", min(pend, n - 1) - c0))
+        if want_vectors and G > 1:
+            npiv = pend - c0
+            cnt = sum(max(0, min(npiv, n - c0 - 2 - j * b)) for j in range(J))
+            msgs.append((x, -2, "U-gather", cnt * (1 + vld)))
+    if want_vectors and result:
+        for x, s in enumerate(back_plan_sizes(n, G, back_skew)):
+            msgs.append((x, -1, "Result", s * n))
+    return [m_ for m_ in msgs if m_[3] > 0]

@@ -38,8 +38,12 @@ def _worker(rank, world, port, n, b, seed, skew, out, order="pipelined"):
                                                                        back_skew=skew,
                                                                        order=order),
                                                     ops=CpuOps())
+        from paper_2511_16174_b200.schedule import validate_trace
+        validate_trace(events, world, ledger)
         out[rank] = (res.lam, res.Q, ledger.words(stage="SBR"), ledger.words(stage="BC"),
-                     ledger.messages(stage="BC"), info.get("rows", info.get("cols")))
+                     ledger.messages(stage="BC"), info.get("rows", info.get("cols")),
+                     {k: (ledger.words(stage=k), ledger.messages(stage=k))
+                      for k in ledger.stages()})
     finally:
         dist.destroy_process_group()
 
@@ -57,7 +61,10 @@ def _run(world, n, b, seed, skew=0.0, order="pipelined"):
                                                 (3, 91, 7, 0.0, "pipelined"),
                                                 (2, 150, 4, 0.0, "pipelined"),
                                                 (3, 91, 7, 0.0, "conventional"),
-                                                (2, 150, 4, 0.0, "conventional")])
+                                                (2, 150, 4, 0.0, "conventional"),
+                                                (4, 96, 8, 0.0, "pipelined"),
+                                                (4, 90, 8, 0.03, "conventional"),
+                                                (8, 160, 8, 0.0, "pipelined")])
 def test_blockwise_protocol_matches_oracle(world, n, b, skew, order):
     out = _run(world, n, b, seed=n + world, skew=skew, order=order)
     g = np.random.default_rng(n + world).standard_normal((n, n))
@@ -65,7 +72,7 @@ def test_blockwise_protocol_matches_oracle(world, n, b, skew, order):
     lam_o, _ = orc.evd(a, b, True)
     ref = out[0]
     for r in range(world):
-        lam, q, sbr_words, bc_words, bc_msgs, rows = out[r]
+        lam, q, sbr_words, bc_words, bc_msgs, rows, by_stage = out[r]
         # every rank returns the same full result
         np.testing.assert_array_equal(lam, ref[0])
         np.testing.assert_array_equal(q, ref[1])
@@ -76,6 +83,13 @@ def test_blockwise_protocol_matches_oracle(world, n, b, skew, order):
         from paper_2511_16174_b200 import comm_broadcast_words
         assert sbr_words == comm_broadcast_words(n, b)
         assert bc_words == (world - 1) * 2 * b * b and bc_msgs == world - 1
+        # the whole measured ledger = the protocol's closed form (schedule.protocol_ledger)
+        from paper_2511_16174_b200.schedule import protocol_ledger
+        want = {}
+        for (_, _, st, w) in protocol_ledger(n, b, world, True, skew):
+            wd, ms = want.get(st, (0, 0))
+            want[st] = (wd + w, ms + 1)
+        assert by_stage == want
     rows = [out[r][5] for r in range(world)]
     assert rows[0][0] == 0 and rows[-1][1] == n
     assert all(rows[i][1] == rows[i + 1][0] for i in range(world - 1))
