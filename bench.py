@@ -94,9 +94,13 @@ def run_b200(args):
     import torch.distributed as dist
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.blockwise:
         # one EVD over all ranks (csrc/dist.cu over NCCL); a failure is a failure, no fallback
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29513")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank,
+                                    world_size=world)
         return run_b200_distributed(args)
     return run_b200_single(args)
 
@@ -558,6 +562,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip the residual/orthogonality check")
     ap.add_argument("--no-same-n", action="store_true", help="skip the n=1024/4096 device runs")
+    ap.add_argument("--blockwise", action="store_true",
+                    help="run the distributed (csrc/dist.cu, NCCL) path even on one rank")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
