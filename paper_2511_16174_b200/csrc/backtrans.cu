@@ -458,221 +458,6 @@ __global__ void __launch_bounds__(WY_THREADS / RT, 2)
   }
 }
 
-// ------------------------------------------------------------ BC-Back, b = 32, DFMA (BLAS2)
-// The reference's own arithmetic (backtrans.py:252-274): every reflector applied on its own,
-// d = tau v^T x, x -= d v, with FP64 FMAs and no wasted work (the compact-WY DMMA kernel above
-// issues 1.25x the BLAS2 flops because a block of 8 staggered reflectors spans 40 columns).
-// One thread owns one row of X and a register window of FG + 32 columns (the FG sweeps of a
-// group at one chase step); the FG reflectors of the step are applied fully unrolled, so every
-// window index is static.  Between steps the window slides by b = 32: the 32 columns that no
-// later step of the group touches are stored, 32 new ones (prefetched into shared memory by
-// cp.async during the step, like the step's V and tau) come in.  X column-major (a 32-row warp
-// moves 256 contiguous bytes per column).  Work units (128-row block, sweep group) are claimed
-// from an atomic counter with per-row-block progress flags, as in the DMMA kernel.
-constexpr int FMA_ROWS = 128;
-
-template <int FG>
-struct FmaSmem {
-  double v[2][FG][32];
-  double tau[2][FG];
-  double xn[32][FMA_ROWS];
-  int unit;
-};
-
-template <bool LEFT, int FG>
-__global__ void __launch_bounds__(FMA_ROWS, 2)
-    bc_back_fma_kernel(int64_t n, const double* __restrict__ tau, const double* __restrict__ V,
-                       double* X, int64_t ldx, int64_t nrows, int* counter, int* progress,
-                       int64_t nunits, int nrb) {
-  constexpr int B = 32, FW = FG + B, NT = FMA_ROWS;
-  extern __shared__ __align__(16) unsigned char fmaraw[];
-  FmaSmem<FG>& S = *reinterpret_cast<FmaSmem<FG>*>(fmaraw);
-  const int tid = threadIdx.x;
-  const int64_t nsw = n - 2;
-  const int64_t ngroups = (nsw + FG - 1) / FG;
-  // the step's FG reflectors (consecutive slots, 32 doubles each) and taus -> buffer `buf`
-  auto stage = [&](int buf, int64_t i0, int64_t j) {
-    const int64_t off = bc_slot_offset_dev(n, B, j) + i0;
-    const int64_t nvalid = n - 2 - j * B - i0;
-    const double* vsrc = V + off * 32;
-    for (int c = tid; c < FG * 16; c += NT) {  // 16-byte chunks
-      const bool ok = (c >> 4) < nvalid;
-      cp_async16(&S.v[buf][0][0] + 2 * c, ok ? vsrc + 2 * c : V, ok);
-    }
-    for (int t = tid; t < FG; t += NT) {
-      const bool ok = t < nvalid;
-      cp_async8(&S.tau[buf][t], ok ? tau + off + t : tau, ok);
-    }
-  };
-  for (;;) {
-    if (tid == 0) S.unit = atomicAdd(counter, 1);
-    __syncthreads();
-    const int64_t u = S.unit;
-    __syncthreads();
-    if (u >= nunits) break;
-    const int64_t seq = u / nrb;
-    const int64_t k = LEFT ? ngroups - 1 - seq : seq;
-    const int rb = (int)(u % nrb);
-    if (tid == 0 && ld_acquire(progress + rb) < (int)seq) {
-      unsigned ns = 64;
-      while (ld_acquire(progress + rb) < (int)seq) {
-        __nanosleep(ns);
-        if (ns < 1024) ns <<= 1;
-      }
-    }
-    const int64_t row = (int64_t)rb * NT + tid;
-    const bool active = row < nrows;
-    double* xr = X + (active ? row : 0);
-    const int64_t i0 = k * FG;
-    const int64_t jmax = (n - 3 - i0) / B;
-    int64_t j = LEFT ? 0 : jmax;
-    int64_t ws = i0 + 1 + j * B;  // window column 0
-    int buf = 0;
-    stage(0, i0, j);
-    cp_async_commit();
-    __syncthreads();  // progress acquired by tid 0 before anyone reads X
-    double x[FW];
-    {
-      const int nw0 = active ? (int)std::max<int64_t>(0, std::min<int64_t>(FW, n - ws)) : 0;
-      const double* src = xr + ws * ldx;
-#pragma unroll
-      for (int c = 0; c < FW; ++c, src += ldx) x[c] = (c < nw0) ? __ldcg(src) : 0.0;
-    }
-    cp_async_wait<0>();
-    __syncthreads();
-    for (int64_t jj = 0; jj <= jmax; ++jj) {
-      const bool more = jj < jmax;
-      const int64_t jn = LEFT ? j + 1 : j - 1;
-      if (more) {
-        stage(buf ^ 1, i0, jn);
-        // the 32 columns entering the window at the next step
-        const int64_t nb = LEFT ? ws + FW : ws - B;
-        const double* src = xr + nb * ldx;
-        const int nok = active ? (int)std::max<int64_t>(0, std::min<int64_t>(B, n - nb)) : 0;
-#pragma unroll
-        for (int c = 0; c < B; ++c, src += ldx) cp_async8(&S.xn[c][tid], c < nok ? src : X, c < nok);
-      }
-      cp_async_commit();
-      const double* vb = &S.v[buf][0][0];
-      const double* tb = &S.tau[buf][0];
-#pragma unroll
-      for (int tt = 0; tt < FG; ++tt) {
-        const int t = LEFT ? FG - 1 - tt : tt;
-        const double2* v2 = reinterpret_cast<const double2*>(vb + t * 32);
-        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const double2 a = v2[e / 2], c = v2[e / 2 + 1];
-          d0 = fma(x[t + e], a.x, d0);
-          d1 = fma(x[t + e + 1], a.y, d1);
-          d2 = fma(x[t + e + 2], c.x, d2);
-          d3 = fma(x[t + e + 3], c.y, d3);
-        }
-        const double dd = -tb[t] * ((d0 + d1) + (d2 + d3));
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const double2 a = v2[e / 2];
-          x[t + e] = fma(dd, a.x, x[t + e]);
-          x[t + e + 1] = fma(dd, a.y, x[t + e + 1]);
-        }
-      }
-      // slide: the columns no later step of this group touches are final
-      // (columns ws + c with c < nw exist; one pointer walks the columns)
-      const int nw = active ? (int)std::max<int64_t>(0, std::min<int64_t>(FW, n - ws)) : 0;
-      if (LEFT) {
-        double* dst = xr + ws * ldx;
-#pragma unroll
-        for (int c = 0; c < B; ++c, dst += ldx)
-          if (c < nw) *dst = x[c];
-      } else {
-        double* dst = xr + (ws + FG) * ldx;
-#pragma unroll
-        for (int c = FG; c < FW; ++c, dst += ldx)
-          if (c < nw) *dst = x[c];
-      }
-      cp_async_wait<0>();
-      if (more) {
-        if (LEFT) {
-#pragma unroll
-          for (int c = 0; c < FG; ++c) x[c] = x[c + B];
-#pragma unroll
-          for (int c = 0; c < B; ++c) x[FG + c] = S.xn[c][tid];
-        } else {
-#pragma unroll
-          for (int c = FW - 1; c >= B; --c) x[c] = x[c - B];
-#pragma unroll
-          for (int c = 0; c < B; ++c) x[c] = S.xn[c][tid];
-        }
-        ws += LEFT ? B : -B;
-        j = jn;
-      } else {
-        // the rest of the window is final too
-        if (LEFT) {
-          double* dst = xr + (ws + B) * ldx;
-#pragma unroll
-          for (int c = B; c < FW; ++c, dst += ldx)
-            if (c < nw) *dst = x[c];
-        } else {
-          double* dst = xr + ws * ldx;
-#pragma unroll
-          for (int c = 0; c < FG; ++c, dst += ldx)
-            if (c < nw) *dst = x[c];
-        }
-      }
-      buf ^= 1;
-      __syncthreads();  // every thread is done with this step's V before it is restaged
-    }
-    if (tid == 0) {
-      __threadfence();
-      st_release(progress + rb, (int)(seq + 1));
-    }
-  }
-}
-
-// PEVD_BCB_FMA: 1 = the DFMA kernel above, 0 = the DMMA compact-WY kernel
-int bcb_use_fma() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("PEVD_BCB_FMA");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
-constexpr int FMA_FG = 48;
-
-template <bool LEFT>
-int bc_back_fma_launch(cudaStream_t st, int64_t n, const double* tau, const double* V, double* X,
-                       int64_t ldx, int64_t nrows, void* ws) {
-  const int nrb = (int)cdiv(nrows, FMA_ROWS);
-  const int64_t ngroups = cdiv(n - 2, FMA_FG);
-  const int64_t nunits = ngroups * nrb;
-  int* counter = (int*)ws;
-  int* progress = counter + 32;
-  PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
-  flops_add(128.0 * (double)bc_num_reflectors(n, 32) * (double)nrows);  // 64 FMA per row each
-  auto kfn = bc_back_fma_kernel<LEFT, FMA_FG>;
-  const size_t smem = sizeof(FmaSmem<FMA_FG>);
-  static int attr_dev = -1;
-  int dev;
-  PEVD_CUDA(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    PEVD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_dev = dev;
-  }
-  int per_sm = 0;
-  PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, FMA_ROWS, smem));
-  if (per_sm < 1) {
-    set_error("bc_back (DFMA): persistent kernel cannot be resident");
-    return ERR_CUDA;
-  }
-  const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
-  kfn<<<(unsigned)grid, FMA_ROWS, smem, st>>>(n, tau, V, X, ldx, nrows, counter, progress, nunits,
-                                               nrb);
-  PEVD_LAUNCH_CHECK();
-  return OK;
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- SBR-Back (compact WY)
@@ -971,8 +756,6 @@ __global__ void wy_tofs_kernel(int64_t n, int64_t jcount, int64_t* tofs) {
 int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                   double* X, int64_t ldx, int64_t nrows, void* ws) {
   if (n < 3 || nrows <= 0 || b < 2) return OK;
-  if (b == 32 && vld == 32 && ws && bcb_use_fma())
-    return bc_back_fma_launch<false>(st, n, tau, V, X, ldx, nrows, ws);
   if (b == 32 && vld == 32 && ws) {  // DMMA compact-WY kernel (fully asynchronous)
     const int nrb = (int)cdiv(nrows, WY_ROWS);
     const int64_t ngroups = cdiv(n - 2, Q4_SG);
@@ -1093,10 +876,7 @@ int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const d
     set_error("bc_back_left_t: needs b = 32, vld = 32 and a workspace");
     return ERR_VALUE;
   }
-  if (bcb_use_fma()) {  // no preparation: the reflectors are applied as stored
-    if (Xt == nullptr || n < 3 || nrows <= 0) return OK;
-    return bc_back_fma_launch<true>(st, n, tau, V, Xt, ldx, nrows, ws);
-  }
+
   static int rt = -1;
   if (rt < 0) {
     const char* e = getenv("PEVD_WYRT");

@@ -1,8 +1,8 @@
-"""BC-Back kernel check + timing (the kernel PEVD_BCB_FMA selects): apply the bulge reflectors of
+"""BC-Back kernel check + timing: apply the bulge reflectors of
 a random band to a random X through pevd_bc_back_left (conventional, on the transpose) and
 pevd_bc_back_right, compare with the CPU oracle at small n, time at large n.
 
-    PEVD_BCB_FMA=1 python tools/bcb_check.py 2048 32768
+    python tools/bcb_check.py 2048 32768
 """
 import ctypes
 import json
