@@ -138,29 +138,10 @@ Layout plan_layout(void* base, int64_t n, int b, int want_vectors, int order) {
   return L;
 }
 
-__global__ void copy_lower_to_full_kernel(int64_t n, const double* src, int64_t lds, double* dst,
-                                          int64_t ldd) {
-  const int64_t total = n * n;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx % n, j = idx / n;
-    dst[i + j * ldd] = src[i + j * lds];
-  }
-}
-
 struct Ev {
   cudaEvent_t a = nullptr, b = nullptr;
 };
 
-// conventional order on the transpose (default; PEVD_CONVT=0 applies Q_b, Q_s from the left)
-bool conv_transposed() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("PEVD_CONVT");
-    v = e ? atoi(e) : 1;
-  }
-  return v != 0;
-}
 
 }  // namespace
 }  // namespace pevd
@@ -273,8 +254,8 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     // ---- conventional: the back-transform preparations (SBR-Back T aggregation, the Z factor
     //      of every BC-Back block; they need only the SBR and chase outputs) on the side stream
     //      beside the divide and conquer
-    const bool conv_t = want_vectors && order == PEVD_ORDER_CONVENTIONAL && conv_transposed() &&
-                        b == 32 && L.vld == 32;
+    // conventional order with b = 32 runs BC-Back on the transpose (the DMMA kernel's layout)
+    const bool conv_t = want_vectors && order == PEVD_ORDER_CONVENTIONAL && b == 32 && L.vld == 32;
     if (want_vectors && order == PEVD_ORDER_CONVENTIONAL) {
       cudaStreamWaitEvent(sb, ev[1].b, 0);
       flops_set_stage(ST_SBR_BACK);

@@ -134,32 +134,50 @@ constexpr int WY_PB = 42;
 constexpr int WY_ZB = 8 * WY_PB;  // doubles of Z per block: 8 rows s x 42 (40 positions p + pad),
                                    // the shared zu layout, so a step's 8 blocks copy linearly
 
+// Per (chase step j, block q of 8 sweeps) one 656-double record, in the kernel's shared layout:
+//   [0, 320)    V of the block: vb[h][tl][s] = element p = 2 s + h of local reflector tl
+//   [320, 656)  Z = V (-T)^T: zb[s][p] (pitch 42)
+// Every step's block count is padded to a multiple of 8 (zero records), so the 8 blocks of a
+// 64-sweep group at a step are ONE contiguous 41,984-byte record, moved by one bulk copy.
+constexpr int WY_VB = 2 * 8 * WY_PA;       // 320
+constexpr int WY_BLK = WY_VB + WY_ZB;      // 656
+constexpr int WY_STEP = 8 * WY_BLK;        // doubles per (group, step)
+
 struct WySmem {
-  double va[2][2][Q4_SG][WY_PA];  // [buf][h][t][s]
-  double zu[2][Q4_SG][WY_PB];     // [buf][8 blk + s][p]
+  double vz[2][WY_STEP];     // [buf][blk][V | Z]
+  uint64_t full[2];          // bulk copy of buffer landed
+  int cnt[2];                // warps done with buffer
   int unit;
 };
 
+// number of padded 8-sweep blocks before chase step j (b = 32): sum_{j' < j} 8 ceil(nb(j') / 8),
+// nb(j') = ceil((n - 2 - 32 j') / 8) = c - 4 j'
+__host__ __device__ __forceinline__ int64_t vz_block0(int64_t n, int64_t j) {
+  const int64_t c = (n - 2 + 7) / 8;
+  const int64_t A = (c + 7) / 8, Bo = (c + 3) / 8;   // ceil((c - 8m) / 8) for even / odd j'
+  const int64_t E = (j + 1) / 2, O = j / 2;
+  return 8 * (E * A - E * (E - 1) / 2 + O * Bo - O * (O - 1) / 2);
+}
+
 // Z = V (-T)^T of every block of 8 consecutive sweeps at every chase step, so that a block
-// acts as X <- X (I - V T V^T) = X + (X V) Z^T.  Block (j, q) covers sweeps 8q..8q+7; its Z
-// (row s = 0..7, window position p = 0..39) lives at Zf + 336 * (tofs[j] + q) + 42 s + p.
+// acts as X <- X (I - V T V^T) = X + (X V) Z^T; written with the block's V into its record
+// (record id = vz_block0(n, j) + q for block q of step j; padding records are zero).
 template <bool BACKWARD>
 __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
-                                  const double* __restrict__ V, int vld,
-                                  const int64_t* __restrict__ tofs, int64_t jcount,
-                                  double* __restrict__ Zf) {
+                                  const double* __restrict__ V, int vld, int64_t jcount,
+                                  double* __restrict__ VZ) {
   // forward:  H_0 H_1 ... H_7 = I - V T V^T, T upper (LAPACK larft 'F')
   // backward: H_7 H_6 ... H_0 = I - V T V^T, T lower (larft 'B')
   constexpr int B = 32;
-  const int64_t total = tofs[jcount];
+  const int64_t total = vz_block0(n, jcount);
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
        id += (int64_t)gridDim.x * blockDim.x) {
     int64_t lo = 0, hi = jcount;
     while (hi - lo > 1) {
       const int64_t mid = (lo + hi) >> 1;
-      if (tofs[mid] <= id) lo = mid; else hi = mid;
+      if (vz_block0(n, mid) <= id) lo = mid; else hi = mid;
     }
-    const int64_t j = lo, q = id - tofs[j];
+    const int64_t j = lo, q = id - vz_block0(n, j);
     const int64_t off = bc_slot_offset_dev(n, B, j);
     const int64_t nsw_j = n - 2 - j * B;
     double tv[8];
@@ -170,6 +188,15 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
       const bool ok = i < nsw_j;
       tv[s] = ok ? tau[off + i] : 0.0;
       v[s] = V + (ok ? (off + i) : off) * vld;
+    }
+    double* rec = VZ + id * WY_BLK;
+    // V part: vb[h][tl][s] = v_tl[2 s + h - tl] inside the support, 0 outside (and for absent
+    // reflectors, whose tau is 0)
+#pragma unroll 1
+    for (int e = 0; e < WY_VB; ++e) {
+      const int h = e / (8 * WY_PA), tl = (e / WY_PA) % 8, ss = e % WY_PA;
+      const int idx = 2 * ss + h - tl;
+      rec[e] = (tv[tl] != 0.0 && idx >= 0 && idx < B) ? v[tl][idx] : 0.0;
     }
     // Gram entries g[u][t] = v_u^T v_t for u < t (v_u starts t - u rows above v_t)
     double G[8][8];
@@ -221,18 +248,19 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
       }
     }
     // Z[p][s] = sum_t v_t[p - t] * (-T)[s][t]
-    double* out = Zf + id * WY_ZB;
+    double* out = rec + WY_VB;
 #pragma unroll 1
-    for (int p = 0; p < 40; ++p) {
+    for (int p = 0; p < WY_PB; ++p) {
       double vp[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) vp[t] = (p - t >= 0 && p - t < B) ? v[t][p - t] : 0.0;
+      for (int t = 0; t < 8; ++t)
+        vp[t] = (tv[t] != 0.0 && p - t >= 0 && p - t < B) ? v[t][p - t] : 0.0;
 #pragma unroll
       for (int s2 = 0; s2 < 8; ++s2) {
         double acc = 0.0;
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc = fma(vp[t], -T[s2][t], acc);
-        out[s2 * WY_PB + p] = acc;
+        out[s2 * WY_PB + p] = (p < 40) ? acc : 0.0;
       }
     }
   }
@@ -241,216 +269,179 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
 // LEFT = false: X <- X Q_b on the rows of X (element (row, col) at X[row + col*ldx]), reflectors
 //   in creation-compatible grouped order (groups ascending, steps bottom-to-top, sweeps
 //   ascending), forward T.
-// LEFT = true:  X <- Q_b X, done as Y <- Y Q_b^T on the rows of Y = X^T (element (row, col) at
-//   X[row*ldx + col]): groups descending, steps top-to-bottom, sweeps descending, backward T
-//   (the conventional grouped order of backtrans.py:232-235).
-// ROWMAJOR: a row's elements are contiguous (X[row*ldx + col]); otherwise X is column-major
-// (X[row + col*ldx], rows contiguous down a column: 64-byte segments per 8-row tile, the faster
-// pattern).  Default: the conventional LEFT application reads the columns of X as its rows.
-// RT: 8-row tiles per warp.  RT = 1: 8 warps (256 threads) per 64-row block; RT = 2: 4 warps of
-// 16 rows (two independent DMMA chains per warp, every V / Z fragment feeds both tiles).
-template <bool LEFT, bool ROWMAJOR = LEFT, int RT = 1>
-__global__ void __launch_bounds__(WY_THREADS / RT, 2)
-    bc_back_wy_kernel(int64_t n, const double* __restrict__ V, int vld,
-                      const double* __restrict__ Zf, const int64_t* __restrict__ tofs, double* X,
-                      int64_t ldx, int64_t nrows, int* counter, int* progress, int64_t nunits,
-                      int nrb) {
-  extern __shared__ __align__(16) unsigned char wyraw[];
+// LEFT = true:  X <- Q_b X, done as Y <- Y Q_b^T on the rows of Y = X^T: groups descending,
+//   steps top-to-bottom, sweeps descending, backward T (the conventional grouped order of
+//   backtrans.py:232-235).  X column-major (X[row + col*ldx], rows contiguous down a column:
+//   64-byte segments per 8-row tile): the conventional application runs on the transpose.
+// Staging: each (group, step) record (V and Z of its 8 blocks, 42 KB) is ONE bulk copy on the
+// TMA engine into a double buffer, completing on an mbarrier.  No __syncthreads per step: every
+// warp waits only for the bytes of the step it is about to apply, and the LAST warp to finish
+// with a buffer (a shared counter) launches the copy of the step after next into it, so warps
+// drift freely within the one-step slack the double buffer gives.
+template <bool LEFT>
+__global__ void __launch_bounds__(WY_THREADS, 2)
+    bc_back_wy_kernel(int64_t n, const double* __restrict__ VZ, double* X, int64_t ldx,
+                      int64_t nrows, int* counter, int* progress, int64_t nunits, int nrb) {
+  extern __shared__ __align__(128) unsigned char wyraw[];
   WySmem& S = *reinterpret_cast<WySmem*>(wyraw);
   constexpr int B = 32;
-  constexpr int NT = WY_THREADS / RT;
+  constexpr int NW = WY_THREADS / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qd = lane & 3, r8 = lane >> 2;
   const int64_t nsw = n - 2;
-  // zero va once: the positions outside each reflector's support are never written
-  for (int e = tid; e < 2 * 2 * Q4_SG * WY_PA; e += NT) (&S.va[0][0][0][0])[e] = 0.0;
+  const int64_t ngroups = (nsw + Q4_SG - 1) / Q4_SG;
+  if (tid == 0) {
+    mbar_init(&S.full[0], 1);
+    mbar_init(&S.full[1], 1);
+    S.cnt[0] = S.cnt[1] = 0;
+    mbar_init_fence();
+  }
   __syncthreads();
-  // stage step j of sweep group i0 into buffer buf with cp.async (zero-filled past the last sweep)
-  // V element e = tid + NT p is reflector t = e / 32 = t0 + (NT / 32) p, entry r = tid % 32; the
-  // step's 64 reflectors are consecutive slots (vld = 32: 2048 contiguous doubles) and its Z
-  // blocks are stored in the shared layout, so every copy is an add on both sides.
-  const int t0 = tid >> 5, rr = tid & 31;
-  constexpr int VBUF = 2 * Q4_SG * WY_PA;  // doubles between the two va buffers
-  constexpr int ZBUF = Q4_SG * WY_PB;      // ... and the two zu buffers
-  auto issue = [&](int buf, int64_t i0, int64_t j) {
-    const int64_t off = bc_slot_offset_dev(n, B, j);
-    const int64_t nvalid = n - 2 - j * B - i0;  // sweeps of this group that exist at step j
-    const double* vsrc = V + (off + i0) * 32 + tid;
-#pragma unroll
-    for (int p = 0; p < Q4_SG * B / NT; ++p) {
-      const int t = t0 + (NT / 32) * p, pos = rr + (t & 7);
-      const bool ok = t < nvalid;
-      cp_async8(&S.va[0][pos & 1][t][pos >> 1] + buf * VBUF, ok ? vsrc + p * NT : V, ok);
-    }
-    const double* zsrc = Zf + (tofs[j] + i0 / 8) * WY_ZB;
-    double* zdst = &S.zu[buf][0][0];
-#pragma unroll
-    for (int p = 0; p < (ZBUF / 2 + NT - 1) / NT; ++p) {
-      const int e = tid + p * NT;  // 16-byte chunk e of the step's 8 blocks
-      if (e < ZBUF / 2) {
-        const bool ok = 8 * (e / (WY_ZB / 2)) < nvalid;
-        cp_async16(zdst + 2 * e, ok ? zsrc + 2 * e : Zf, ok);
-      }
-    }
-    cp_async_commit();
-  };
+  uint32_t gstep = 0;  // steps this CTA has consumed (buffer = gstep & 1, parity = (gstep >> 1) & 1)
+  // record of step j of group k
+  auto rec = [&](int64_t k, int64_t j) { return VZ + (vz_block0(n, j) + 8 * k) * WY_BLK; };
   for (;;) {
     if (tid == 0) S.unit = atomicAdd(counter, 1);
     __syncthreads();
     const int64_t u = S.unit;
     __syncthreads();
     if (u >= nunits) break;
-    const int64_t ngroups = (nsw + Q4_SG - 1) / Q4_SG;
     const int64_t seq = u / nrb;                       // groups this row block has done before
     const int64_t k = LEFT ? ngroups - 1 - seq : seq;
     const int rb = (int)(u % nrb);
-    if (tid == 0 && ld_acquire(progress + rb) < (int)seq) {
-      unsigned ns = 64;
-      while (ld_acquire(progress + rb) < (int)seq) {
-        __nanosleep(ns);
-        if (ns < 1024) ns <<= 1;
-      }
-    }
-    const int64_t cs = ROWMAJOR ? 1 : ldx;             // column stride of a row's elements
-    bool active[RT];
-    double* x[RT];
-#pragma unroll
-    for (int rt = 0; rt < RT; ++rt) {
-      const int64_t row = (int64_t)rb * WY_ROWS + warp * 8 * RT + rt * 8 + r8;
-      active[rt] = row < nrows;
-      x[rt] = X + (active[rt] ? (ROWMAJOR ? row * ldx : row) : 0);
-    }
     const int64_t i0 = k * Q4_SG;
     const int64_t jmax = (n - 3 - i0) / B;
     const int64_t jfirst = LEFT ? 0 : jmax;
-    int64_t ws = i0 + 1 + jfirst * B;
-    int buf = 0;
-    issue(buf, i0, jfirst);
-    __syncthreads();  // progress acquired by tid 0 before anyone reads X
-    double w[RT][12][2];
-#pragma unroll
-    for (int rt = 0; rt < RT; ++rt)
-#pragma unroll
-      for (int c = 0; c < 12; ++c)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t col = ws + 8 * c + 2 * qd + h;
-          w[rt][c][h] = (active[rt] && col < n) ? __ldcg(x[rt] + col * cs) : 0.0;
+    if (tid == 0) {
+      // the unit's first two steps (the buffers are free: every warp passed the barrier above)
+      for (int64_t s2 = 0; s2 < 2 && s2 <= jmax; ++s2) {
+        const uint32_t g = gstep + (uint32_t)s2;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&S.full[g & 1], WY_STEP * 8);
+        bulk_g2s(S.vz[g & 1], rec(k, LEFT ? jfirst + s2 : jfirst - s2), WY_STEP * 8, &S.full[g & 1]);
+      }
+      if (ld_acquire(progress + rb) < (int)seq) {
+        unsigned ns = 64;
+        while (ld_acquire(progress + rb) < (int)seq) {
+          __nanosleep(ns);
+          if (ns < 1024) ns <<= 1;
         }
-    cp_async_wait<0>();
-    __syncthreads();
-    for (int64_t jj = 0; jj <= jmax; ++jj) {
-      const int64_t j = LEFT ? jj : jmax - jj;
+      }
+    }
+    const int64_t row = (int64_t)rb * WY_ROWS + warp * 8 + r8;
+    const bool active = row < nrows;
+    double* x = X + (active ? row : 0);
+    int64_t ws = i0 + 1 + jfirst * B;
+    __syncthreads();  // progress acquired by tid 0 before anyone reads X
+    double w[12][2];
+#pragma unroll
+    for (int c = 0; c < 12; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t col = ws + 8 * c + 2 * qd + h;
+        w[c][h] = (active && col < n) ? __ldcg(x + col * ldx) : 0.0;
+      }
+    for (int64_t jj = 0; jj <= jmax; ++jj, ++gstep) {
       const bool more = jj < jmax;
-      // prefetch the next step: its new window columns (registers) and its V / Z (other buffer:
-      // the barrier that ended the previous step means nobody still reads it)
-      double nx[RT][4][2];
+      const int buf = gstep & 1;
+      // prefetch the next step's new window columns (registers)
+      double nx[4][2];
       const int64_t nbase = LEFT ? ws + 3 * B : ws - B;
 #pragma unroll
-      for (int rt = 0; rt < RT; ++rt)
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int64_t col = nbase + 8 * c + 2 * qd + h;
-            nx[rt][c][h] = (more && active[rt] && col < n) ? __ldcg(x[rt] + col * cs) : 0.0;
-          }
-      if (more) issue(buf ^ 1, i0, LEFT ? j + 1 : j - 1);
-      // ---- apply the 8 blocks of this step: P = X V (10 DMMA), X += P Z^T (10 DMMA), per tile
+        for (int h = 0; h < 2; ++h) {
+          const int64_t col = nbase + 8 * c + 2 * qd + h;
+          nx[c][h] = (more && active && col < n) ? __ldcg(x + col * ldx) : 0.0;
+        }
+      mbar_wait(&S.full[buf], (gstep >> 1) & 1);  // this step's V and Z have landed
+      const double* vz = S.vz[buf];
+      // ---- apply the 8 blocks of this step: P = X V (10 DMMA), X += P Z^T (10 DMMA)
 #pragma unroll
       for (int bb = 0; bb < Q4_SG / 8; ++bb) {
         const int blk = LEFT ? Q4_SG / 8 - 1 - bb : bb;
-        const int tb = blk * 8;
-        double p0[RT], p1[RT], e0[RT], e1[RT];
-#pragma unroll
-        for (int rt = 0; rt < RT; ++rt) p0[rt] = p1[rt] = e0[rt] = e1[rt] = 0.0;
-        const double* v0 = &S.va[buf][0][tb + r8][qd];
-        const double* v1 = &S.va[buf][1][tb + r8][qd];
+        const double* vb = vz + blk * WY_BLK;
+        double p0 = 0.0, p1 = 0.0, e0 = 0.0, e1 = 0.0;
+        const double* v0 = vb + r8 * WY_PA + qd;
+        const double* v1 = v0 + 8 * WY_PA;
 #pragma unroll
         for (int cc = 0; cc < 5; ++cc) {
           const double a = v0[4 * cc], c = v1[4 * cc];
-#pragma unroll
-          for (int rt = 0; rt < RT; ++rt) {
-            dmma884(p0[rt], p1[rt], w[rt][blk + cc][0], a);
-            dmma884(e0[rt], e1[rt], w[rt][blk + cc][1], c);
-          }
+          dmma884(p0, p1, w[blk + cc][0], a);
+          dmma884(e0, e1, w[blk + cc][1], c);
         }
-#pragma unroll
-        for (int rt = 0; rt < RT; ++rt) {
-          p0[rt] += e0[rt];
-          p1[rt] += e1[rt];
-        }
-        const double* z0 = &S.zu[buf][tb + 2 * qd][r8];
-        const double* z1 = &S.zu[buf][tb + 2 * qd + 1][r8];
+        p0 += e0;
+        p1 += e1;
+        const double* z0 = vb + WY_VB + (2 * qd) * WY_PB + r8;
+        const double* z1 = z0 + WY_PB;
         // all five tiles' first k-step, then the second: two updates of a tile are 5 DMMAs apart
 #pragma unroll
-        for (int cc = 0; cc < 5; ++cc) {
-          const double z = z0[8 * cc];
+        for (int cc = 0; cc < 5; ++cc) dmma884(w[blk + cc][0], w[blk + cc][1], p0, z0[8 * cc]);
 #pragma unroll
-          for (int rt = 0; rt < RT; ++rt)
-            dmma884(w[rt][blk + cc][0], w[rt][blk + cc][1], p0[rt], z);
-        }
-#pragma unroll
-        for (int cc = 0; cc < 5; ++cc) {
-          const double z = z1[8 * cc];
-#pragma unroll
-          for (int rt = 0; rt < RT; ++rt)
-            dmma884(w[rt][blk + cc][0], w[rt][blk + cc][1], p1[rt], z);
+        for (int cc = 0; cc < 5; ++cc) dmma884(w[blk + cc][0], w[blk + cc][1], p1, z1[8 * cc]);
+      }
+      // ---- done with this buffer: the last warp refills it with the step after next
+      __syncwarp();
+      if (lane == 0) {
+        const int prev = atomicAdd(&S.cnt[buf], 1);
+        if (prev == NW - 1) {
+          S.cnt[buf] = 0;
+          if (jj + 2 <= jmax) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&S.full[buf], WY_STEP * 8);
+            bulk_g2s(S.vz[buf], rec(k, LEFT ? jfirst + jj + 2 : jfirst - jj - 2), WY_STEP * 8,
+                     &S.full[buf]);
+          }
         }
       }
       // ---- slide by b = 32 (4 tiles): the trailing 4 tiles (right) / leading 4 tiles (left)
       //      are final for this group
 #pragma unroll
-      for (int rt = 0; rt < RT; ++rt) {
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int h = 0; h < 2; ++h) {
+          const int cw = LEFT ? c : c + 8;
+          const int64_t col = ws + 8 * cw + 2 * qd + h;
+          if (active && col < n) x[col * ldx] = w[cw][h];
+        }
+      if (more) {
+        if (!LEFT) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int cw = LEFT ? c : c + 8;
-            const int64_t col = ws + 8 * cw + 2 * qd + h;
-            if (active[rt] && col < n) x[rt][col * cs] = w[rt][cw][h];
+          for (int c = 11; c >= 4; --c) {
+            w[c][0] = w[c - 4][0];
+            w[c][1] = w[c - 4][1];
           }
-        if (more) {
-          if (!LEFT) {
 #pragma unroll
-            for (int c = 11; c >= 4; --c) {
-              w[rt][c][0] = w[rt][c - 4][0];
-              w[rt][c][1] = w[rt][c - 4][1];
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              w[rt][c][0] = nx[rt][c][0];
-              w[rt][c][1] = nx[rt][c][1];
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              w[rt][c][0] = w[rt][c + 4][0];
-              w[rt][c][1] = w[rt][c + 4][1];
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              w[rt][8 + c][0] = nx[rt][c][0];
-              w[rt][8 + c][1] = nx[rt][c][1];
-            }
+          for (int c = 0; c < 4; ++c) {
+            w[c][0] = nx[c][0];
+            w[c][1] = nx[c][1];
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < 12; ++c) {
-            if (LEFT ? c < 4 : c >= 8) continue;  // already stored above
+          for (int c = 0; c < 8; ++c) {
+            w[c][0] = w[c + 4][0];
+            w[c][1] = w[c + 4][1];
+          }
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int64_t col = ws + 8 * c + 2 * qd + h;
-              if (active[rt] && col < n) x[rt][col * cs] = w[rt][c][h];
-            }
+          for (int c = 0; c < 4; ++c) {
+            w[8 + c][0] = nx[c][0];
+            w[8 + c][1] = nx[c][1];
+          }
+        }
+        ws += LEFT ? B : -B;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 12; ++c) {
+          if (LEFT ? c < 4 : c >= 8) continue;  // already stored above
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t col = ws + 8 * c + 2 * qd + h;
+            if (active && col < n) x[col * ldx] = w[c][h];
           }
         }
       }
-      if (more) ws += LEFT ? B : -B;
-      buf ^= 1;
-      cp_async_wait<0>();
-      __syncthreads();
     }
+    __syncthreads();  // every warp is done with the unit (and its buffers) before the next
     if (tid == 0) {
       __threadfence();
       st_release(progress + rb, (int)(seq + 1));
@@ -731,71 +722,69 @@ int transpose(cudaStream_t st, int64_t rows, int64_t cols, const double* in, int
   return OK;
 }
 
+static int64_t wy_counter_bytes(int64_t nrows) { return ((nrows / 32 + 64) * 4 + 255) / 256 * 256; }
+
 int64_t bc_back_ws_bytes(int64_t n, int64_t nrows) {
-  // counters + T-factor offsets + the -T factors of every block of 8 sweeps (64 doubles each)
+  // counters + the (V, Z) record of every padded block of 8 sweeps at every chase step
   const int64_t jcount = n >= 3 ? (n - 3) / 32 + 1 : 1;
-  int64_t nblk = 0;
-  for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(std::max<int64_t>(n - 2 - j * 32, 0), 8);
-  return ((nrows / 32 + 64) * 4 + 255) / 256 * 256 + ((jcount + 2) * 8 + 255) / 256 * 256 +
-         nblk * (int64_t)WY_ZB * 8 + 256;
+  return wy_counter_bytes(nrows) + (n >= 3 ? vz_block0(n, jcount) : 0) * (int64_t)WY_BLK * 8 + 256;
 }
 
-// tofs[j] = number of 8-sweep blocks before chase step j (prefix sum of cdiv(n - 2 - 32 j, 8)),
-// on the device so the BC-Back preparation needs no host synchronisation
-__global__ void wy_tofs_kernel(int64_t n, int64_t jcount, int64_t* tofs) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    int64_t acc = 0;
-    tofs[0] = 0;
-    for (int64_t j = 0; j < jcount; ++j) {
-      acc += (n - 2 - j * 32 + 7) / 8;
-      tofs[j + 1] = acc;
-    }
+// The DMMA compact-WY BC-Back (b = 32, vld = 32): X <- X Q_b (LEFT = false) or Xt <- Xt Q_b^T
+// (LEFT = true, the conventional application on the transpose).  `prepared`: the counters and
+// the (V, Z) records of ws were already built by a call with X == nullptr (depends on the chase
+// output only, so the orchestrators run it beside the divide and conquer).
+template <bool LEFT>
+static int bc_back_wy_launch(cudaStream_t st, int64_t n, const double* tau, const double* V,
+                             double* X, int64_t ldx, int64_t nrows, void* ws, bool prepared) {
+  const int nrb = (int)cdiv(nrows, WY_ROWS);
+  const int64_t ngroups = cdiv(n - 2, Q4_SG);
+  const int64_t nunits = ngroups * nrb;
+  int* counter = (int*)ws;
+  int* progress = counter + 32;
+  const int64_t jcount = (n - 3) / 32 + 1;
+  double* VZ = (double*)((char*)ws + wy_counter_bytes(nrows));
+  const int64_t nrec = vz_block0(n, jcount);
+  if (!prepared) {
+    PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
+    wy_tfactor_kernel<LEFT><<<(unsigned)std::min<int64_t>(cdiv(nrec, 128), 16384), 128, 0, st>>>(
+        n, tau, V, 32, jcount, VZ);
+    PEVD_LAUNCH_CHECK();
   }
+  if (X == nullptr) return OK;  // preparation only
+  // executed: 20 DMMA (10240 flops) per 8 rows per (unpadded) block of 8 reflectors
+  {
+    int64_t nblk = 0;
+    for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(n - 2 - j * 32, 8);
+    flops_add(1280.0 * (double)nrows * (double)nblk);
+  }
+  auto kfn = bc_back_wy_kernel<LEFT>;
+  const size_t smem = sizeof(WySmem);
+  static int attr_dev = -1;
+  int dev;
+  PEVD_CUDA(cudaGetDevice(&dev));
+  if (attr_dev != dev) {
+    PEVD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_dev = dev;
+  }
+  int per_sm = 0;
+  PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, WY_THREADS, smem));
+  if (per_sm < 1) {
+    set_error("bc_back: persistent kernel cannot be resident");
+    return ERR_CUDA;
+  }
+  const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
+  kfn<<<(unsigned)grid, WY_THREADS, smem, st>>>(n, VZ, X, ldx, nrows, counter, progress, nunits,
+                                               nrb);
+  PEVD_LAUNCH_CHECK();
+  return OK;
 }
 
 int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                   double* X, int64_t ldx, int64_t nrows, void* ws) {
   if (n < 3 || nrows <= 0 || b < 2) return OK;
-  if (b == 32 && vld == 32 && ws) {  // DMMA compact-WY kernel (fully asynchronous)
-    const int nrb = (int)cdiv(nrows, WY_ROWS);
-    const int64_t ngroups = cdiv(n - 2, Q4_SG);
-    const int64_t nunits = ngroups * nrb;
-    int* counter = (int*)ws;
-    int* progress = counter + 32;
-    const int64_t jcount = (n - 3) / 32 + 1;
-    int64_t* tofs = (int64_t*)((char*)ws + ((nrows / 32 + 64) * 4 + 255) / 256 * 256);
-    double* Tf = (double*)((char*)tofs + ((jcount + 2) * 8 + 255) / 256 * 256);
-    PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
-    wy_tofs_kernel<<<1, 32, 0, st>>>(n, jcount, tofs);
-    PEVD_LAUNCH_CHECK();
-    int64_t nblk = 0;
-    for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(n - 2 - j * 32, 8);
-    wy_tfactor_kernel<false><<<(unsigned)std::min<int64_t>(cdiv(nblk, 128), 16384), 128, 0, st>>>(
-        n, tau, V, vld, tofs, jcount, Tf);
-    PEVD_LAUNCH_CHECK();
-    auto kfn = bc_back_wy_kernel<false, false, 1>;
-    const size_t smem = sizeof(WySmem);
-    static int attr_dev = -1;
-    int dev;
-    PEVD_CUDA(cudaGetDevice(&dev));
-    if (attr_dev != dev) {
-      PEVD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_dev = dev;
-    }
-    int per_sm = 0;
-    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, WY_THREADS, smem));
-    if (per_sm < 1) {
-      set_error("bc_back: persistent kernel cannot be resident");
-      return ERR_CUDA;
-    }
-    // executed: 20 DMMA (10240 flops) per 8 rows per block of 8 reflectors
-    flops_add(1280.0 * (double)nrows * (double)nblk);
-    const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
-    kfn<<<(unsigned)grid, WY_THREADS, smem, st>>>(n, V, vld, Tf, tofs, X, ldx, nrows, counter,
-                                                 progress, nunits, nrb);
-    PEVD_LAUNCH_CHECK();
-    return OK;
-  }
+  if (b == 32 && vld == 32 && ws)  // DMMA compact-WY kernel (fully asynchronous)
+    return bc_back_wy_launch<false>(st, n, tau, V, X, ldx, nrows, ws, false);
   // any other b (or a padded reflector stride): one thread per row, reflector by reflector
   flops_add(4.0 * b * (double)bc_num_reflectors(n, b) * (double)nrows);
   bc_back_right_generic<<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, b, tau, V, vld, X, ldx,
@@ -804,70 +793,17 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
   return OK;
 }
 
-template <bool TMEM, int KRT = 1>
-int bc_back_left_impl(cudaStream_t st, int64_t n, int b, const double* tau, const double* V,
-                      int vld, double* X, int64_t ldx, int64_t ncols, void* ws,
-                      bool prepared = false) {
+// X (n x ncols, column-major) <- Q_b X one reflector at a time (any b; the b = 32 product paths
+// run bc_back_left_t on the transpose instead)
+int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
+                 double* X, int64_t ldx, int64_t ncols, void* ws) {
+  (void)ws;
   if (n < 3 || ncols <= 0 || b < 2) return OK;
-  if (b == 32 && vld == 32 && ws) {  // the DMMA kernel reads each step's V as 2048 contiguous
-    // X <- Q_b X  ==  (X^T Q_b^T)^T: the DMMA compact-WY kernel in reverse order on the rows of
-    // X^T (= the columns of X, contiguous), backward T factors
-    const int nrb = (int)cdiv(ncols, WY_ROWS);
-    const int64_t ngroups = cdiv(n - 2, Q4_SG);
-    const int64_t nunits = ngroups * nrb;
-    int* counter = (int*)ws;
-    int* progress = counter + 32;
-    const int64_t jcount = (n - 3) / 32 + 1;
-    int64_t* tofs = (int64_t*)((char*)ws + ((ncols / 32 + 64) * 4 + 255) / 256 * 256);
-    double* Tf = (double*)((char*)tofs + ((jcount + 2) * 8 + 255) / 256 * 256);
-    if (!prepared) {  // counters, block offsets and the Z of every block (BC output only)
-      PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
-      wy_tofs_kernel<<<1, 32, 0, st>>>(n, jcount, tofs);
-      PEVD_LAUNCH_CHECK();
-      int64_t nblk = 0;
-      for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(n - 2 - j * 32, 8);
-      wy_tfactor_kernel<true><<<(unsigned)std::min<int64_t>(cdiv(nblk, 128), 16384), 128, 0, st>>>(
-          n, tau, V, vld, tofs, jcount, Tf);
-      PEVD_LAUNCH_CHECK();
-    }
-    if (X == nullptr) return OK;  // preparation only
-    {
-      int64_t nblk = 0;
-      for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(n - 2 - j * 32, 8);
-      flops_add(1280.0 * (double)ncols * (double)nblk);  // executed DMMA flops, as above
-    }
-    const size_t smem = sizeof(WySmem);
-    static int attr_dev = -1;
-    int dev;
-    PEVD_CUDA(cudaGetDevice(&dev));
-    if (attr_dev != dev) {
-      PEVD_CUDA(cudaFuncSetAttribute(bc_back_wy_kernel<true, !TMEM, KRT>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_dev = dev;
-    }
-    int per_sm = 0;
-    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bc_back_wy_kernel<true, !TMEM, KRT>,
-                                                            WY_THREADS / KRT, smem));
-    if (per_sm < 1) {
-      set_error("bc_back_left: persistent kernel cannot be resident");
-      return ERR_CUDA;
-    }
-    const int64_t grid = std::min<int64_t>((int64_t)per_sm * num_sms(), nunits);
-    bc_back_wy_kernel<true, !TMEM, KRT><<<(unsigned)grid, WY_THREADS / KRT, smem, st>>>(
-        n, V, vld, Tf, tofs, X, ldx, ncols, counter, progress, nunits, nrb);
-    PEVD_LAUNCH_CHECK();
-    return OK;
-  }
   flops_add(4.0 * b * (double)bc_num_reflectors(n, b) * (double)ncols);
   bc_back_left_generic<<<(unsigned)cdiv(ncols, 128), 128, 0, st>>>(n, b, tau, V, vld, X, ldx,
                                                                    ncols);
   PEVD_LAUNCH_CHECK();
   return OK;
-}
-
-int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
-                 double* X, int64_t ldx, int64_t ncols, void* ws) {
-  return bc_back_left_impl<false>(st, n, b, tau, V, vld, X, ldx, ncols, ws);
 }
 
 int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
@@ -876,15 +812,8 @@ int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const d
     set_error("bc_back_left_t: needs b = 32, vld = 32 and a workspace");
     return ERR_VALUE;
   }
-
-  static int rt = -1;
-  if (rt < 0) {
-    const char* e = getenv("PEVD_WYRT");
-    rt = e ? atoi(e) : 1;
-  }
-  if (rt == 1)
-    return bc_back_left_impl<true, 1>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws, prepared);
-  return bc_back_left_impl<true, 2>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws, prepared);
+  if (n < 3 || nrows <= 0) return OK;
+  return bc_back_wy_launch<true>(st, n, tau, V, Xt, ldx, nrows, ws, prepared);
 }
 
 }  // namespace pevd
