@@ -119,6 +119,14 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
 int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q,
                int64_t ldq, int want_vectors, int order, pevd_stats* stats);
 
+/* The input check of SymmetricMatrix (core.py:75-84) on the device: out2[0] = max |A_ij - A_ji|,
+ * out2[1] = ||A||_F (HOST array of 2).  A device pointer (column-major, lda).  Synchronous. */
+int pevd_asymmetry(int64_t n, const double* A, int64_t lda, double* out2, void* stream);
+/* out (cols x rows, ldo) = in^T (in: rows x cols, ldi), device pointers: the C-order Q of
+ * pipeline.py:503 without a host transpose. */
+int pevd_transpose(int64_t rows, int64_t cols, const double* in, int64_t ldi, double* out,
+                   int64_t ldo, void* stream);
+
 /* ---------------------------------------------------------------- per-stage (device pointers)
  * Each replaces one reference function; `stream` is a cudaStream_t; all are asynchronous except
  * where noted. */

@@ -96,6 +96,8 @@ SIGNATURES = {
     "pevd_bc_back_workspace_bytes": (_i64, [_i64, _i64]),
     "pevd_bc_back_right": (_int, [_i64, _int, _vp, _vp, _int, _vp, _i64, _i64, _vp, _vp]),
     "pevd_bc_back_left": (_int, [_i64, _int, _vp, _vp, _int, _vp, _i64, _i64, _vp, _vp]),
+    "pevd_asymmetry": (_int, [_i64, _vp, _i64, ctypes.POINTER(_dbl), _vp]),
+    "pevd_transpose": (_int, [_i64, _i64, _vp, _i64, _vp, _i64, _vp]),
     "pevd_nccl_unique_id": (_int, [ctypes.c_char_p]),
     "pevd_comm_nccl_create": (_int, [_int, _int, ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "pevd_comm_destroy": (None, [_vp]),

@@ -138,6 +138,73 @@ Layout plan_layout(void* base, int64_t n, int b, int want_vectors, int order) {
   return L;
 }
 
+// max |A_ij - A_ji| and sum of squares over 32 x 32 tile pairs (one CTA per lower tile pair,
+// read through shared memory so both tiles stream coalesced); per-CTA partials, reduced in a
+// fixed order by asym_finish (deterministic)
+__global__ void asym_partials(int64_t n, const double* __restrict__ A, int64_t lda, int64_t nt,
+                              double* __restrict__ part) {
+  __shared__ double t[32][33];
+  __shared__ double rmax[8], rsum[8];
+  const int64_t ntiles = nt * (nt + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int64_t id = blockIdx.x; id < ntiles; id += gridDim.x) {
+    // tile (I, J), I >= J, row-major enumeration of the lower triangle of tiles
+    int64_t I = (int64_t)((sqrt(8.0 * (double)id + 1.0) - 1.0) / 2.0);
+    while (I * (I + 1) / 2 > id) --I;
+    while ((I + 1) * (I + 2) / 2 <= id) ++I;
+    const int64_t J = id - I * (I + 1) / 2;
+    double mx = 0.0, sq = 0.0;
+    // upper tile (J, I) transposed into shared memory: t[c][r] = A[J*32 + r, I*32 + c]
+    for (int k = ty; k < 32; k += 8) {
+      const int64_t r = J * 32 + tx, c = I * 32 + k;
+      t[k][tx] = (r < n && c < n) ? A[r + c * lda] : 0.0;
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      const int64_t r = I * 32 + tx, c = J * 32 + k;  // lower element A[r, c]
+      if (r < n && c < n) {
+        const double a = A[r + c * lda];
+        const double m = t[tx][k];                   // A[c, r]
+        mx = fmax(mx, fabs(a - m));
+        sq += (I == J) ? a * a : a * a + m * m;
+      }
+    }
+    __syncthreads();
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+    for (int o = 16; o > 0; o >>= 1) {
+      if (o < 16) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    }
+    if (tx == 0) {
+      rmax[ty] = mx;
+      rsum[ty] = sq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m2 = 0.0, s2 = 0.0;
+      for (int w = 0; w < 8; ++w) {
+        m2 = fmax(m2, rmax[w]);
+        s2 += rsum[w];
+      }
+      part[2 * blockIdx.x] = fmax(id == blockIdx.x ? 0.0 : part[2 * blockIdx.x], m2);
+      part[2 * blockIdx.x + 1] = (id == blockIdx.x ? 0.0 : part[2 * blockIdx.x + 1]) + s2;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void asym_finish(int nparts, const double* __restrict__ part, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double m = 0.0, s = 0.0;
+    for (int i = 0; i < nparts; ++i) {
+      m = fmax(m, part[2 * i]);
+      s += part[2 * i + 1];
+    }
+    out[0] = m;
+    out[1] = sqrt(s);
+  }
+}
+
 struct Ev {
   cudaEvent_t a = nullptr, b = nullptr;
 };
@@ -363,6 +430,39 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
   if (rc == ERR_CUDA && g_err[0] == '\0') set_error("CUDA failure");
   cleanup();
   return rc;
+}
+
+int pevd_transpose(int64_t rows, int64_t cols, const double* in, int64_t ldi, double* out,
+                   int64_t ldo, void* stream) {
+  return transpose((cudaStream_t)stream, rows, cols, in, ldi, out, ldo);
+}
+
+int pevd_asymmetry(int64_t n, const double* A, int64_t lda, double* out2, void* stream) {
+  if (n < 1 || lda < n || !A || !out2) {
+    set_error("pevd_asymmetry: bad arguments");
+    return ERR_VALUE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nt = cdiv(n, 32);
+  const int64_t ntiles = nt * (nt + 1) / 2;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)num_sms() * 16);
+  double* d = nullptr;
+  if (cudaMallocAsync(&d, (2 * grid + 2) * 8, st) != cudaSuccess) {
+    set_error("pevd_asymmetry: allocation failed");
+    return ERR_NOMEM;
+  }
+  asym_partials<<<grid, 256, 0, st>>>(n, A, lda, nt, d + 2);
+  count_launch();
+  asym_finish<<<1, 32, 0, st>>>(grid, d + 2, d);
+  count_launch();
+  cudaError_t e = cudaMemcpyAsync(out2, d, 16, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(d, st);
+  if (e != cudaSuccess) {
+    set_error("pevd_asymmetry: %s", cudaGetErrorString(e));
+    return ERR_CUDA;
+  }
+  return OK;
 }
 
 int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q, int64_t ldq,

@@ -36,9 +36,8 @@ constexpr int BC_WARPS = 2;  // warps per CTA
 constexpr int DONE = 1 << 30;
 
 struct WarpSmem {
-  double SL[BMAX * LDS_];
+  double SLC[2][BMAX * LDS_];  // left block / coupling block, ping-ponged between steps
   double SW[BMAX * LDS_];
-  double SC[BMAX * LDS_];
   double vs[BMAX];
   double wv[BMAX];
 };
@@ -85,6 +84,11 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
   const int64_t wglob = (int64_t)blockIdx.x * BC_WARPS + (threadIdx.x >> 5);
   const int64_t total_warps = (int64_t)gridDim.x * BC_WARPS;
   for (int64_t gi = wglob; gi < gend; gi += total_warps) {
+    // The coupling block of step j (rows [w0+L, w0+L+b) x columns [w0, w0+L)) IS the left block
+    // of step j+1 of the same sweep, and nobody else touches it in between (the next sweep
+    // reaches it only after this one completed step j+2): it stays in shared memory -- the two
+    // buffers swap roles -- and is neither stored at step j nor reloaded at step j+1.
+    int cur = 0;  // SLC[cur] = this step's left block, SLC[cur ^ 1] its coupling block
     for (int64_t j = 0; gi + 1 + j * b <= n - 2; ++j) {
       // ---- wait for the predecessor sweep to complete step j+2.  Polling is a relaxed L2 load
       //      (an acquire per poll would invalidate L1 on every iteration); once the flag is seen
@@ -110,7 +114,11 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
       // the whole matrix's fixed slots)
       const int64_t slot = (int64_t)j * (slot_n - 2) - (int64_t)b * j * (j - 1) / 2 + slot_col0 + gi;
 
-      // ---- stage the whole region with independent loads (one L2 round trip, not 3b)
+      const bool last = gi + 1 + (j + 1) * b > n - 2;  // no step j+1 in this sweep
+      double* SL = S.SLC[cur];
+      double* SC = S.SLC[cur ^ 1];
+      // ---- stage the region with independent loads (one L2 round trip, not 3b); the left block
+      //      of a step j >= 1 is already in shared memory
       double rl[BMAX], rw[BMAX], rc[BMAX];
       {
         // element q of this lane's row in each region: one pointer per region advanced by
@@ -121,7 +129,7 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
         const double* pc = pw + L;
 #pragma unroll
         for (int q = 0; q < BMAX; ++q) {
-          rl[q] = (q < nleft && lane < L) ? __ldcg(pl) : 0.0;
+          rl[q] = (j == 0 && q < nleft && lane < L) ? __ldcg(pl) : 0.0;
           rw[q] = (q < L && lane >= q && lane < L) ? __ldcg(pw) : 0.0;
           rc[q] = (q < L && lane < nT) ? __ldcg(pc) : 0.0;
           pl += stp;
@@ -131,21 +139,34 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
       }
 #pragma unroll
       for (int q = 0; q < BMAX; ++q) {
-        S.SL[lane * LDS_ + q] = rl[q];
-        S.SC[lane * LDS_ + q] = rc[q];
+        if (j == 0) SL[lane * LDS_ + q] = rl[q];
+        SC[lane * LDS_ + q] = rc[q];
         if (lane >= q) {
           S.SW[lane * LDS_ + q] = rw[q];
           S.SW[q * LDS_ + lane] = rw[q];
         }
       }
       __syncwarp();
-      const double x = (lane < L) ? S.SL[lane * LDS_] : 0.0;
+      const double x = (lane < L) ? SL[lane * LDS_] : 0.0;
       const double tail = warp_sum((lane >= 1 && lane < L) ? x * x : 0.0);
       if (tail == 0.0) {
-        // nothing to annihilate: the reference records no reflector here (tau = 0 slot)
+        // nothing to annihilate: the reference records no reflector here (tau = 0 slot).  The
+        // left block still holds the previous step's coupling update (kept in shared memory,
+        // never stored), and on the last step the coupling block must reach memory too.
         if (tau_out) {
           if (lane == 0) tau_out[slot] = 0.0;
           for (int r = lane; r < vld; r += 32) V_out[slot * vld + r] = (r == 0) ? 1.0 : 0.0;
+        }
+        const int64_t stp = LDB - 1;
+        if (j > 0) {
+          double* pl = Bd + cg * LDB + (w0 - cg) + lane;
+          for (int q = 0; q < nleft; ++q, pl += stp)
+            if (lane < L) *pl = SL[lane * LDS_ + q];
+        }
+        if (last) {
+          double* pc = Bd + w0 * LDB + lane + L;
+          for (int c = 0; c < L; ++c, pc += stp)
+            if (lane < nT) *pc = SC[lane * LDS_ + c];
         }
       } else {
         const double x0 = __shfl_sync(0xffffffffu, x, 0);
@@ -156,7 +177,7 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
         const double vsq = 1.0 + warp_sum((lane >= 1) ? v * v : 0.0);
         const double tau = 2.0 / vsq;
         S.vs[lane] = v;
-        if (lane < L) S.SL[lane * LDS_] = (lane == 0) ? alpha : 0.0;
+        if (lane < L) SL[lane * LDS_] = (lane == 0) ? alpha : 0.0;
         __syncwarp();
         // (all staged entries outside the live L x L / nT x L region are zero and v is zero
         //  beyond L, so every loop below runs the full BMAX width without predicates; four
@@ -167,14 +188,14 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
           double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll
           for (int r = 0; r < BMAX; r += 4) {
-            d0 = fma(S.vs[r], S.SL[r * LDS_ + q], d0);
-            d1 = fma(S.vs[r + 1], S.SL[(r + 1) * LDS_ + q], d1);
-            d2 = fma(S.vs[r + 2], S.SL[(r + 2) * LDS_ + q], d2);
-            d3 = fma(S.vs[r + 3], S.SL[(r + 3) * LDS_ + q], d3);
+            d0 = fma(S.vs[r], SL[r * LDS_ + q], d0);
+            d1 = fma(S.vs[r + 1], SL[(r + 1) * LDS_ + q], d1);
+            d2 = fma(S.vs[r + 2], SL[(r + 2) * LDS_ + q], d2);
+            d3 = fma(S.vs[r + 3], SL[(r + 3) * LDS_ + q], d3);
           }
           const double dot = tau * ((d0 + d1) + (d2 + d3));
 #pragma unroll
-          for (int r = 0; r < BMAX; ++r) S.SL[r * LDS_ + q] -= dot * S.vs[r];
+          for (int r = 0; r < BMAX; ++r) SL[r * LDS_ + q] -= dot * S.vs[r];
         }
         // ---- H A H on the window (lane = row r)
         double u = 0.0;
@@ -197,14 +218,14 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
           double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll
           for (int c = 0; c < BMAX; c += 4) {
-            d0 = fma(S.SC[lane * LDS_ + c], S.vs[c], d0);
-            d1 = fma(S.SC[lane * LDS_ + c + 1], S.vs[c + 1], d1);
-            d2 = fma(S.SC[lane * LDS_ + c + 2], S.vs[c + 2], d2);
-            d3 = fma(S.SC[lane * LDS_ + c + 3], S.vs[c + 3], d3);
+            d0 = fma(SC[lane * LDS_ + c], S.vs[c], d0);
+            d1 = fma(SC[lane * LDS_ + c + 1], S.vs[c + 1], d1);
+            d2 = fma(SC[lane * LDS_ + c + 2], S.vs[c + 2], d2);
+            d3 = fma(SC[lane * LDS_ + c + 3], S.vs[c + 3], d3);
           }
           const double dot = tau * ((d0 + d1) + (d2 + d3));
 #pragma unroll
-          for (int c = 0; c < BMAX; ++c) S.SC[lane * LDS_ + c] -= dot * S.vs[c];
+          for (int c = 0; c < BMAX; ++c) SC[lane * LDS_ + c] -= dot * S.vs[c];
         }
         __syncwarp();
 #pragma unroll
@@ -220,13 +241,13 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
           double* pl = Bd + cg * LDB + (w0 - cg) + lane;
 #pragma unroll 4
           for (int q = 0; q < nleft; ++q, pl += stp)
-            if (lane < L) *pl = S.SL[lane * LDS_ + q];
+            if (lane < L) *pl = SL[lane * LDS_ + q];
           double* pw = Bd + w0 * LDB + lane;
           double* pc = pw + L;
 #pragma unroll 4
           for (int c = 0; c < L; ++c, pw += stp, pc += stp) {
             if (lane >= c && lane < L) *pw = S.SW[lane * LDS_ + c];
-            if (lane < nT) *pc = S.SC[lane * LDS_ + c];
+            if (last && lane < nT) *pc = SC[lane * LDS_ + c];
           }
         }
         if (tau_out) {
@@ -240,6 +261,7 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
         __threadfence();  // orders the warp's band stores (after __syncwarp) before the flag
         st_relaxed(prog + gi, (int)(j + 1));
       }
+      cur ^= 1;  // this step's coupling block is the next step's left block
     }
     __syncwarp();
     if (lane == 0) {

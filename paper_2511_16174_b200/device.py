@@ -254,15 +254,28 @@ def bc_back_left(n, b, tau, V, x):
     return from_dev(dx)
 
 
-def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None):
-    """Whole single-GPU EVD through pevd_syevd_device: (lam, Q or None, PevdStats)."""
+def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=False,
+          sym_tol=1e-13):
+    """Whole single-GPU EVD through pevd_syevd_device: (lam, Q or None, PevdStats).
+
+    The host array goes to the device without a host-side transpose: a Fortran-order array is
+    A column-major, a C-order one is A^T column-major (the same matrix when symmetric).
+    check_sym: the SymmetricMatrix test (core.py:75-84) runs on the device (pevd_asymmetry)
+    instead of over the host copy.  Q comes back Fortran-ordered in conventional order and
+    C-ordered otherwise (pipeline.py:495, 503) -- the device transposes, not the host."""
     L = _lib.load()
     torch = _torch()
     a = np.asarray(a, dtype=np.float64)
     n = a.shape[0]
     oc = _lib.ORDER_CODES[order]
     bb = max(1, min(b, n - 1)) if n > 1 else 1
-    da = to_dev(a)
+    mem = a.T if a.flags.f_contiguous else np.ascontiguousarray(a)
+    da = torch.from_numpy(mem).cuda()     # (n, n): column-major A (or A^T)
+    if check_sym:
+        out = (ctypes.c_double * 2)()
+        _lib.check(L.pevd_asymmetry(n, _p(da), n, out, _stream()), "asymmetry check")
+        if out[0] > sym_tol * max(1.0, out[1]):
+            raise ValueError(f"asymmetry {out[0]:.3e} exceeds tolerance")
     lam = empty(n)
     q = empty(n, n) if want_vectors else None
     ws = workspace(L.pevd_syevd_workspace_bytes(n, bb, int(want_vectors), oc))
@@ -272,7 +285,17 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None):
     if rc == _lib.PEVD_ERR_CONVERGE:
         raise RuntimeError(L.pevd_last_error().decode())
     _lib.check(rc, "syevd")
-    return lam.cpu().numpy()[:n], (from_dev(q) if want_vectors else None), st
+    del ws, da
+    qh = None
+    if want_vectors:
+        if order == "conventional":
+            qh = q.cpu().numpy().T                    # Fortran order, no host copy
+        else:
+            qt = torch.empty_like(q)                  # C order: transposed on the device
+            _lib.check(L.pevd_transpose(n, n, _p(q), n, _p(qt), n, _stream()), "transpose")
+            del q
+            qh = qt.cpu().numpy()
+    return lam.cpu().numpy()[:n], qh, st
 
 
 def syevd_multi(a, workers: int, b: int, col_ranges, back_ranges, want_vectors=True,

@@ -37,6 +37,15 @@ from .messaging import BROADCAST, HOST, CommLedger, TraceLog
 from .schedule import back_plan_sizes, partition
 
 ORDERS = ("pipelined", "sequential", "conventional")
+HOST_CHECK_MAX_N = 4096  # above this the input's symmetry check runs on the device
+
+
+def _cuda_ready() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
 
 
 class PipelineError(RuntimeError):
@@ -109,10 +118,18 @@ def back_ranges(n: int, workers: int, back_skew: float):
 
 def run(a, cfg: PipelineConfig):
     """A = Q diag(lam) Q^T on the GPU; returns (EigenResult, events, ledger, counter)."""
+    device_check = False
     if isinstance(a, SymmetricMatrix):
         dense = a.data
     else:
-        dense = SymmetricMatrix.from_dense(np.asarray(a, dtype=np.float64)).data
+        arr = np.asarray(a, dtype=np.float64)
+        if arr.ndim == 2 and arr.shape[0] == arr.shape[1] and arr.shape[0] > HOST_CHECK_MAX_N \
+                and cfg.workers == 1 and _cuda_ready():
+            # large inputs: the SymmetricMatrix check (core.py:75-84) runs on the device after the
+            # copy the EVD needs anyway, instead of an n^2 host temporary; no host F-order copy
+            dense, device_check = arr, True
+        else:
+            dense = SymmetricMatrix.from_dense(arr).data
     n = int(dense.shape[0])
     partition(n, cfg.workers)  # raises ValueError for workers > n (schedule.py:26-27)
     b = min(cfg.b, n - 1) if n > 1 else 0
@@ -135,7 +152,8 @@ def run(a, cfg: PipelineConfig):
         return _run_multi(dense, n, b, cfg, device)
     t0 = time.perf_counter_ns()
     try:
-        lam, q, st = device.syevd(dense, max(b, 1), cfg.want_vectors, cfg.order)
+        lam, q, st = device.syevd(dense, max(b, 1), cfg.want_vectors, cfg.order,
+                                  check_sym=device_check)
     except ValueError:
         raise
     except RuntimeError as exc:  # non-convergence keeps the reference's exception type
@@ -152,15 +170,14 @@ def run(a, cfg: PipelineConfig):
             back = HOST if cfg.order == "pipelined" else 0
             trace.add(back, "SBR-Back", 0, ns(st.sbr_back_ms[0]), ns(st.sbr_back_ms[1]))
             trace.add(back, "BC-Back", 0, ns(st.bc_back_ms[0]), ns(st.bc_back_ms[1]))
-            trace.add(0, "FinalMultiply", 0, ns(st.final_ms[0]), ns(st.final_ms[1]))
+            if cfg.order != "conventional":  # conventional order has no final multiply
+                trace.add(0, "FinalMultiply", 0, ns(st.final_ms[0]), ns(st.final_ms[1]))
     ledger = CommLedger()  # one GPU: nothing moves between devices
     counter = _macs(st)
     result = EigenResult(lam=lam, Q=q if cfg.want_vectors else None,
                          vectors_computed=bool(cfg.want_vectors))
-    if cfg.want_vectors and cfg.order == "conventional":
-        result.Q = np.asfortranarray(result.Q)
-    elif cfg.want_vectors:
-        result.Q = np.ascontiguousarray(result.Q)  # pipeline.py:503 (C order)
+    # (device.syevd returns Q Fortran-ordered in conventional order, C-ordered otherwise:
+    #  pipeline.py:495, 503)
     if cfg.trace_path:
         trace.to_ndjson(cfg.trace_path)
     return result, trace.events(), ledger, counter

@@ -219,3 +219,40 @@ def test_row_accumulator_and_orders():
         u.validate_order(pkg.application_order(u, direction), direction)
     with pytest.raises(ValueError, match="dependency"):
         u.validate_order(pkg.application_order(u, "reordered")[::-1], "reordered")
+
+
+def test_large_input_checked_on_device():
+    """n > HOST_CHECK_MAX_N: the SymmetricMatrix check (core.py:75-84) runs on the device
+    (pevd_asymmetry) and the host array is not transposed; C- and F-ordered inputs give the
+    same eigenvalues, Q comes back in the reference's order per mode (pipeline.py:495, 503)."""
+    from paper_2511_16174_b200.pipeline import HOST_CHECK_MAX_N
+    n = HOST_CHECK_MAX_N + 100
+    a = _sym(n, 77)
+    res_c, _, _, _ = pkg.run(a, pkg.PipelineConfig(workers=1, b=32, order="pipelined"))
+    assert res_c.Q.flags.c_contiguous
+    res_f, _, _, _ = pkg.run(np.asfortranarray(a), pkg.PipelineConfig(workers=1, b=32,
+                                                                       order="conventional"))
+    assert res_f.Q.flags.f_contiguous
+    lam_ref = np.linalg.eigvalsh(a)
+    for r in (res_c, res_f):
+        np.testing.assert_allclose(r.lam, lam_ref, atol=10 * n * EPS * np.abs(lam_ref).max())
+    assert orc.backward_error(a, res_c.Q, res_c.lam) <= 1e-15
+    assert orc.orthogonality(res_f.Q) <= 1e-15
+    bad = a.copy()
+    bad[7, 3] += 1e-6
+    with pytest.raises(ValueError, match="asymmetry"):
+        pkg.run(bad, pkg.PipelineConfig(workers=1, b=32))
+
+
+def test_device_asymmetry_kernel_matches_numpy():
+    import ctypes
+    import torch
+    from paper_2511_16174_b200 import _lib
+    L = _lib.load()
+    for n in (1, 31, 33, 100, 1000):
+        g = np.random.default_rng(n).standard_normal((n, n))
+        d = torch.from_numpy(g.T.copy()).cuda()      # column-major g
+        out = (ctypes.c_double * 2)()
+        _lib.check(L.pevd_asymmetry(n, ctypes.c_void_p(d.data_ptr()), n, out, None), "asym")
+        assert out[0] == np.abs(g - g.T).max()
+        assert abs(out[1] - np.linalg.norm(g)) <= 1e-12 * np.linalg.norm(g)
