@@ -192,11 +192,12 @@ int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, int64_t ldy, cons
                        double* X, int64_t ldx, int64_t ncols, void* workspace, void* stream);
 
 /* BC-Back backtrans.py:277-310.  right: X (nrows x n, ldx) <- X Q_b ("reordered", i.e. the
- * transpose of Q_b^T X^T).  left: X (n x ncols, ldx) <- Q_b X ("conventional"; for b = 32 it runs
- * on X^T in the workspace, the kernel's coalesced layout).  The workspace
- * (pevd_bc_back_workspace_bytes(n, rows or cols)) holds scheduler counters, the Z factors of the
- * reflector blocks and that transpose. */
-int64_t pevd_bc_back_workspace_bytes(int64_t n, int64_t nrows);
+ * transpose of Q_b^T X^T).  left: X (n x ncols, ldx) <- Q_b X ("conventional"; for the DMMA
+ * bandwidths b in {8, 16, 24, 32} it runs on X^T in the workspace, the kernel's coalesced
+ * layout; other b apply the reflectors one by one).  The workspace
+ * (pevd_bc_back_workspace_bytes(n, rows or cols, b)) holds scheduler counters, the (V, Z)
+ * records of the reflector blocks and that transpose. */
+int64_t pevd_bc_back_workspace_bytes(int64_t n, int64_t nrows, int b);
 int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
                        int64_t ldx, int64_t nrows, void* workspace, void* stream);
 int pevd_bc_back_left(int64_t n, int b, const double* tau, const double* V, int vld, double* X,

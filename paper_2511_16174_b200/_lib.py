@@ -93,7 +93,7 @@ SIGNATURES = {
     "pevd_sbr_back_workspace_bytes": (_i64, [_i64, _int]),
     "pevd_sbr_back_form": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _vp, _vp]),
     "pevd_sbr_back_left": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp]),
-    "pevd_bc_back_workspace_bytes": (_i64, [_i64, _i64]),
+    "pevd_bc_back_workspace_bytes": (_i64, [_i64, _i64, _int]),
     "pevd_bc_back_right": (_int, [_i64, _int, _vp, _vp, _int, _vp, _i64, _i64, _vp, _vp]),
     "pevd_bc_back_left": (_int, [_i64, _int, _vp, _vp, _int, _vp, _i64, _i64, _vp, _vp]),
     "pevd_asymmetry": (_int, [_i64, _vp, _i64, ctypes.POINTER(_dbl), _vp]),

@@ -133,7 +133,7 @@ Layout plan_layout(void* base, int64_t n, int b, int want_vectors, int order) {
   L.ws_bc = c.take(bc_ws_bytes(n, b));
   L.ws_dc = c.take(bisect ? stebz_ws_bytes(n) : stedc_ws_bytes(n));
   L.ws_back = c.take(sbr_back_ws_bytes(n, b));
-  L.ws_bcb = c.take(bc_back_ws_bytes(n, n));
+  L.ws_bcb = c.take(bc_back_ws_bytes(n, n, b));
   L.total = c.off;
   return L;
 }
@@ -322,7 +322,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     //      of every BC-Back block; they need only the SBR and chase outputs) on the side stream
     //      beside the divide and conquer
     // conventional order with b = 32 runs BC-Back on the transpose (the DMMA kernel's layout)
-    const bool conv_t = want_vectors && order == PEVD_ORDER_CONVENTIONAL && b == 32 && L.vld == 32;
+    const bool conv_t = want_vectors && order == PEVD_ORDER_CONVENTIONAL && bc_back_dmma_ok(b, L.vld);
     if (want_vectors && order == PEVD_ORDER_CONVENTIONAL) {
       cudaStreamWaitEvent(sb, ev[1].b, 0);
       flops_set_stage(ST_SBR_BACK);
@@ -601,8 +601,8 @@ int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, int64_t ldy, cons
 static int64_t ws_round(int64_t x) { return (x + 255) / 256 * 256; }
 
 // + room for the transpose of a left operand (the fast column-major BC-Back path, below)
-int64_t pevd_bc_back_workspace_bytes(int64_t n, int64_t nrows) {
-  return ws_round(bc_back_ws_bytes(n, nrows)) + n * nrows * 8 + 256;
+int64_t pevd_bc_back_workspace_bytes(int64_t n, int64_t nrows, int b) {
+  return ws_round(bc_back_ws_bytes(n, nrows, b)) + n * nrows * 8 + 256;
 }
 
 int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
@@ -613,9 +613,9 @@ int pevd_bc_back_right(int64_t n, int b, const double* tau, const double* V, int
 int pevd_bc_back_left(int64_t n, int b, const double* tau, const double* V, int vld, double* X,
                       int64_t ldx, int64_t ncols, void* workspace, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (b == 32 && vld == 32 && workspace && n >= 3 && ncols > 0) {
+  if (bc_back_dmma_ok(b, vld) && workspace && n >= 3 && ncols > 0) {
     // on the transpose: the DMMA kernel then reads X column-major (its coalesced pattern)
-    double* Xt = (double*)((char*)workspace + ws_round(bc_back_ws_bytes(n, ncols)));
+    double* Xt = (double*)((char*)workspace + ws_round(bc_back_ws_bytes(n, ncols, b)));
     PEVD_TRY(transpose(st, n, ncols, X, ldx, Xt, ncols));
     PEVD_TRY(bc_back_left_t(st, n, b, tau, V, vld, Xt, ncols, ncols, workspace));
     return transpose(st, ncols, n, Xt, ncols, X, ldx);

@@ -121,63 +121,106 @@ constexpr int Q4_SG = 64;
 // are prefetched into registers during the previous step and staged double-buffered.
 constexpr int WY_ROWS = 64;  // 8 warps x 8 rows
 constexpr int WY_THREADS = 256;
-// Shared-memory layouts, each conflict-free for its DMMA fragment pattern (a 64-bit warp access
-// is served per half-warp: lanes (r8 in 0..3, qd in 0..3) must hit 16 distinct 8-byte banks).
-// Window positions are relative to the block of 8 reflectors: reflector t (local index) covers
-// p = (t % 8) + idx, idx in [0, 32), so a block spans p in [0, 40).
-//  * va[h][t][s]:  P = X V operand, element p = 2 s + h of reflector t (zero outside its support;
-//                  lane reads t = tb + r8, s = 4 cc + qd: address 20 r8 + qd -> pitch 20)
-//  * zu[8 blk + s][p]: X += P Z^T operand, Z = V (-T)^T of the block (lane reads s = 2 qd + hh,
-//                  p = 8 cc + r8: address 84 qd + r8 -> pitch 42, 2 * 42 = 4 mod 16)
-constexpr int WY_PA = 20;
-constexpr int WY_PB = 42;
-constexpr int WY_ZB = 8 * WY_PB;  // doubles of Z per block: 8 rows s x 42 (40 positions p + pad),
-                                   // the shared zu layout, so a step's 8 blocks copy linearly
+// Per-bandwidth layout constants (B = b, a multiple of 8 up to 32).  A block of 8 staggered
+// reflectors spans 8 + B window columns.
+//  * V part vb[h][tl][s] (pitch PA): element p = 2 s + h of local reflector tl; the lanes of a
+//    half warp read PA r8 + qd: PA = 4 or 12 mod 16 makes them 16 distinct 8-byte banks
+//  * Z part zb[s][p] (pitch PB = 8 + B + 2): lanes read 2 qd PB + r8 (2 PB = 4 mod 16)
+constexpr int wy_pitch(int need) {  // smallest pitch >= need with pitch % 16 in {4, 12}
+  return (need % 16 == 4 || need % 16 == 12) ? need : wy_pitch(need + 1);
+}
 
-// Per (chase step j, block q of 8 sweeps) one 656-double record, in the kernel's shared layout:
-//   [0, 320)    V of the block: vb[h][tl][s] = element p = 2 s + h of local reflector tl
-//   [320, 656)  Z = V (-T)^T: zb[s][p] (pitch 42)
-// Every step's block count is padded to a multiple of 8 (zero records), so the 8 blocks of a
-// 64-sweep group at a step are ONE contiguous 41,984-byte record, moved by one bulk copy.
-constexpr int WY_VB = 2 * 8 * WY_PA;       // 320
-constexpr int WY_BLK = WY_VB + WY_ZB;      // 656
-constexpr int WY_STEP = 8 * WY_BLK;        // doubles per (group, step)
+template <int B>
+struct WyB {
+  static_assert(B % 8 == 0 && B >= 8 && B <= 32, "BC-Back DMMA kernel: b in {8, 16, 24, 32}");
+  static constexpr int SPAN = 8 + B;                       // window columns of one block
+  static constexpr int PA = wy_pitch(SPAN / 2);
+  static constexpr int PB = SPAN + 2;
+  static constexpr int VB = 2 * 8 * PA;
+  static constexpr int ZB = 8 * PB;
+  static constexpr int BLK = VB + ZB;                      // doubles per record
+  static constexpr int STEP = 8 * BLK;                     // doubles per (group, step)
+  static constexpr int NBT = SPAN / 8;                     // accumulator tiles per block
+  static constexpr int NWT = (Q4_SG + B) / 8;              // tiles of the window
+  static constexpr int SLT = B / 8;                        // tiles the window slides per step
+};
+static_assert(WyB<32>::PA == 20 && WyB<32>::BLK == 656, "b = 32 layout");
+static_assert(WyB<16>::PA % 16 == 12 || WyB<16>::PA % 16 == 4, "pitch");
+static_assert(WyB<8>::PA >= 8 && WyB<24>::PA >= 16, "pitch covers the span");
 
+template <int B>
 struct WySmem {
-  double vz[2][WY_STEP];     // [buf][blk][V | Z]
-  uint64_t full[2];          // bulk copy of buffer landed
-  int cnt[2];                // warps done with buffer
+  double vz[2][WyB<B>::STEP];  // [buf][blk][V | Z]
+  uint64_t full[2];            // bulk copy of buffer landed
+  int cnt[2];                  // warps done with buffer
   int unit;
 };
 
-// number of padded 8-sweep blocks before chase step j (b = 32): sum_{j' < j} 8 ceil(nb(j') / 8),
-// nb(j') = ceil((n - 2 - 32 j') / 8) = c - 4 j'
+// sum_{i < cnt} floor((a i + b) / m) for a, b >= 0, m > 0 (Euclid-like, O(log))
+__host__ __device__ __forceinline__ int64_t floor_sum(int64_t cnt, int64_t m, int64_t a, int64_t b) {
+  int64_t ans = 0;
+  while (true) {
+    if (a >= m) {
+      ans += (cnt - 1) * cnt / 2 * (a / m);
+      a %= m;
+    }
+    if (b >= m) {
+      ans += cnt * (b / m);
+      b %= m;
+    }
+    const int64_t y_max = a * cnt + b;
+    if (y_max < m) break;
+    cnt = y_max / m;
+    b = y_max % m;
+    const int64_t t = m;
+    m = a;
+    a = t;
+  }
+  return ans;
+}
+
+// records (padded 8-sweep blocks) before chase step j: sum_{j' < j} 8 ceil(nb(j') / 8) with
+// nb(j') = ceil((n - 2 - B j') / 8) = c - (B / 8) j'; every step's block count is padded to a
+// multiple of 8 (zero records) so the 8 blocks of a 64-sweep group are one contiguous record
+template <int B>
 __host__ __device__ __forceinline__ int64_t vz_block0(int64_t n, int64_t j) {
-  const int64_t c = (n - 2 + 7) / 8;
-  const int64_t A = (c + 7) / 8, Bo = (c + 3) / 8;   // ceil((c - 8m) / 8) for even / odd j'
-  const int64_t E = (j + 1) / 2, O = j / 2;
-  return 8 * (E * A - E * (E - 1) / 2 + O * Bo - O * (O - 1) / 2);
+  if (j <= 0) return 0;
+  const int64_t c = (n - 2 + 7) / 8, g = B / 8;
+  if (B == 32) {  // ceil((c - 4 j') / 8) alternates between two arithmetic series
+    const int64_t A = (c + 7) / 8, Bo = (c + 3) / 8;
+    const int64_t E = (j + 1) / 2, O = j / 2;
+    return 8 * (E * A - E * (E - 1) / 2 + O * Bo - O * (O - 1) / 2);
+  }
+  // sum_{i'=0}^{j-1} floor((c + 7 - g (j - 1) + g i') / 8), i' = j - 1 - j'
+  return 8 * floor_sum(j, 8, g, c + 7 - g * (j - 1));
+}
+
+// records of chase step j (its 8-sweep block count padded to a multiple of 8)
+template <int B>
+__host__ __device__ __forceinline__ int64_t vz_step_records(int64_t n, int64_t j) {
+  const int64_t nb = (n - 2 + 7) / 8 - (B / 8) * j;
+  return 8 * ((nb + 7) / 8);
 }
 
 // Z = V (-T)^T of every block of 8 consecutive sweeps at every chase step, so that a block
 // acts as X <- X (I - V T V^T) = X + (X V) Z^T; written with the block's V into its record
 // (record id = vz_block0(n, j) + q for block q of step j; padding records are zero).
-template <bool BACKWARD>
+template <int B, bool BACKWARD>
 __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
                                   const double* __restrict__ V, int vld, int64_t jcount,
                                   double* __restrict__ VZ) {
   // forward:  H_0 H_1 ... H_7 = I - V T V^T, T upper (LAPACK larft 'F')
   // backward: H_7 H_6 ... H_0 = I - V T V^T, T lower (larft 'B')
-  constexpr int B = 32;
-  const int64_t total = vz_block0(n, jcount);
+  using C = WyB<B>;
+  const int64_t total = vz_block0<B>(n, jcount);
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
        id += (int64_t)gridDim.x * blockDim.x) {
     int64_t lo = 0, hi = jcount;
     while (hi - lo > 1) {
       const int64_t mid = (lo + hi) >> 1;
-      if (vz_block0(n, mid) <= id) lo = mid; else hi = mid;
+      if (vz_block0<B>(n, mid) <= id) lo = mid; else hi = mid;
     }
-    const int64_t j = lo, q = id - vz_block0(n, j);
+    const int64_t j = lo, q = id - vz_block0<B>(n, j);
     const int64_t off = bc_slot_offset_dev(n, B, j);
     const int64_t nsw_j = n - 2 - j * B;
     double tv[8];
@@ -189,12 +232,12 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
       tv[s] = ok ? tau[off + i] : 0.0;
       v[s] = V + (ok ? (off + i) : off) * vld;
     }
-    double* rec = VZ + id * WY_BLK;
+    double* rec = VZ + id * C::BLK;
     // V part: vb[h][tl][s] = v_tl[2 s + h - tl] inside the support, 0 outside (and for absent
     // reflectors, whose tau is 0)
 #pragma unroll 1
-    for (int e = 0; e < WY_VB; ++e) {
-      const int h = e / (8 * WY_PA), tl = (e / WY_PA) % 8, ss = e % WY_PA;
+    for (int e = 0; e < C::VB; ++e) {
+      const int h = e / (8 * C::PA), tl = (e / C::PA) % 8, ss = e % C::PA;
       const int idx = 2 * ss + h - tl;
       rec[e] = (tv[tl] != 0.0 && idx >= 0 && idx < B) ? v[tl][idx] : 0.0;
     }
@@ -248,9 +291,9 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
       }
     }
     // Z[p][s] = sum_t v_t[p - t] * (-T)[s][t]
-    double* out = rec + WY_VB;
+    double* out = rec + C::VB;
 #pragma unroll 1
-    for (int p = 0; p < WY_PB; ++p) {
+    for (int p = 0; p < C::PB; ++p) {
       double vp[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t)
@@ -260,7 +303,7 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
         double acc = 0.0;
 #pragma unroll
         for (int t = 0; t < 8; ++t) acc = fma(vp[t], -T[s2][t], acc);
-        out[s2 * WY_PB + p] = (p < 40) ? acc : 0.0;
+        out[s2 * C::PB + p] = (p < C::SPAN) ? acc : 0.0;
       }
     }
   }
@@ -273,19 +316,21 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
 //   steps top-to-bottom, sweeps descending, backward T (the conventional grouped order of
 //   backtrans.py:232-235).  X column-major (X[row + col*ldx], rows contiguous down a column:
 //   64-byte segments per 8-row tile): the conventional application runs on the transpose.
-// Staging: each (group, step) record (V and Z of its 8 blocks, 42 KB) is ONE bulk copy on the
-// TMA engine into a double buffer, completing on an mbarrier.  No __syncthreads per step: every
-// warp waits only for the bytes of the step it is about to apply, and the LAST warp to finish
-// with a buffer (a shared counter) launches the copy of the step after next into it, so warps
-// drift freely within the one-step slack the double buffer gives.
-template <bool LEFT>
+// Staging: each (group, step) record (V and Z of its 8 blocks, 42 KB at b = 32) is ONE bulk copy
+// on the TMA engine into a double buffer, completing on an mbarrier.  No __syncthreads per step:
+// every warp waits only for the bytes of the step it is about to apply, and the LAST warp to
+// finish with a buffer (a shared counter) launches the copy of the step after next into it, so
+// warps drift freely within the one-step slack the double buffer gives.
+template <int B, bool LEFT>
 __global__ void __launch_bounds__(WY_THREADS, 2)
     bc_back_wy_kernel(int64_t n, const double* __restrict__ VZ, double* X, int64_t ldx,
                       int64_t nrows, int* counter, int* progress, int64_t nunits, int nrb) {
+  using C = WyB<B>;
   extern __shared__ __align__(128) unsigned char wyraw[];
-  WySmem& S = *reinterpret_cast<WySmem*>(wyraw);
-  constexpr int B = 32;
+  WySmem<B>& S = *reinterpret_cast<WySmem<B>*>(wyraw);
   constexpr int NW = WY_THREADS / 32;
+  constexpr int NWT = C::NWT, SLT = C::SLT, NBT = C::NBT;
+  constexpr uint32_t STEP_BYTES = C::STEP * 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int qd = lane & 3, r8 = lane >> 2;
   const int64_t nsw = n - 2;
@@ -298,8 +343,8 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
   }
   __syncthreads();
   uint32_t gstep = 0;  // steps this CTA has consumed (buffer = gstep & 1, parity = (gstep >> 1) & 1)
-  // record of step j of group k
-  auto rec = [&](int64_t k, int64_t j) { return VZ + (vz_block0(n, j) + 8 * k) * WY_BLK; };
+  // record of group k at the step whose padded block prefix is `off`
+  auto rec = [&](int64_t k, int64_t off) { return VZ + (off + 8 * k) * C::BLK; };
   for (;;) {
     if (tid == 0) S.unit = atomicAdd(counter, 1);
     __syncthreads();
@@ -312,13 +357,18 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
     const int64_t i0 = k * Q4_SG;
     const int64_t jmax = (n - 3 - i0) / B;
     const int64_t jfirst = LEFT ? 0 : jmax;
+    // block prefix of the step two ahead of the current one, advanced by one step per step
+    // (uniform over the CTA; the refilling warp uses it)
+    const int64_t dj = LEFT ? 1 : -1;
+    int64_t off2 = (jmax >= 2) ? vz_block0<B>(n, jfirst + 2 * dj) : 0;
     if (tid == 0) {
       // the unit's first two steps (the buffers are free: every warp passed the barrier above)
       for (int64_t s2 = 0; s2 < 2 && s2 <= jmax; ++s2) {
         const uint32_t g = gstep + (uint32_t)s2;
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&S.full[g & 1], WY_STEP * 8);
-        bulk_g2s(S.vz[g & 1], rec(k, LEFT ? jfirst + s2 : jfirst - s2), WY_STEP * 8, &S.full[g & 1]);
+        mbar_arrive_expect_tx(&S.full[g & 1], STEP_BYTES);
+        bulk_g2s(S.vz[g & 1], rec(k, vz_block0<B>(n, jfirst + s2 * dj)), STEP_BYTES,
+                 &S.full[g & 1]);
       }
       if (ld_acquire(progress + rb) < (int)seq) {
         unsigned ns = 64;
@@ -333,9 +383,9 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
     double* x = X + (active ? row : 0);
     int64_t ws = i0 + 1 + jfirst * B;
     __syncthreads();  // progress acquired by tid 0 before anyone reads X
-    double w[12][2];
+    double w[NWT][2];
 #pragma unroll
-    for (int c = 0; c < 12; ++c)
+    for (int c = 0; c < NWT; ++c)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t col = ws + 8 * c + 2 * qd + h;
@@ -344,11 +394,16 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
     for (int64_t jj = 0; jj <= jmax; ++jj, ++gstep) {
       const bool more = jj < jmax;
       const int buf = gstep & 1;
+      const int64_t off2_now = off2;  // prefix of step jj + 2 (used by the refill below)
+      {  // ... and of step jj + 3 for the next iteration
+        const int64_t j2 = jfirst + (jj + 2) * dj;
+        off2 += LEFT ? vz_step_records<B>(n, j2) : -vz_step_records<B>(n, j2 - 1);
+      }
       // prefetch the next step's new window columns (registers)
-      double nx[4][2];
-      const int64_t nbase = LEFT ? ws + 3 * B : ws - B;
+      double nx[SLT][2];
+      const int64_t nbase = LEFT ? ws + 8 * NWT : ws - B;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < SLT; ++c)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int64_t col = nbase + 8 * c + 2 * qd + h;
@@ -356,32 +411,32 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
         }
       mbar_wait(&S.full[buf], (gstep >> 1) & 1);  // this step's V and Z have landed
       const double* vz = S.vz[buf];
-      // ---- apply the 8 blocks of this step: P = X V (10 DMMA), X += P Z^T (10 DMMA)
+      // ---- apply the 8 blocks of this step: P = X V (2 NBT DMMA), X += P Z^T (2 NBT DMMA)
 #pragma unroll
       for (int bb = 0; bb < Q4_SG / 8; ++bb) {
         const int blk = LEFT ? Q4_SG / 8 - 1 - bb : bb;
-        const double* vb = vz + blk * WY_BLK;
+        const double* vb = vz + blk * C::BLK;
         double p0 = 0.0, p1 = 0.0;
-        const double* v0 = vb + r8 * WY_PA + qd;
-        const double* v1 = v0 + 8 * WY_PA;
-// two interleaved chains (k-step parities) merged by a DADD: 26.0 TF/s at n = 32768 against
-        // 25.5 for one chain of 10 dependent DMMAs
+        const double* v0 = vb + r8 * C::PA + qd;
+        const double* v1 = v0 + 8 * C::PA;
+        // two interleaved chains (k-step parities) merged by a DADD: 26.0 TF/s at n = 32768
+        // against 25.5 for one chain of 10 dependent DMMAs (b = 32)
         double e0 = 0.0, e1 = 0.0;
 #pragma unroll
-        for (int cc = 0; cc < 5; ++cc) {
+        for (int cc = 0; cc < NBT; ++cc) {
           const double a = v0[4 * cc], c = v1[4 * cc];
           dmma884(p0, p1, w[blk + cc][0], a);
           dmma884(e0, e1, w[blk + cc][1], c);
         }
         p0 += e0;
         p1 += e1;
-        const double* z0 = vb + WY_VB + (2 * qd) * WY_PB + r8;
-        const double* z1 = z0 + WY_PB;
-        // all five tiles' first k-step, then the second: two updates of a tile are 5 DMMAs apart
+        const double* z0 = vb + C::VB + (2 * qd) * C::PB + r8;
+        const double* z1 = z0 + C::PB;
+        // all tiles' first k-step, then the second: two updates of a tile are NBT DMMAs apart
 #pragma unroll
-        for (int cc = 0; cc < 5; ++cc) dmma884(w[blk + cc][0], w[blk + cc][1], p0, z0[8 * cc]);
+        for (int cc = 0; cc < NBT; ++cc) dmma884(w[blk + cc][0], w[blk + cc][1], p0, z0[8 * cc]);
 #pragma unroll
-        for (int cc = 0; cc < 5; ++cc) dmma884(w[blk + cc][0], w[blk + cc][1], p1, z1[8 * cc]);
+        for (int cc = 0; cc < NBT; ++cc) dmma884(w[blk + cc][0], w[blk + cc][1], p1, z1[8 * cc]);
       }
       // ---- done with this buffer: the last warp refills it with the step after next
       __syncwarp();
@@ -391,51 +446,50 @@ __global__ void __launch_bounds__(WY_THREADS, 2)
           S.cnt[buf] = 0;
           if (jj + 2 <= jmax) {
             fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&S.full[buf], WY_STEP * 8);
-            bulk_g2s(S.vz[buf], rec(k, LEFT ? jfirst + jj + 2 : jfirst - jj - 2), WY_STEP * 8,
-                     &S.full[buf]);
+            mbar_arrive_expect_tx(&S.full[buf], STEP_BYTES);
+            bulk_g2s(S.vz[buf], rec(k, off2_now), STEP_BYTES, &S.full[buf]);
           }
         }
       }
-      // ---- slide by b = 32 (4 tiles): the trailing 4 tiles (right) / leading 4 tiles (left)
+      // ---- slide by b (SLT tiles): the trailing SLT tiles (right) / leading SLT tiles (left)
       //      are final for this group
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < SLT; ++c)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int cw = LEFT ? c : c + 8;
+          const int cw = LEFT ? c : c + NWT - SLT;
           const int64_t col = ws + 8 * cw + 2 * qd + h;
           if (active && col < n) x[col * ldx] = w[cw][h];
         }
       if (more) {
         if (!LEFT) {
 #pragma unroll
-          for (int c = 11; c >= 4; --c) {
-            w[c][0] = w[c - 4][0];
-            w[c][1] = w[c - 4][1];
+          for (int c = NWT - 1; c >= SLT; --c) {
+            w[c][0] = w[c - SLT][0];
+            w[c][1] = w[c - SLT][1];
           }
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < SLT; ++c) {
             w[c][0] = nx[c][0];
             w[c][1] = nx[c][1];
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            w[c][0] = w[c + 4][0];
-            w[c][1] = w[c + 4][1];
+          for (int c = 0; c < NWT - SLT; ++c) {
+            w[c][0] = w[c + SLT][0];
+            w[c][1] = w[c + SLT][1];
           }
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            w[8 + c][0] = nx[c][0];
-            w[8 + c][1] = nx[c][1];
+          for (int c = 0; c < SLT; ++c) {
+            w[NWT - SLT + c][0] = nx[c][0];
+            w[NWT - SLT + c][1] = nx[c][1];
           }
         }
         ws += LEFT ? B : -B;
       } else {
 #pragma unroll
-        for (int c = 0; c < 12; ++c) {
-          if (LEFT ? c < 4 : c >= 8) continue;  // already stored above
+        for (int c = 0; c < NWT; ++c) {
+          if (LEFT ? c < SLT : c >= NWT - SLT) continue;  // already stored above
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int64_t col = ws + 8 * c + 2 * qd + h;
@@ -727,42 +781,58 @@ int transpose(cudaStream_t st, int64_t rows, int64_t cols, const double* in, int
 
 static int64_t wy_counter_bytes(int64_t nrows) { return ((nrows / 32 + 64) * 4 + 255) / 256 * 256; }
 
-int64_t bc_back_ws_bytes(int64_t n, int64_t nrows) {
-  // counters + the (V, Z) record of every padded block of 8 sweeps at every chase step
-  const int64_t jcount = n >= 3 ? (n - 3) / 32 + 1 : 1;
-  return wy_counter_bytes(nrows) + (n >= 3 ? vz_block0(n, jcount) : 0) * (int64_t)WY_BLK * 8 + 256;
+bool bc_back_dmma_ok(int b, int vld) { return (b == 8 || b == 16 || b == 24 || b == 32) && vld >= b; }
+
+template <int B>
+static int64_t wy_records(int64_t n) {
+  return n >= 3 ? vz_block0<B>(n, (n - 3) / B + 1) * (int64_t)WyB<B>::BLK : 0;
 }
 
-// The DMMA compact-WY BC-Back (b = 32, vld = 32): X <- X Q_b (LEFT = false) or Xt <- Xt Q_b^T
-// (LEFT = true, the conventional application on the transpose).  `prepared`: the counters and
-// the (V, Z) records of ws were already built by a call with X == nullptr (depends on the chase
-// output only, so the orchestrators run it beside the divide and conquer).
-template <bool LEFT>
+int64_t bc_back_ws_bytes(int64_t n, int64_t nrows, int b) {
+  // counters + the (V, Z) record of every padded block of 8 sweeps at every chase step
+  int64_t rec = 0;
+  switch (b) {
+    case 8: rec = wy_records<8>(n); break;
+    case 16: rec = wy_records<16>(n); break;
+    case 24: rec = wy_records<24>(n); break;
+    case 32: rec = wy_records<32>(n); break;
+    default: rec = 0;  // the reflector-by-reflector kernels need no workspace
+  }
+  return wy_counter_bytes(nrows) + rec * 8 + 256;
+}
+
+// The DMMA compact-WY BC-Back: X <- X Q_b (LEFT = false) or Xt <- Xt Q_b^T (LEFT = true, the
+// conventional application on the transpose).  `prepared`: the counters and the (V, Z) records
+// of ws were already built by a call with X == nullptr (they depend on the chase output only,
+// so the orchestrators run that beside the divide and conquer).
+template <int B, bool LEFT>
 static int bc_back_wy_launch(cudaStream_t st, int64_t n, const double* tau, const double* V,
-                             double* X, int64_t ldx, int64_t nrows, void* ws, bool prepared) {
+                             int vld, double* X, int64_t ldx, int64_t nrows, void* ws,
+                             bool prepared) {
+  using C = WyB<B>;
   const int nrb = (int)cdiv(nrows, WY_ROWS);
   const int64_t ngroups = cdiv(n - 2, Q4_SG);
   const int64_t nunits = ngroups * nrb;
   int* counter = (int*)ws;
   int* progress = counter + 32;
-  const int64_t jcount = (n - 3) / 32 + 1;
+  const int64_t jcount = (n - 3) / B + 1;
   double* VZ = (double*)((char*)ws + wy_counter_bytes(nrows));
-  const int64_t nrec = vz_block0(n, jcount);
+  const int64_t nrec = vz_block0<B>(n, jcount);
   if (!prepared) {
     PEVD_CUDA(cudaMemsetAsync(ws, 0, (size_t)(nrb + 32) * 4, st));
-    wy_tfactor_kernel<LEFT><<<(unsigned)std::min<int64_t>(cdiv(nrec, 128), 16384), 128, 0, st>>>(
-        n, tau, V, 32, jcount, VZ);
+    wy_tfactor_kernel<B, LEFT><<<(unsigned)std::min<int64_t>(cdiv(nrec, 128), 16384), 128, 0, st>>>(
+        n, tau, V, vld, jcount, VZ);
     PEVD_LAUNCH_CHECK();
   }
   if (X == nullptr) return OK;  // preparation only
-  // executed: 20 DMMA (10240 flops) per 8 rows per (unpadded) block of 8 reflectors
+  // executed: 4 NBT DMMA (512 flops each) per 8 rows per (unpadded) block of 8 reflectors
   {
     int64_t nblk = 0;
-    for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(n - 2 - j * 32, 8);
-    flops_add(1280.0 * (double)nrows * (double)nblk);
+    for (int64_t j = 0; j < jcount; ++j) nblk += cdiv(n - 2 - j * B, 8);
+    flops_add(4.0 * C::NBT * 512.0 / 8.0 * (double)nrows * (double)nblk);
   }
-  auto kfn = bc_back_wy_kernel<LEFT>;
-  const size_t smem = sizeof(WySmem);
+  auto kfn = bc_back_wy_kernel<B, LEFT>;
+  const size_t smem = sizeof(WySmem<B>);
   static int attr_dev = -1;
   int dev;
   PEVD_CUDA(cudaGetDevice(&dev));
@@ -783,11 +853,23 @@ static int bc_back_wy_launch(cudaStream_t st, int64_t n, const double* tau, cons
   return OK;
 }
 
+template <bool LEFT>
+static int bc_back_wy_dispatch(cudaStream_t st, int64_t n, int b, const double* tau,
+                               const double* V, int vld, double* X, int64_t ldx, int64_t nrows,
+                               void* ws, bool prepared) {
+  switch (b) {
+    case 8: return bc_back_wy_launch<8, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
+    case 16: return bc_back_wy_launch<16, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
+    case 24: return bc_back_wy_launch<24, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
+    default: return bc_back_wy_launch<32, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
+  }
+}
+
 int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                   double* X, int64_t ldx, int64_t nrows, void* ws) {
   if (n < 3 || nrows <= 0 || b < 2) return OK;
-  if (b == 32 && vld == 32 && ws)  // DMMA compact-WY kernel (fully asynchronous)
-    return bc_back_wy_launch<false>(st, n, tau, V, X, ldx, nrows, ws, false);
+  if (bc_back_dmma_ok(b, vld) && ws)  // DMMA compact-WY kernel (fully asynchronous)
+    return bc_back_wy_dispatch<false>(st, n, b, tau, V, vld, X, ldx, nrows, ws, false);
   // any other b (or a padded reflector stride): one thread per row, reflector by reflector
   flops_add(4.0 * b * (double)bc_num_reflectors(n, b) * (double)nrows);
   bc_back_right_generic<<<(unsigned)cdiv(nrows, 128), 128, 0, st>>>(n, b, tau, V, vld, X, ldx,
@@ -811,12 +893,12 @@ int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const dou
 
 int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                    double* Xt, int64_t ldx, int64_t nrows, void* ws, bool prepared) {
-  if (!(b == 32 && vld == 32 && ws)) {  // only the DMMA kernel has the transposed layout
-    set_error("bc_back_left_t: needs b = 32, vld = 32 and a workspace");
+  if (!(bc_back_dmma_ok(b, vld) && ws)) {  // only the DMMA kernel has the transposed layout
+    set_error("bc_back_left_t: needs b in {8, 16, 24, 32} and a workspace");
     return ERR_VALUE;
   }
   if (n < 3 || nrows <= 0) return OK;
-  return bc_back_wy_launch<true>(st, n, tau, V, Xt, ldx, nrows, ws, prepared);
+  return bc_back_wy_dispatch<true>(st, n, b, tau, V, vld, Xt, ldx, nrows, ws, prepared);
 }
 
 }  // namespace pevd

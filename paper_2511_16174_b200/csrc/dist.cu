@@ -631,7 +631,7 @@ int dist_syevd(Comm& C, int64_t n, int b, double* blk, int64_t ldb, const int64_
     K.ws_bc = A.take<char>(bc_ws_bytes(n, b));
     K.ws_dc = A.take<char>(bisect ? stebz_ws_bytes(n) : stedc_ws_bytes(n));
     K.ws_back = want_vectors ? A.take<char>(sbr_back_ws_bytes(n, b)) : nullptr;
-    K.ws_bcb = want_vectors ? A.take<char>(bc_back_ws_bytes(n, std::max<int64_t>(nbk, 1))) : nullptr;
+    K.ws_bcb = want_vectors ? A.take<char>(bc_back_ws_bytes(n, std::max<int64_t>(nbk, 1), b)) : nullptr;
   };
   carve(ar);  // sizes
   Arena real;
@@ -705,7 +705,7 @@ int dist_syevd(Comm& C, int64_t n, int b, double* blk, int64_t ldb, const int64_
       flops_set_stage(ST_SBR_BACK);
       if ((rc = sbr_back_prepare(K.bs, n, b, K.Ystair, n, K.Tall, K.ws_back))) break;
       flops_set_stage(ST_BC_BACK);
-      if (nbk > 0 && b == 32 &&
+      if (nbk > 0 && bc_back_dmma_ok(b, K.vld) &&
           (rc = bc_back_left_t(K.bs, n, b, K.tau, K.V, K.vld, nullptr, nbk, nbk, K.ws_bcb, false)))
         break;
     } else if (want_vectors && nbk > 0) {
@@ -738,7 +738,7 @@ int dist_syevd(Comm& C, int64_t n, int b, double* blk, int64_t ldb, const int64_
         double* Xt = (double*)K.ws_dc;  // the D&C's ping-pong buffer is free now
         flops_set_stage(ST_BC_BACK);
         sp = stage_span(TR_BC_BACK, cs);
-        if (b == 32) {  // the DMMA kernel on the transpose (its coalesced pattern)
+        if (bc_back_dmma_ok(b, K.vld)) {  // the DMMA kernel on the transpose (its coalesced pattern)
           if ((rc = transpose(cs, n, nbk, K.Qd + bl0 * n, n, Xt, nbk))) break;
           if ((rc = bc_back_left_t(cs, n, b, K.tau, K.V, K.vld, Xt, nbk, nbk, K.ws_bcb, true)))
             break;

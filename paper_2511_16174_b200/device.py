@@ -231,7 +231,7 @@ def bc_back_right(n, b, tau, V, x):
     dt = torch.from_numpy(np.ascontiguousarray(tau)).cuda()
     dv = torch.from_numpy(np.ascontiguousarray(V).reshape(-1)).cuda()
     dx = to_dev(x)
-    ws = workspace(L.pevd_bc_back_workspace_bytes(n, x.shape[0]))
+    ws = workspace(L.pevd_bc_back_workspace_bytes(n, x.shape[0], b))
     rc = L.pevd_bc_back_right(n, b, _p(dt), _p(dv), vld, _p(dx), x.shape[0], x.shape[0], _p(ws),
                               _stream())
     _lib.check(rc, "bc_back_right")
@@ -247,7 +247,7 @@ def bc_back_left(n, b, tau, V, x):
     dt = torch.from_numpy(np.ascontiguousarray(tau)).cuda()
     dv = torch.from_numpy(np.ascontiguousarray(V).reshape(-1)).cuda()
     dx = to_dev(x)
-    ws = workspace(L.pevd_bc_back_workspace_bytes(n, x.shape[1]))
+    ws = workspace(L.pevd_bc_back_workspace_bytes(n, x.shape[1], b))
     rc = L.pevd_bc_back_left(n, b, _p(dt), _p(dv), vld, _p(dx), x.shape[0], x.shape[1], _p(ws),
                              _stream())
     _lib.check(rc, "bc_back_left")

@@ -123,7 +123,8 @@ def test_stedc_matches_reference_solver(case):
         assert col[np.argmax(np.abs(col))] > 0
 
 
-@pytest.mark.parametrize("n,b", [(24, 3), (64, 8), (130, 32), (500, 32), (701, 32)])
+@pytest.mark.parametrize("n,b", [(24, 3), (64, 8), (130, 32), (500, 32), (701, 32), (333, 8),
+                                 (400, 16), (515, 24), (257, 12)])
 def test_bc_back_matches_oracle(n, b):
     rng = np.random.default_rng(n)
     a = rng.standard_normal((n, n))

@@ -37,7 +37,7 @@ def refl(n, b, seed):
 
 
 def apply(fn, n, tau, V, X):
-    ws = torch.empty(L.pevd_bc_back_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(L.pevd_bc_back_workspace_bytes(n, n, 32), dtype=torch.uint8, device="cuda")
     _lib.check(fn(n, 32, P(tau.data_ptr()), P(V.data_ptr()), 32, P(X.data_ptr()), n, n,
                   P(ws.data_ptr()), P(torch.cuda.current_stream().cuda_stream)), "bc_back")
 

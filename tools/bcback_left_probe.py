@@ -12,6 +12,6 @@ ws = torch.empty(L.pevd_bc_workspace_bytes(n, b), dtype=torch.uint8, device="cud
 s = P(torch.cuda.current_stream().cuda_stream)
 _lib.check(L.pevd_bc(n, b, P(bands.data_ptr()), P(d.data_ptr()), P(e.data_ptr()), P(tau.data_ptr()), P(V.data_ptr()), 32, P(ws.data_ptr()), s), "bc")
 X = torch.randn((n, n), dtype=torch.float64, device="cuda")
-ws = torch.empty(L.pevd_bc_back_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+ws = torch.empty(L.pevd_bc_back_workspace_bytes(n, n, 32), dtype=torch.uint8, device="cuda")
 _lib.check(L.pevd_bc_back_left(n, b, P(tau.data_ptr()), P(V.data_ptr()), 32, P(X.data_ptr()), n, n, P(ws.data_ptr()), s), "bcbl")
 torch.cuda.synchronize()

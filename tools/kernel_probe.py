@@ -71,7 +71,7 @@ def main():
         b = 32
         tau, V, vld, _ = reflectors(n, b)
         X = torch.randn((n, n), dtype=torch.float64, device="cuda")
-        ws = torch.empty(L.pevd_bc_back_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+        ws = torch.empty(L.pevd_bc_back_workspace_bytes(n, n, 32), dtype=torch.uint8, device="cuda")
         fn = L.pevd_bc_back_right if mode == "bcback" else L.pevd_bc_back_left
         ms, ts = timed(lambda: _lib.check(fn(n, b, ptr(tau), ptr(V), vld, ptr(X), n, n, ptr(ws),
                                              stream()), mode))
