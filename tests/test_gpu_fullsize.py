@@ -98,3 +98,56 @@ def test_planted_values_only(kind, n):
     err = float(np.abs(lam - lam_true).max())
     assert err <= 10 * n * EPS * float(np.abs(lam_true).max()), f"{kind}: |dlam| {err:.3e}"
     assert np.all(np.diff(lam) >= 0)
+
+
+def test_dc_standalone_65536_cluster0():
+    """Config c5's solver at its own size on one GPU: the planted Cluster0 matrix (one eigenvalue
+    lmax, the other 65535 at lmax / cond) is reduced to a tridiagonal T (SBR + chase), then the
+    divide and conquer runs on T alone (near-total deflation).  Checked: the planted
+    eigenvalues, and ||T Q - Q Lam||_F / (n ||T||_F), ||Q^T Q - I||_F / n on the device."""
+    import torch
+    from paper_2511_16174_b200 import _lib, matgen
+    L = _lib.load()
+    P = ctypes.c_void_p
+    n, b = 65536, 32
+    s = P(torch.cuda.current_stream().cuda_stream)
+    spec = matgen.SpectrumSpec("Cluster0", n, seed=5)
+    A, lam_true = matgen.generate(spec)
+    bands = torch.empty((b + 1) * n, dtype=torch.float64, device="cuda")
+    ws = torch.empty(L.pevd_sbr_workspace_bytes(n, b), dtype=torch.uint8, device="cuda")
+    _lib.check(L.pevd_sbr(n, b, P(A.data_ptr()), n, P(bands.data_ptr()), None, P(ws.data_ptr()),
+                          s), "sbr")
+    del A, ws
+    torch.cuda.empty_cache()
+    d = torch.empty(n, dtype=torch.float64, device="cuda")
+    e = torch.empty(n, dtype=torch.float64, device="cuda")
+    ws = torch.empty(L.pevd_bc_workspace_bytes(n, b), dtype=torch.uint8, device="cuda")
+    _lib.check(L.pevd_bc(n, b, P(bands.data_ptr()), P(d.data_ptr()), P(e.data_ptr()), None, None,
+                         32, P(ws.data_ptr()), s), "bc")
+    del ws, bands
+    d0, e0 = d.clone(), e[: n - 1].clone()
+    Q = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    ws = torch.empty(L.pevd_stedc_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+    _lib.check(L.pevd_stedc(n, P(d.data_ptr()), P(e.data_ptr()), P(Q.data_ptr()), n,
+                            P(ws.data_ptr()), s), "stedc")
+    del ws
+    torch.cuda.empty_cache()
+    lam = d.cpu().numpy()
+    err = float(np.abs(lam - lam_true).max())
+    assert err <= 10 * n * EPS * float(np.abs(lam_true).max()), f"|dlam| {err:.3e}"
+    # T Q - Q Lam, row block by row block (Q column-major: tensor row j = column j of Q)
+    tn = float(torch.sqrt(torch.sum(d0 * d0) + 2 * torch.sum(e0 * e0)))
+    res2, orth2 = 0.0, 0.0
+    blk = 4096
+    for j0 in range(0, n, blk):
+        Qb = Q[j0:j0 + blk]                                  # columns j0.. of Q: (cols, n)
+        TQ = Qb * d0[None, :]
+        TQ[:, :-1] += Qb[:, 1:] * e0[None, :]
+        TQ[:, 1:] += Qb[:, :-1] * e0[None, :]
+        R = TQ - Qb * d[j0:j0 + blk, None]
+        res2 += float(torch.sum(R * R))
+        G = Qb @ Q.t()                                       # (Q^T Q)[j0.., :]
+        G[:, j0:j0 + blk].diagonal().sub_(1.0)
+        orth2 += float(torch.sum(G * G))
+    res, orth = res2 ** 0.5 / (n * tn), orth2 ** 0.5 / n
+    assert res <= 1e-12 and orth <= 1e-12, f"residual {res:.2e}, ortho {orth:.2e}"
