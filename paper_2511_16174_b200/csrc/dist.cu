@@ -559,7 +559,11 @@ int Rank::sbr() {
     int64_t strip_hi = tl;
     if (x + nbl < R) strip_hi = tl + std::min<int64_t>(b, n - b - tl);
     PEVD_TRY(link(cs, ts));
+    // (the trailing update is a trace event of the helper lane: it runs beside the next panel's
+    //  QR and broadcast, whose Comm spans it overlaps)
+    const size_t tsp = open(TR_SBR, r, ts, 0, -1);
     PEVD_TRY(trailing(t0, tl, 2 * K, P1, P2, ru, strip_hi, cs, ts));
+    close(tsp, ts);
     trail_done = new_event();
     PEVD_CUDA(cudaEventRecord(trail_done, ts));
     set ^= 1;

@@ -167,24 +167,26 @@ def slot_offset(n: int, b: int, j: int) -> int:
 def slots_to_reference(n: int, b: int, tau, V):
     """Fixed slots -> the reference BulgeReflectorSet arrays (bulge.py:33-68): only recorded
     reflectors (tau != 0), canonical order (chase step j outer, sweep i inner)."""
-    i_l, j_l, r_l, l_l, t_l, v_l = [], [], [], [], [], []
     stride = ((b + 7) // 8) * 8
+    tau = np.asarray(tau).reshape(-1)
+    V = np.asarray(V).reshape(len(tau), -1) if len(tau) else np.zeros((0, stride))
+    js, is_ = [], []
     j = 0
-    while n - 2 - j * b > 0:
-        off = slot_offset(n, b, j)
-        for i in range(n - 2 - j * b):
-            t = tau[off + i]
-            if t != 0.0:
-                r0 = i + 1 + j * b
-                i_l.append(i); j_l.append(j); r_l.append(r0); l_l.append(min(b, n - r0))
-                t_l.append(t)
-                vv = np.zeros(stride)
-                vv[: V.shape[1]] = V[off + i][:stride]
-                v_l.append(vv)
+    while n - 2 - j * b > 0:        # slot(i, j) = offset(j) + i, i < n - 2 - j b
+        cnt = n - 2 - j * b
+        js.append(np.full(cnt, j, dtype=np.int64))
+        is_.append(np.arange(cnt, dtype=np.int64))
         j += 1
-    return dict(i=np.array(i_l, np.int64), j=np.array(j_l, np.int64),
-                row0=np.array(r_l, np.int64), len=np.array(l_l, np.int64),
-                tau=np.array(t_l), v=np.array(v_l).reshape(len(t_l), stride))
+    jj = np.concatenate(js) if js else np.zeros(0, np.int64)
+    ii = np.concatenate(is_) if is_ else np.zeros(0, np.int64)
+    keep = np.nonzero(tau[: len(jj)] != 0.0)[0]       # slot order is already (j, i) order
+    r0 = ii[keep] + 1 + jj[keep] * b
+    v = np.zeros((len(keep), stride))
+    w = min(stride, V.shape[1]) if len(keep) else 0
+    if len(keep):
+        v[:, :w] = V[keep, :w]
+    return dict(i=ii[keep], j=jj[keep], row0=r0, len=np.minimum(b, n - r0),
+                tau=tau[keep].copy(), v=v)
 
 
 def stedc(d, e):
@@ -254,6 +256,78 @@ def bc_back_left(n, b, tau, V, x):
     return from_dev(dx)
 
 
+STAGED_MIN_BYTES = 256 << 20  # larger host <-> device copies go through pinned staging
+STAGE_THREADS = 8
+STAGE_CHUNK = 1 << 22          # doubles per chunk (32 MB)
+
+
+def _staged_copy(host: np.ndarray, dev, to_device: bool):
+    """Host <-> device copy of a contiguous numpy array through pinned staging buffers, several
+    host threads at once (torch copies release the GIL).  A 19.3 GB pageable copy takes 3.6 s
+    host -> device and 10.3 s device -> host (first-touch page faults, one thread) on the pool's
+    B200 boxes; staged with 8 threads it is ~1.5 s (tools/h2d_probe.py)."""
+    import threading
+    torch = _torch()
+    flat_h = torch.from_numpy(host.reshape(-1))
+    flat_d = dev.view(-1)
+    N = flat_h.numel()
+    errs = []
+
+    def work(tid):
+        try:
+            st = torch.cuda.Stream()
+            bufs = [torch.empty(STAGE_CHUNK, dtype=torch.float64, pin_memory=True)
+                    for _ in range(2)]
+            evs = [None, None]
+            k = 0
+            for c0 in range(tid * STAGE_CHUNK, N, STAGE_THREADS * STAGE_CHUNK):
+                c1 = min(N, c0 + STAGE_CHUNK)
+                buf = bufs[k & 1][: c1 - c0]
+                if evs[k & 1] is not None:
+                    evs[k & 1].synchronize()
+                with torch.cuda.stream(st):
+                    if to_device:
+                        buf.copy_(flat_h[c0:c1])
+                        flat_d[c0:c1].copy_(buf, non_blocking=True)
+                    else:
+                        buf.copy_(flat_d[c0:c1], non_blocking=True)
+                        st.synchronize()
+                        flat_h[c0:c1].copy_(buf)
+                    e = torch.cuda.Event()
+                    e.record(st)
+                    evs[k & 1] = e
+                k += 1
+            st.synchronize()
+        except BaseException as exc:  # surfaced below
+            errs.append(exc)
+
+    torch.cuda.synchronize()
+    th = [threading.Thread(target=work, args=(i,)) for i in range(STAGE_THREADS)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+
+
+def _to_device(mem: np.ndarray):
+    torch = _torch()
+    if mem.nbytes < STAGED_MIN_BYTES:
+        return torch.from_numpy(mem).cuda()
+    out = torch.empty(mem.shape, dtype=torch.float64, device="cuda")
+    _staged_copy(mem, out, True)
+    return out
+
+
+def _to_host(t) -> np.ndarray:
+    if t.numel() * 8 < STAGED_MIN_BYTES:
+        return t.cpu().numpy()
+    out = np.empty(tuple(t.shape), dtype=np.float64)
+    _staged_copy(out, t.contiguous(), False)
+    return out
+
+
 def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=False,
           sym_tol=1e-13):
     """Whole single-GPU EVD through pevd_syevd_device: (lam, Q or None, PevdStats).
@@ -270,7 +344,7 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=F
     oc = _lib.ORDER_CODES[order]
     bb = max(1, min(b, n - 1)) if n > 1 else 1
     mem = a.T if a.flags.f_contiguous else np.ascontiguousarray(a)
-    da = torch.from_numpy(mem).cuda()     # (n, n): column-major A (or A^T)
+    da = _to_device(mem)                  # (n, n): column-major A (or A^T)
     if check_sym:
         out = (ctypes.c_double * 2)()
         _lib.check(L.pevd_asymmetry(n, _p(da), n, out, _stream()), "asymmetry check")
@@ -289,12 +363,12 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=F
     qh = None
     if want_vectors:
         if order == "conventional":
-            qh = q.cpu().numpy().T                    # Fortran order, no host copy
+            qh = _to_host(q).T                        # Fortran order, no host transpose
         else:
             qt = torch.empty_like(q)                  # C order: transposed on the device
             _lib.check(L.pevd_transpose(n, n, _p(q), n, _p(qt), n, _stream()), "transpose")
             del q
-            qh = qt.cpu().numpy()
+            qh = _to_host(qt)
     return lam.cpu().numpy()[:n], qh, st
 
 

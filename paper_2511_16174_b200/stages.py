@@ -92,11 +92,11 @@ def sym_rank2k_update(a, y, z, counter: FlopCounter | None = None, stage: str = 
         raise ValueError("shape mismatch in rank-2k update")
     yz = np.hstack([y, z])
     zy = np.hstack([z, y])
-    upd = device.dgemm(yz, zy, trans_b=True)
+    new = device.dgemm(yz, zy, alpha=-1.0, beta=1.0, c=a, trans_b=True)  # a - [y z][z y]^T
     il = np.tril_indices(m)
-    a[il] -= upd[il]
+    a[il] = new[il]                  # the lower triangle from the device ...
     iu = np.triu_indices(m, 1)
-    a[iu] = a.T[iu]
+    a[iu] = a.T[iu]                  # ... mirrored (a copy, no host arithmetic)
     if counter is not None:
         counter.add(stage, m * (m + 1) * k)
     return a
@@ -108,7 +108,7 @@ def form_z(a_trailing, w, y, counter: FlopCounter | None = None, stage: str = "S
     if a_trailing.shape != (m, m) or y.shape != (m, k):
         raise ValueError("shape mismatch in form_z")
     aw = device.dsymm_lower(a_trailing, w)
-    z = aw - 0.5 * device.dgemm(y, device.dgemm(w, aw, trans_a=True))
+    z = device.dgemm(y, device.dgemm(w, aw, trans_a=True), alpha=-0.5, beta=1.0, c=aw)
     if counter is not None:
         counter.add(stage, m * m * k + k * k * m + m * k * k)
     return z
@@ -121,7 +121,8 @@ def trailing_update(a2, y, z, mode: str = "symmetric", counter: FlopCounter | No
     if a2.shape != (m, m) or z.shape != (m, k):
         raise ValueError("shape mismatch in trailing update")
     if mode == "full":
-        a2 -= device.dgemm(np.hstack([y, z]), np.hstack([z, y]), trans_b=True)
+        a2[...] = device.dgemm(np.hstack([y, z]), np.hstack([z, y]), alpha=-1.0, beta=1.0, c=a2,
+                               trans_b=True)
         if counter is not None:
             counter.add(stage, 2 * m * m * k)
     elif mode == "symmetric":
@@ -155,7 +156,7 @@ def sbr_reduce(a: SymmetricMatrix, cfg: SbrConfig, counter: FlopCounter | None =
     for x, (c0, pw, t0) in enumerate(round_schedule(n, b)):
         Y = np.asfortranarray(ystair[t0:, c0:c0 + pw])
         T = device.t_block(tall, x, b, pw)
-        p = ReflectorPanel(W=Y @ T, Y=Y, col_offset=c0)
+        p = ReflectorPanel(W=device.dgemm(Y, T), Y=Y, col_offset=c0)
         p._T = T
         panels.append(p)
     if counter is not None:
@@ -270,11 +271,10 @@ class BulgeReflectorSet:
                 j += 1
             tau = np.zeros(max(nslot, 1))
             V = np.zeros((max(nslot, 1), _pad8(b)))
-            for p in range(len(self.tau)):
-                i, jj = int(self.i_idx[p]), int(self.j_idx[p])
-                s = device.slot_offset(n, b, jj) + i
-                tau[s] = self.tau[p]
-                V[s] = self.v[p]
+            jj = self.j_idx.astype(np.int64)
+            s_ = jj * (n - 2) - b * jj * (jj - 1) // 2 + self.i_idx.astype(np.int64)
+            tau[s_] = self.tau
+            V[s_] = self.v
             self._slots = (tau, V)
         return self._slots
 
@@ -448,8 +448,9 @@ def _form_qs(factors: SbrFactors) -> np.ndarray:
         t0 = n - m
         ystair[t0:, p.col_offset:p.col_offset + pw] = p.Y
         T = getattr(p, "_T", None)
-        if T is None:  # W = Y T  ->  T = argmin ||Y T - W|| (upper triangular)
-            T = np.triu(np.linalg.lstsq(p.Y, p.W, rcond=None)[0])
+        if T is None:  # W = Y T with Y unit lower trapezoidal: T = Y1^{-1} W1 (top pw x pw)
+            from scipy.linalg import solve_triangular
+            T = np.triu(solve_triangular(p.Y[:pw], p.W[:pw], lower=True, unit_diagonal=True))
         tall[x * b * b: x * b * b + pw * pw] = np.asarray(T).T.reshape(-1)
     return device.sbr_back_form(n, b, ystair, tall)
 

@@ -92,9 +92,21 @@ def test_usage_errors(tmp_path, capsys):
     assert "required" in capsys.readouterr().err
     assert main(["solve", str(tmp_path / "missing.evd1"),
                  "--out", str(tmp_path / "x")]) == EXIT_USAGE
-    assert main(["simulate", "--n", "64"]) == EXIT_USAGE
-    assert "not part of the B200 build" in capsys.readouterr().err
+    assert main(["simulate", "--n", "64", "--model", str(tmp_path / "nope.json")]) == EXIT_USAGE
+    assert "malformed cost model" in capsys.readouterr().err
 
+
+def test_simulate(tmp_path, capsys):
+    """cli.py simulate (reference cli.py:209-231): both orders priced, trace written."""
+    from paper_2511_16174_b200.messaging import TraceLog
+    from paper_2511_16174_b200.schedule import validate_trace
+    trace = tmp_path / "sim.ndjson"
+    for model in ("calibrated", "b200", "unit"):
+        assert main(["simulate", "--n", "4096", "--workers", "4", "--model", model,
+                     "--trace", str(trace)]) == 0
+        out = capsys.readouterr().out
+        assert "pipelined  makespan" in out and "ratio" in out
+        validate_trace(TraceLog.from_ndjson(trace), 4)
 
 # ---------------------------------------------------------------- solve / verify (GPU)
 @pytest.mark.gpu

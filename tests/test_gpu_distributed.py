@@ -71,6 +71,23 @@ def test_workers_in_one_process(G, n, b, order):
     np.testing.assert_array_equal(res.Q, res2.Q)
 
 
+def test_comm_overlaps_trailing_update():
+    """Lookahead, from the device events: the next group's first panel is factored and its
+    broadcast runs while the previous group's rank-2K trailing update (a helper-lane SBR event,
+    block = rank) is still running on the same rank."""
+    import paper_2511_16174_b200 as pkg
+    n, b, G = 1600, 32, 2
+    a = _sym(n, 1234)
+    res, events, ledger, _ = pkg.run(a, pkg.PipelineConfig(workers=G, b=b, order="conventional"))
+    assert orc.backward_error(a, res.Q, res.lam) <= 1e-15
+    upd = [e for e in events if e.worker == -1 and e.stage == "SBR"]
+    comm = [e for e in events if e.stage == "Comm"]
+    assert len(upd) >= G * 2
+    overlap = [(u, c) for u in upd for c in comm
+               if c.worker == u.block and c.t_start < u.t_end and u.t_start < c.t_end]
+    assert overlap, "no comm span overlaps a trailing update"
+
+
 def test_workers_values_only():
     import paper_2511_16174_b200 as pkg
     n, b = 300, 32

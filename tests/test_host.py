@@ -124,3 +124,22 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), f
+
+
+def test_product_house_vector_matches_golden_kats():
+    # the package's own house_vector (stages.py, the convention the kernels inline) against the
+    # reference's golden vectors and KATs (tests/test_core.py:33-44), not just the oracle's
+    G = np.load("tests/golden/golden.npz")
+    from paper_2511_16174_b200.stages import house_vector
+    idx = 0
+    while f"hv{idx}_x" in G:
+        v, tau, alpha = house_vector(G[f"hv{idx}_x"])
+        np.testing.assert_allclose(v, G[f"hv{idx}_v"], rtol=1e-15, atol=1e-15)
+        assert abs(tau - float(G[f"hv{idx}_tau"])) <= 1e-15 * max(1.0, abs(tau))
+        assert abs(alpha - float(G[f"hv{idx}_alpha"])) <= 1e-14 * max(1.0, abs(alpha))
+        idx += 1
+    assert idx > 0
+    v, tau, alpha = house_vector([0.0, 3.0, 4.0])
+    assert alpha == -5.0
+    v, tau, alpha = house_vector([3.5, 0.0, 0.0])
+    assert tau == 0.0 and alpha == 3.5
