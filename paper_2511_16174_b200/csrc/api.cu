@@ -318,15 +318,18 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
       if ((rc = bc_back_right(sback, n, b, L.tau, L.V, L.vld, L.Qs, n, n, L.ws_bcb))) break;
       cudaEventRecord(ev[4].b, sback);
     }
-    // ---- conventional: the back-transform preparations (SBR-Back T aggregation, the Z factor
-    //      of every BC-Back block; they need only the SBR and chase outputs) on the side stream
-    //      beside the divide and conquer
-    // conventional order with b = 32 runs BC-Back on the transpose (the DMMA kernel's layout)
+    // ---- conventional: the back-transform preparations on the side stream: the SBR-Back T
+    //      aggregation needs only the SBR output, so it runs beside the latency-bound chase
+    //      (enqueued after it, so the chase's cooperative grid is resident first); the Z factor
+    //      of every BC-Back block needs the chase output and runs beside the divide and conquer
+    // conventional order with b in {8, 16, 24, 32} runs BC-Back on the transpose (the DMMA
+    // kernel's layout)
     const bool conv_t = want_vectors && order == PEVD_ORDER_CONVENTIONAL && bc_back_dmma_ok(b, L.vld);
     if (want_vectors && order == PEVD_ORDER_CONVENTIONAL) {
-      cudaStreamWaitEvent(sb, ev[1].b, 0);
+      cudaStreamWaitEvent(sb, ev[0].b, 0);
       flops_set_stage(ST_SBR_BACK);
       if ((rc = sbr_back_prepare(sb, n, b, A, lda, L.Tall, L.ws_back))) break;
+      cudaStreamWaitEvent(sb, ev[1].b, 0);
       flops_set_stage(ST_BC_BACK);
       if (conv_t &&
           (rc = bc_back_left_t(sb, n, b, L.tau, L.V, L.vld, nullptr, n, n, L.ws_bcb, false)))

@@ -786,7 +786,8 @@ int gemm(cudaStream_t st, const GemmArgs& g0, double* ws, int64_t ws_elems) {
     const int ks = ws ? pick_ks(tiles, g.k, 2 * sms, 512, g.m * g.n, ws_elems) : 1;
     if (g.n <= 32) {
       // 4 warps of 32 x 32, BK = 16, 3 stages: 79 KB of shared memory -> 2 CTAs/SM; 8 LDS per
-      // 16 DMMA (27-28 TF/s at m = 24576-49152 vs 23-24 for 8 warps of 16 x 32)
+      // 16 DMMA (27-28 TF/s at m = 24576-49152 vs 23-24 for 8 warps of 16 x 32; 64-row tiles
+      // with 2 warps lose at every m from 4096 to 32768, e.g. 27.5 vs 28.8 TF/s at 16384)
       if (g.transB) PEVD_TRY((launch_fast<false, true, 128, 32, 16, 32, 32, 3, true>(st, g, ks, ks > 1 ? ws : nullptr)));
       else PEVD_TRY((launch_fast<false, false, 128, 32, 16, 32, 32, 3, true>(st, g, ks, ks > 1 ? ws : nullptr)));
       if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));

@@ -43,7 +43,7 @@ def apply(fn, n, tau, V, X):
 
 
 def main():
-    out = {"fma": os.environ.get("PEVD_BCB_FMA", "0")}
+    out = {}
     n = int(sys.argv[1])
     tau, V = refl(n, 32, 1)
     X0 = torch.randn((n, n), dtype=torch.float64, device="cuda")

@@ -1,6 +1,6 @@
 """Time individual device stages through the C ABI (CUDA events, after warm-up).
 
-  python tools/kernel_probe.py bcback 16384        # BC-Back on n x n rows (PEVD_BCBACK_G picks G)
+  python tools/kernel_probe.py bcback 16384        # BC-Back on n x n rows
   python tools/kernel_probe.py gemm 8192 8192 8192 [ta tb]
   python tools/kernel_probe.py sbr 16384
   python tools/kernel_probe.py stedc 16384
@@ -77,7 +77,7 @@ def main():
                                              stream()), mode))
         nref = L.pevd_bc_num_reflectors(n, b)
         flops = 4.0 * b * nref * n
-        out.update(n=n, G=os.environ.get("PEVD_BCBACK_G", "default"), ms=ms, ts=ts,
+        out.update(n=n, ms=ms, ts=ts,
                    tflops=flops / ms / 1e9)
     elif mode == "bc":
         n = int(sys.argv[2])
