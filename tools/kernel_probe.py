@@ -166,10 +166,22 @@ def main():
                                            ptr(ws), stream()), "pqr")
         ms, ts = timed(f, reps=3)
         out.update(m=m, us_per_panel=ms * 1e3 / 20)
-    elif mode == "stedc":
+    elif mode in ("stedc", "stedc_goe"):
         n = int(sys.argv[2])
         d0 = torch.randn(n, dtype=torch.float64, device="cuda")
         e = torch.randn(n, dtype=torch.float64, device="cuda")
+        if mode == "stedc_goe":  # the tridiagonal of a GOE matrix (SBR + chase): little deflation
+            b = 32
+            A = torch.randn((n, n), dtype=torch.float64, device="cuda")
+            A = (A + A.t()) / 2
+            bands = torch.empty((b + 1) * n, dtype=torch.float64, device="cuda")
+            ws = torch.empty(L.pevd_sbr_workspace_bytes(n, b), dtype=torch.uint8, device="cuda")
+            _lib.check(L.pevd_sbr(n, b, ptr(A), n, ptr(bands), None, ptr(ws), stream()), "sbr")
+            del A, ws
+            ws = torch.empty(L.pevd_bc_workspace_bytes(n, b), dtype=torch.uint8, device="cuda")
+            _lib.check(L.pevd_bc(n, b, ptr(bands), ptr(d0), ptr(e), None, None, 32, ptr(ws),
+                                 stream()), "bc")
+            del ws
         d = torch.empty_like(d0)
         Q = torch.empty((n, n), dtype=torch.float64, device="cuda")
         ws = torch.empty(L.pevd_stedc_workspace_bytes(n), dtype=torch.uint8, device="cuda")
