@@ -589,6 +589,7 @@ __global__ void merge_vectors(MergeBufs B) {
 // in), so the U columns landing there are one contiguous range [ja, jb).
 __global__ void merge_gemm_args(MergeBufs B, const double* X, int64_t ldx, double* Y, int64_t ldy,
                                 int nm, int64_t clo, int64_t chi) {
+  // (X here is the compacted operand buffer of merge_gather_cols: no column maps)
   const int mi = blockIdx.x * blockDim.x + threadIdx.x;
   if (mi >= nm) return;
   const int lo = B.lo[mi], mid = B.mid[mi], hi = B.hi[mi];
@@ -607,18 +608,43 @@ __global__ void merge_gemm_args(MergeBufs B, const double* X, int64_t ldx, doubl
   const int ja = lower(clo), jb = lower(chi);
   GemmArgs t{};
   t.m = mid - lo; t.n = jb - ja; t.k = k1 + k2; t.alpha = 1.0; t.beta = 0.0;
-  t.A = X + lo + (int64_t)lo * ldx; t.lda = ldx; t.amap = B.amapT + lo;
+  t.A = X + lo + (int64_t)lo * ldx; t.lda = ldx; t.amap = nullptr;
   t.B = U + (int64_t)ja * K; t.ldb = K;
   t.C = Y + lo + (int64_t)lo * ldy; t.ldc = ldy; t.cmap = cm + ja;
   t.transA = 0; t.transB = 0; t.amode = A_GENERAL; t.cmode = C_ALL;
   GemmArgs bt = t;
   bt.m = hi - mid; bt.k = k2 + k3;
-  bt.A = X + mid + (int64_t)lo * ldx; bt.amap = B.amapB + lo;
+  bt.A = X + mid + (int64_t)lo * ldx; bt.amap = nullptr;
   bt.B = U + k1 + (int64_t)ja * K;
   bt.C = Y + mid + (int64_t)lo * ldy;
   if (K == 0) { t.m = 0; bt.m = 0; }
   B.gargs[2 * mi] = t;
   B.gargs[2 * mi + 1] = bt;
+}
+
+// The merge GEMMs' A operands, compacted: the k1 + k2 columns of Q1 the top GEMM reads (through
+// amapT) and the k2 + k3 columns of Q2 the bottom one reads (amapB) are copied next to each
+// other, so the GEMMs stream plain column blocks (a gathered operand made every cp.async wait on
+// an index load: 10% of the grouped GEMM's stall samples).  Xc has X's block structure: the
+// top block at rows [lo, mid), the bottom one at rows [mid, hi), both from column lo.
+__global__ void merge_gather_cols(MergeBufs B, const double* __restrict__ X, int64_t ldx,
+                                  double* __restrict__ Xc, int64_t ldc) {
+  const int mi = blockIdx.y;
+  const int lo = B.lo[mi], mid = B.mid[mi], hi = B.hi[mi];
+  const int* mint = B.mint + mi * M_NINT;
+  const int K = mint[M_K], k1 = mint[M_K1], k2 = mint[M_K2], k3 = mint[M_K3];
+  const int c = blockIdx.x;
+  if (K == 0) return;
+  if (c < k1 + k2) {
+    const double* src = X + (int64_t)(lo + B.amapT[lo + c]) * ldx;
+    double* dst = Xc + (int64_t)(lo + c) * ldc;
+    for (int r = lo + threadIdx.x; r < mid; r += blockDim.x) dst[r] = src[r];
+  }
+  if (c < k2 + k3) {
+    const double* src = X + (int64_t)(lo + B.amapB[lo + c]) * ldx;
+    double* dst = Xc + (int64_t)(lo + c) * ldc;
+    for (int r = mid + threadIdx.x; r < hi; r += blockDim.x) dst[r] = src[r];
+  }
 }
 
 // deflated eigenpairs: copy the (rotated) column of X into its sorted output position
@@ -758,6 +784,7 @@ int64_t stedc_ws_bytes(int64_t n) {
   const int64_t nm_total = std::max<int64_t>(1, (int64_t)p.cuts.size());
   WsLayout w;
   w.add(n * n * 8);                 // second ping-pong buffer
+  w.add(n * n * 8);                 // compacted merge-GEMM operands
   w.add(u_elems_for(p) * 8);        // U
   w.add(24 * n * 8);                // per-element arrays
   w.add(nm_total * (M_NINT * 4 + 8 + 2 * (int64_t)sizeof(GemmArgs) + 8) + 4 * n * 4 + 4096);
@@ -782,6 +809,7 @@ int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int
   char* base = (char*)ws;
   WsLayout w;
   double* W2 = (double*)(base + w.add(n * n * 8));
+  double* Xc = (double*)(base + w.add(n * n * 8));
   double* Ubuf = (double*)(base + w.add(u_elems_for(p) * 8));
   double* arr = (double*)(base + w.add(24 * n * 8));
   char* misc = base + w.add(nm_total * (M_NINT * 4 + 8 + 2 * (int64_t)sizeof(GemmArgs) + 8) +
@@ -903,7 +931,9 @@ int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int
     PEVD_LAUNCH_CHECK();
     // only the last level writes Q: it alone is restricted to the wanted columns
     const int64_t clo = (l == nlev - 1) ? col_lo : 0, chi = (l == nlev - 1) ? col_hi : n;
-    merge_gemm_args<<<(unsigned)cdiv(nm, 128), 128, 0, st>>>(B, X, ldx, Y, ldy, nm, clo, chi);
+    merge_gather_cols<<<dim3((unsigned)smax, nm), 256, 0, st>>>(B, X, ldx, Xc, n);
+    PEVD_LAUNCH_CHECK();
+    merge_gemm_args<<<(unsigned)cdiv(nm, 128), 128, 0, st>>>(B, Xc, n, Y, ldy, nm, clo, chi);
     PEVD_LAUNCH_CHECK();
     PEVD_TRY(gemm_grouped(st, B.gargs, 2 * nm, hmax, smax));
     merge_deflated_copy<<<dim3((unsigned)smax, nm), 256, 0, st>>>(B, X, ldx, Y, ldy, clo, chi);
