@@ -32,14 +32,15 @@ namespace {
 
 constexpr int BMAX = 32;
 constexpr int LDS_ = BMAX + 1;
-constexpr int BC_WARPS = 2;  // warps per CTA
 constexpr int DONE = 1 << 30;
 
-struct WarpSmem {
+// one sweep per CTA (two warps)
+struct ChaseSmem {
   double SLC[2][BMAX * LDS_];  // left block / coupling block, ping-ponged between steps
   double SW[BMAX * LDS_];
   double vs[BMAX];
   double wv[BMAX];
+  double tau;
 };
 
 __global__ void band_to_work(int64_t n, int b, const double* __restrict__ bands,
@@ -73,28 +74,31 @@ __global__ void work_to_tridiag(int64_t n, const double* __restrict__ Bd, int64_
   }
 }
 
-__global__ void __launch_bounds__(BC_WARPS * 32)
+// Two warps per sweep.  Warp 0 owns the left block and the window (the Householder vector, the
+// left application on the bulge columns, the two-sided window update), warp 1 the coupling block
+// (its right application) and, on the sweep's last step, its store: the two halves of a step's
+// work and of its loads / stores run side by side, which shortens the per-step critical path the
+// whole wavefront waits on (~3n step slots).  Same arithmetic, in the same order, as one warp.
+__global__ void __launch_bounds__(64)
     bc_chase_kernel(int64_t n, int b, double* __restrict__ Bd, int64_t LDB, int* prog,
                     double* __restrict__ tau_out, double* __restrict__ V_out, int vld,
                     int64_t sweep_end, int64_t slot_n, int64_t slot_col0) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  WarpSmem& S = reinterpret_cast<WarpSmem*>(smraw)[threadIdx.x >> 5];
-  const int lane = threadIdx.x & 31;
+  ChaseSmem& S = *reinterpret_cast<ChaseSmem*>(smraw);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t gend = sweep_end < n - 2 ? sweep_end : n - 2;
-  const int64_t wglob = (int64_t)blockIdx.x * BC_WARPS + (threadIdx.x >> 5);
-  const int64_t total_warps = (int64_t)gridDim.x * BC_WARPS;
-  for (int64_t gi = wglob; gi < gend; gi += total_warps) {
+  const int64_t stp = LDB - 1;  // pointer step from one band column to the next, same row
+  for (int64_t gi = blockIdx.x; gi < gend; gi += gridDim.x) {
     // The coupling block of step j (rows [w0+L, w0+L+b) x columns [w0, w0+L)) IS the left block
     // of step j+1 of the same sweep, and nobody else touches it in between (the next sweep
     // reaches it only after this one completed step j+2): it stays in shared memory -- the two
     // buffers swap roles -- and is neither stored at step j nor reloaded at step j+1.
     int cur = 0;  // SLC[cur] = this step's left block, SLC[cur ^ 1] its coupling block
     for (int64_t j = 0; gi + 1 + j * b <= n - 2; ++j) {
-      // ---- wait for the predecessor sweep to complete step j+2.  Polling is a relaxed L2 load
-      //      (an acquire per poll would invalidate L1 on every iteration); once the flag is seen
-      //      one acquire load of it pairs with the producer's fence + flag store (release
-      //      pattern), and __syncwarp extends the order to the other lanes, whose band reads then
-      //      go through L2 (ld.cg).  (A fence.acq_rel here costs 5 ms more at n = 49152.)
+      // ---- wait for the predecessor sweep to complete step j+2 (both warps read band data).
+      //      Polling is a relaxed L2 load; once the flag is seen one acquire load of it pairs
+      //      with the producer's fence + flag store (release pattern), and __syncwarp extends
+      //      the order to the other lanes, whose band reads then go through L2 (ld.cg).
       if (gi > 0) {
         if (lane == 0) {
           const int need = (int)(j + 3);
@@ -110,111 +114,130 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
       const int nleft = (int)(w0 - cg);  // 1 (j = 0) or b
       const int64_t tend = (w0 + L + b < n) ? w0 + L + b : n;
       const int nT = (int)(tend - (w0 + L));
+      const bool last = gi + 1 + (j + 1) * b > n - 2;  // no step j+1 in this sweep
       // reflector (slot_col0 + gi, j) of the slot_n problem (a relayed tail writes straight into
       // the whole matrix's fixed slots)
       const int64_t slot = (int64_t)j * (slot_n - 2) - (int64_t)b * j * (j - 1) / 2 + slot_col0 + gi;
-
-      const bool last = gi + 1 + (j + 1) * b > n - 2;  // no step j+1 in this sweep
       double* SL = S.SLC[cur];
       double* SC = S.SLC[cur ^ 1];
-      // ---- stage the region with independent loads (one L2 round trip, not 3b); the left block
-      //      of a step j >= 1 is already in shared memory
-      double rl[BMAX], rw[BMAX], rc[BMAX];
-      {
-        // element q of this lane's row in each region: one pointer per region advanced by
-        // LDB - 1 per column (no 64-bit multiply per element)
-        const int64_t stp = LDB - 1;
+      // ---- stage the region with independent loads (one L2 round trip per warp, not 3b)
+      if (wid == 0) {
+        double rl[BMAX], rw[BMAX];
         const double* pl = Bd + cg * LDB + (w0 - cg) + lane;
         const double* pw = Bd + w0 * LDB + lane;
-        const double* pc = pw + L;
 #pragma unroll
         for (int q = 0; q < BMAX; ++q) {
           rl[q] = (j == 0 && q < nleft && lane < L) ? __ldcg(pl) : 0.0;
           rw[q] = (q < L && lane >= q && lane < L) ? __ldcg(pw) : 0.0;
-          rc[q] = (q < L && lane < nT) ? __ldcg(pc) : 0.0;
           pl += stp;
           pw += stp;
+        }
+#pragma unroll
+        for (int q = 0; q < BMAX; ++q) {
+          if (j == 0) SL[lane * LDS_ + q] = rl[q];
+          if (lane >= q) {
+            S.SW[lane * LDS_ + q] = rw[q];
+            S.SW[q * LDS_ + lane] = rw[q];
+          }
+        }
+      } else {
+        double rc[BMAX];
+        const double* pc = Bd + w0 * LDB + lane + L;
+#pragma unroll
+        for (int q = 0; q < BMAX; ++q) {
+          rc[q] = (q < L && lane < nT) ? __ldcg(pc) : 0.0;
           pc += stp;
         }
-      }
 #pragma unroll
-      for (int q = 0; q < BMAX; ++q) {
-        if (j == 0) SL[lane * LDS_ + q] = rl[q];
-        SC[lane * LDS_ + q] = rc[q];
-        if (lane >= q) {
-          S.SW[lane * LDS_ + q] = rw[q];
-          S.SW[q * LDS_ + lane] = rw[q];
+        for (int q = 0; q < BMAX; ++q) SC[lane * LDS_ + q] = rc[q];
+      }
+      __syncthreads();  // staged; a step j >= 1 left block (warp 1's last coupling) is visible
+      // ---- the Householder vector (warp 0)
+      if (wid == 0) {
+        const double x = (lane < L) ? SL[lane * LDS_] : 0.0;
+        const double tail = warp_sum((lane >= 1 && lane < L) ? x * x : 0.0);
+        if (tail == 0.0) {
+          if (lane == 0) S.tau = 0.0;  // nothing to annihilate: the reference records no reflector
+        } else {
+          const double x0 = __shfl_sync(0xffffffffu, x, 0);
+          const double nrm = sqrt(x0 * x0 + tail);
+          const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+          const double denom = x0 - alpha;
+          const double v = (lane == 0) ? 1.0 : ((lane < L) ? x / denom : 0.0);
+          const double vsq = 1.0 + warp_sum((lane >= 1) ? v * v : 0.0);
+          S.vs[lane] = v;
+          if (lane == 0) S.tau = 2.0 / vsq;
+          if (lane < L) SL[lane * LDS_] = (lane == 0) ? alpha : 0.0;
         }
       }
-      __syncwarp();
-      const double x = (lane < L) ? SL[lane * LDS_] : 0.0;
-      const double tail = warp_sum((lane >= 1 && lane < L) ? x * x : 0.0);
-      if (tail == 0.0) {
-        // nothing to annihilate: the reference records no reflector here (tau = 0 slot).  The
-        // left block still holds the previous step's coupling update (kept in shared memory,
-        // never stored), and on the last step the coupling block must reach memory too.
-        if (tau_out) {
-          if (lane == 0) tau_out[slot] = 0.0;
-          for (int r = lane; r < vld; r += 32) V_out[slot * vld + r] = (r == 0) ? 1.0 : 0.0;
+      __syncthreads();  // v and tau visible to both warps
+      const double tau = S.tau;
+      // (all staged entries outside the live L x L / nT x L region are zero and v is zero beyond
+      //  L, so every loop runs the full BMAX width without predicates; four partial sums break
+      //  the dependent-FMA chains)
+      if (wid == 0) {
+        if (tau != 0.0) {
+          const double v = S.vs[lane];
+          // ---- H from the left on the bulge columns strictly between (lane = column q)
+          if (lane >= 1 && lane < nleft) {
+            const int q = lane;
+            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+            for (int r = 0; r < BMAX; r += 4) {
+              d0 = fma(S.vs[r], SL[r * LDS_ + q], d0);
+              d1 = fma(S.vs[r + 1], SL[(r + 1) * LDS_ + q], d1);
+              d2 = fma(S.vs[r + 2], SL[(r + 2) * LDS_ + q], d2);
+              d3 = fma(S.vs[r + 3], SL[(r + 3) * LDS_ + q], d3);
+            }
+            const double dot = tau * ((d0 + d1) + (d2 + d3));
+#pragma unroll
+            for (int r = 0; r < BMAX; ++r) SL[r * LDS_ + q] -= dot * S.vs[r];
+          }
+          // ---- H A H on the window (lane = row r)
+          double u = 0.0;
+          {
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+            for (int c = 0; c < BMAX; c += 4) {
+              a0 = fma(S.SW[lane * LDS_ + c], S.vs[c], a0);
+              a1 = fma(S.SW[lane * LDS_ + c + 1], S.vs[c + 1], a1);
+              a2 = fma(S.SW[lane * LDS_ + c + 2], S.vs[c + 2], a2);
+              a3 = fma(S.SW[lane * LDS_ + c + 3], S.vs[c + 3], a3);
+            }
+            u = tau * ((a0 + a1) + (a2 + a3));
+          }
+          const double gam = 0.5 * tau * warp_sum(v * u);
+          const double w = u - gam * v;
+          S.wv[lane] = w;
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < BMAX; ++c) {
+            if (c <= lane) S.SW[lane * LDS_ + c] -= v * S.wv[c] + w * S.vs[c];
+          }
+          __syncwarp();
         }
-        const int64_t stp = LDB - 1;
-        if (j > 0) {
+        // ---- write back: the left block (it also carries the previous step's coupling update,
+        //      never stored) and, when a reflector was applied, the window; the reflector slot
+        if (tau != 0.0 || j > 0) {
           double* pl = Bd + cg * LDB + (w0 - cg) + lane;
+#pragma unroll 4
           for (int q = 0; q < nleft; ++q, pl += stp)
             if (lane < L) *pl = SL[lane * LDS_ + q];
         }
-        if (last) {
-          double* pc = Bd + w0 * LDB + lane + L;
-          for (int c = 0; c < L; ++c, pc += stp)
-            if (lane < nT) *pc = SC[lane * LDS_ + c];
+        if (tau != 0.0) {
+          double* pw = Bd + w0 * LDB + lane;
+#pragma unroll 4
+          for (int c = 0; c < L; ++c, pw += stp)
+            if (lane >= c && lane < L) *pw = S.SW[lane * LDS_ + c];
+        }
+        if (tau_out) {
+          if (lane == 0) tau_out[slot] = tau;
+          for (int r = lane; r < vld; r += 32)
+            V_out[slot * vld + r] = (tau != 0.0) ? ((r < L) ? S.vs[r] : 0.0) : (r == 0 ? 1.0 : 0.0);
         }
       } else {
-        const double x0 = __shfl_sync(0xffffffffu, x, 0);
-        const double nrm = sqrt(x0 * x0 + tail);
-        const double alpha = (x0 >= 0.0) ? -nrm : nrm;
-        const double denom = x0 - alpha;
-        const double v = (lane == 0) ? 1.0 : ((lane < L) ? x / denom : 0.0);
-        const double vsq = 1.0 + warp_sum((lane >= 1) ? v * v : 0.0);
-        const double tau = 2.0 / vsq;
-        S.vs[lane] = v;
-        if (lane < L) SL[lane * LDS_] = (lane == 0) ? alpha : 0.0;
-        __syncwarp();
-        // (all staged entries outside the live L x L / nT x L region are zero and v is zero
-        //  beyond L, so every loop below runs the full BMAX width without predicates; four
-        //  partial sums break the dependent-FMA chains)
-        // ---- H from the left on the bulge columns strictly between (lane = column q)
-        if (lane >= 1 && lane < nleft) {
-          const int q = lane;
-          double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-          for (int r = 0; r < BMAX; r += 4) {
-            d0 = fma(S.vs[r], SL[r * LDS_ + q], d0);
-            d1 = fma(S.vs[r + 1], SL[(r + 1) * LDS_ + q], d1);
-            d2 = fma(S.vs[r + 2], SL[(r + 2) * LDS_ + q], d2);
-            d3 = fma(S.vs[r + 3], SL[(r + 3) * LDS_ + q], d3);
-          }
-          const double dot = tau * ((d0 + d1) + (d2 + d3));
-#pragma unroll
-          for (int r = 0; r < BMAX; ++r) SL[r * LDS_ + q] -= dot * S.vs[r];
-        }
-        // ---- H A H on the window (lane = row r)
-        double u = 0.0;
-        {
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll
-          for (int c = 0; c < BMAX; c += 4) {
-            a0 = fma(S.SW[lane * LDS_ + c], S.vs[c], a0);
-            a1 = fma(S.SW[lane * LDS_ + c + 1], S.vs[c + 1], a1);
-            a2 = fma(S.SW[lane * LDS_ + c + 2], S.vs[c + 2], a2);
-            a3 = fma(S.SW[lane * LDS_ + c + 3], S.vs[c + 3], a3);
-          }
-          u = tau * ((a0 + a1) + (a2 + a3));
-        }
-        const double gam = 0.5 * tau * warp_sum(v * u);
-        const double w = u - gam * v;
-        S.wv[lane] = w;
         // ---- H from the right on the coupling rows (lane = row t)
-        {
+        if (tau != 0.0) {
           double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll
           for (int c = 0; c < BMAX; c += 4) {
@@ -227,44 +250,24 @@ __global__ void __launch_bounds__(BC_WARPS * 32)
 #pragma unroll
           for (int c = 0; c < BMAX; ++c) SC[lane * LDS_ + c] -= dot * S.vs[c];
         }
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c < BMAX; ++c) {
-          if (c <= lane) S.SW[lane * LDS_ + c] -= v * S.wv[c] + w * S.vs[c];
-        }
-        __syncwarp();
-        // ---- write back
-        {
-          // one pointer per region, advanced by LDB - 1 per column: no 64-bit multiplies in
-          // the store loops
-          const int64_t stp = LDB - 1;
-          double* pl = Bd + cg * LDB + (w0 - cg) + lane;
-#pragma unroll 4
-          for (int q = 0; q < nleft; ++q, pl += stp)
-            if (lane < L) *pl = SL[lane * LDS_ + q];
-          double* pw = Bd + w0 * LDB + lane;
-          double* pc = pw + L;
-#pragma unroll 4
-          for (int c = 0; c < L; ++c, pw += stp, pc += stp) {
-            if (lane >= c && lane < L) *pw = S.SW[lane * LDS_ + c];
-            if (last && lane < nT) *pc = SC[lane * LDS_ + c];
-          }
-        }
-        if (tau_out) {
-          if (lane == 0) tau_out[slot] = tau;
-          for (int r = lane; r < vld; r += 32) V_out[slot * vld + r] = (r < L) ? S.vs[r] : 0.0;
+        // the last step's coupling block has no next step to carry it: store it
+        if (last) {
+          double* pc = Bd + w0 * LDB + lane + L;
+          for (int c = 0; c < L; ++c, pc += stp)
+            if (lane < nT) *pc = SC[lane * LDS_ + c];
         }
       }
-      // ---- publish progress
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();  // orders the warp's band stores (after __syncwarp) before the flag
+      // ---- publish progress once both warps' stores are issued (the barrier orders warp 1's
+      //      stores before thread 0's gpu-scope fence, whose release covers them cumulatively)
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
         st_relaxed(prog + gi, (int)(j + 1));
       }
       cur ^= 1;  // this step's coupling block is the next step's left block
     }
-    __syncwarp();
-    if (lane == 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
       __threadfence();
       st_relaxed(prog + gi, DONE);
     }
@@ -320,7 +323,7 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
         nref += std::max<int64_t>(0, std::min<int64_t>(sweep_end, n - 2 - j * b));
       flops_add(14.0 * b * b * (double)nref);
     }
-    const size_t smem = sizeof(WarpSmem) * BC_WARPS;
+    const size_t smem = sizeof(ChaseSmem);
     auto kfn = bc_chase_kernel;
     static int attr_dev = -1;
     int dev;
@@ -330,8 +333,7 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
       attr_dev = dev;
     }
     int per_sm = 0;
-    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn,
-                                                            BC_WARPS * 32, smem));
+    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 64, smem));
     if (per_sm < 1) {
       set_error("bc_reduce: chase kernel cannot be resident");
       return ERR_CUDA;
@@ -340,12 +342,12 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
     // warp free when its turn comes, more would only add spinning warps next to the back stream
     // (cooperative: one full wave at most)
     const int64_t want_warps = std::min<int64_t>(n - 2, std::max<int64_t>(2 * n / (3 * b), 2 * num_sms()));
-    const int64_t need = cdiv(want_warps, BC_WARPS);
+    const int64_t need = want_warps;  // one sweep (two warps) per CTA
     const int grid = (int)std::min<int64_t>((int64_t)per_sm * num_sms(), need);
     int64_t n_ = n, sweep_end_ = sweep_end, LDB_ = LDB;
     int b_ = b, vld_ = vld;
     void* args[] = {&n_, &b_, &Bd, &LDB_, &prog, &tau, &V, &vld_, &sweep_end_, &slot_n, &slot_col0};
-    PEVD_CUDA(cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(BC_WARPS * 32), args,
+    PEVD_CUDA(cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(64), args,
                                           smem, st));
     PEVD_LAUNCH_CHECK();
   } else if (tau && n >= 3 && slot_n == n && slot_col0 == 0) {
