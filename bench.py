@@ -373,8 +373,12 @@ def run_b200_single(args):
             t = torch.tensor([ems], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
+        # pevd_syevd uploads the lower trapezoid of each 512-column block (include/pevd.h:
+        # only the lower triangle of A is read) and downloads Q slab by slab, overlapped with
+        # the last SBR-Back blocks (csrc/hostio.h)
+        h2d = sum(8 * (n - j0) * min(512, n - j0) for j0 in range(0, n, 512))
         e2e = {"value": round(world * 4 * n ** 3 / (ems * 1e-3) / 1e12, 4), "unit": "TFLOP/s",
-               "ms_per_step": round(ems, 1), "h2d_bytes_per_step": 8 * n * n,
+               "ms_per_step": round(ems, 1), "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8 * n * n + 8 * n}
     cpu = None
     if rank == 0 and not args.no_cpu:

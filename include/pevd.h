@@ -114,8 +114,19 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
                       int64_t ldq, int want_vectors, int order, void* workspace,
                       int64_t workspace_bytes, void* stream, pevd_stats* stats);
 
-/* HOST pointers (A column-major, lda); allocates device memory itself, copies in and out.
- * Q may be NULL when want_vectors == 0.  A is not modified. */
+/* As pevd_syevd_device, but Q (a DEVICE buffer it computes in) is also delivered to the HOST
+ * buffer Qh (column-major, ldqh >= n): in conventional order the last back-transformation runs
+ * in column slabs and each slab's copy overlaps the next slab's compute, so only the last
+ * slab's copy is exposed.  Pinned Qh is copied by the copy engines; pageable Qh through pinned
+ * staging chunks worked by several host threads (PEVD_STAGE_THREADS, default 8). */
+int pevd_syevd_device_host_q(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
+                             int64_t ldq, double* Qh, int64_t ldqh, int want_vectors, int order,
+                             void* workspace, int64_t workspace_bytes, void* stream,
+                             pevd_stats* stats);
+
+/* HOST pointers (A column-major, lda; only its lower triangle is read and copied to the
+ * device); allocates device memory itself.  Q comes back as pevd_syevd_device_host_q delivers
+ * it.  Q may be NULL when want_vectors == 0.  A is not modified. */
 int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q,
                int64_t ldq, int want_vectors, int order, pevd_stats* stats);
 

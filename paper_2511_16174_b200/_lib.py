@@ -73,6 +73,8 @@ SIGNATURES = {
     "pevd_syevd_workspace_bytes": (_i64, [_i64, _int, _int, _int]),
     "pevd_syevd_device": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _int, _int, _vp, _i64,
                                  _vp, ctypes.POINTER(PevdStats)]),
+    "pevd_syevd_device_host_q": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _int,
+                                        _int, _vp, _i64, _vp, ctypes.POINTER(PevdStats)]),
     "pevd_syevd": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _int, _int,
                           ctypes.POINTER(PevdStats)]),
     "pevd_dgemm": (_int, [_int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp,

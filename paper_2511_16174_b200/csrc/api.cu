@@ -12,6 +12,8 @@
 #include <atomic>
 #include <mutex>
 #include <vector>
+#include <memory>
+#include "hostio.h"
 #include "kernels.cuh"
 #include "../../include/pevd.h"
 
@@ -227,9 +229,16 @@ int64_t pevd_syevd_workspace_bytes(int64_t n, int b, int want_vectors, int order
   return plan_layout(nullptr, n, b, want_vectors, order).total + 4096;
 }
 
-int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
-                      int64_t ldq, int want_vectors, int order, void* workspace,
-                      int64_t workspace_bytes, void* stream, pevd_stats* stats) {
+}  // extern "C"
+
+namespace pevd {
+namespace {
+
+// The single-GPU orchestrator behind pevd_syevd_device / pevd_syevd_device_host_q / pevd_syevd.
+// hq (optional): Q's host destination; its copies are queued as columns of Q become final.
+int syevd_impl(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q, int64_t ldq,
+               int want_vectors, int order, void* workspace, int64_t workspace_bytes,
+               cudaStream_t sm, pevd_stats* stats, HostQ* hq) {
   if (n < 1 || lda < n || (want_vectors && (!Q || ldq < n)) || b < 1) {
     set_error("pevd_syevd_device: bad arguments (n=%lld, b=%d)", (long long)n, b);
     return ERR_VALUE;
@@ -238,7 +247,6 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     set_error("order must be 0 (pipelined), 1 (sequential) or 2 (conventional)");
     return ERR_VALUE;
   }
-  cudaStream_t sm = (cudaStream_t)stream;
   if (stats) memset(stats, 0, sizeof(*stats));
   // trivial sizes (pipeline.py:90-93: b = min(b, n-1); n == 1 has nothing to reduce)
   if (n == 1) {
@@ -246,6 +254,7 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
     if (want_vectors) {
       const double one = 1.0;
       PEVD_CUDA(cudaMemcpyAsync(Q, &one, 8, cudaMemcpyHostToDevice, sm));
+      if (hq && hq->slab_ready(sm, Q, ldq, 1, 0, 1)) return ERR_CUDA;
     }
     PEVD_CUDA(cudaStreamSynchronize(sm));
     return OK;
@@ -368,7 +377,24 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
         cudaEventRecord(ev[5].b, sm);
         flops_set_stage(ST_SBR_BACK);
         cudaEventRecord(ev[3].a, sm);
-        if ((rc = sbr_back_apply_left(sm, n, b, A, lda, L.Tall, Q, ldq, n, L.ws_back, true))) break;
+        if (hq) {
+          // all but the last Q_SLAB_GROUPS aggregated blocks over every column, then those (the
+          // largest, m ~ n) slab by slab: each slab's copy to the host overlaps the next
+          // slab's GEMMs, and only the last slab's copy is exposed
+          const std::vector<int64_t> sl = q_slab_bounds(n);
+          const int64_t gsplit = sl.size() > 2 ? Q_SLAB_GROUPS : 0;
+          if (gsplit > 0)
+            rc = sbr_back_apply_left(sm, n, b, A, lda, L.Tall, Q, ldq, n, L.ws_back, true, gsplit);
+          for (size_t s = 0; s + 1 < sl.size() && rc == OK; ++s) {
+            rc = sbr_back_apply_left(sm, n, b, A, lda, L.Tall, Q + sl[s] * ldq, ldq,
+                                     sl[s + 1] - sl[s], L.ws_back, true, 0, gsplit > 0 ? gsplit : -1);
+            if (rc == OK && hq->slab_ready(sm, Q, ldq, n, sl[s], sl[s + 1] - sl[s])) rc = ERR_CUDA;
+          }
+          if (rc) break;
+        } else if ((rc = sbr_back_apply_left(sm, n, b, A, lda, L.Tall, Q, ldq, n, L.ws_back,
+                                             true))) {
+          break;
+        }
         cudaEventRecord(ev[3].b, sm);
       } else if (order == PEVD_ORDER_CONVENTIONAL) {
         flops_set_stage(ST_BC_BACK);
@@ -393,6 +419,10 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
         GemmArgs g{n, n, n, 1.0, 0.0, L.Qs, n, L.Qd, n, Q, ldq, 0, 0, A_GENERAL, C_ALL};
         if ((rc = gemm(sm, g, nullptr, 0))) break;
         cudaEventRecord(ev[5].b, sm);
+      }
+      if (hq && !conv_t && hq->slab_ready(sm, Q, ldq, n, 0, n)) {
+        rc = ERR_CUDA;
+        break;
       }
     }
     if (cudaStreamSynchronize(sm) != cudaSuccess) {
@@ -432,6 +462,53 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
   } while (0);
   if (rc == ERR_CUDA && g_err[0] == '\0') set_error("CUDA failure");
   cleanup();
+  return rc;
+}
+
+}  // namespace
+}  // namespace pevd
+
+extern "C" {
+
+int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
+                      int64_t ldq, int want_vectors, int order, void* workspace,
+                      int64_t workspace_bytes, void* stream, pevd_stats* stats) {
+  return syevd_impl(n, b, A, lda, lam, Q, ldq, want_vectors, order, workspace, workspace_bytes,
+                    (cudaStream_t)stream, stats, nullptr);
+}
+
+int pevd_syevd_device_host_q(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
+                             int64_t ldq, double* Qh, int64_t ldqh, int want_vectors, int order,
+                             void* workspace, int64_t workspace_bytes, void* stream,
+                             pevd_stats* stats) {
+  if (want_vectors && (!Qh || ldqh < n)) {
+    set_error("pevd_syevd_device_host_q: bad host Q (ldqh=%lld, n=%lld)", (long long)ldqh,
+              (long long)n);
+    return ERR_VALUE;
+  }
+  if (!want_vectors)
+    return syevd_impl(n, b, A, lda, lam, Q, ldq, 0, order, workspace, workspace_bytes,
+                      (cudaStream_t)stream, stats, nullptr);
+  int dev = 0;
+  PEVD_CUDA(cudaGetDevice(&dev));
+  HostQ hq;
+  hq.Qh = Qh;
+  hq.ldqh = ldqh;
+  hq.pinned = host_is_pinned(Qh);
+  std::unique_ptr<Stager> stager;
+  if (hq.pinned) {
+    PEVD_CUDA(cudaStreamCreateWithFlags(&hq.cs, cudaStreamNonBlocking));
+  } else {
+    stager.reset(new Stager(dev));
+    hq.stager = stager.get();
+  }
+  int rc = syevd_impl(n, b, A, lda, lam, Q, ldq, 1, order, workspace, workspace_bytes,
+                      (cudaStream_t)stream, stats, &hq);
+  if (hq.finish() && rc == OK) {
+    set_error("device -> host copy of Q failed");
+    rc = ERR_CUDA;
+  }
+  if (hq.cs) cudaStreamDestroy(hq.cs);
   return rc;
 }
 
@@ -478,34 +555,57 @@ int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, doub
   const int64_t wsb = pevd_syevd_workspace_bytes(n, bb, want_vectors, order);
   double *dA = nullptr, *dlam = nullptr, *dQ = nullptr;
   void* ws = nullptr;
+  cudaStream_t st = nullptr;
+  int dev = 0;
   int rc = OK;
   auto fail_alloc = [&](const char* what) {
     set_error("device allocation failed (%s)", what);
     rc = ERR_NOMEM;
   };
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    set_error("CUDA context unavailable: %s", cudaGetErrorString(cudaGetLastError()));
+    return ERR_CUDA;
+  }
   if (cudaMalloc(&dA, n * n * 8) != cudaSuccess) fail_alloc("A");
   else if (cudaMalloc(&dlam, n * 8) != cudaSuccess) fail_alloc("lam");
   else if (want_vectors && cudaMalloc(&dQ, n * n * 8) != cudaSuccess) fail_alloc("Q");
   else if (cudaMalloc(&ws, wsb) != cudaSuccess) fail_alloc("workspace");
   if (rc == OK) {
-    if (cudaMemcpy2D(dA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice) != cudaSuccess) {
-      set_error("H2D copy failed");
+    // only the lower trapezoid of each column block goes up: the strictly upper triangle of A
+    // is never referenced on the device (the SBR reads A through its lower triangle)
+    const int64_t CB = 512;
+    cudaError_t e = cudaSuccess;
+    if (host_is_pinned(A)) {
+      for (int64_t j0 = 0; j0 < n && e == cudaSuccess; j0 += CB)
+        e = cudaMemcpy2DAsync(dA + j0 + j0 * n, n * 8, A + j0 + j0 * lda, lda * 8, (n - j0) * 8,
+                              std::min(CB, n - j0), cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    } else {
+      Stager up(dev);
+      for (int64_t j0 = 0; j0 < n; j0 += CB)
+        up.h2d(A + j0 + j0 * lda, lda, dA + j0 + j0 * n, n, n - j0, std::min(CB, n - j0));
+      e = up.drain();
+    }
+    if (e != cudaSuccess) {
+      set_error("H2D copy failed: %s", cudaGetErrorString(e));
       rc = ERR_CUDA;
     }
   }
   if (rc == OK)
-    rc = pevd_syevd_device(n, b, dA, n, dlam, dQ, n, want_vectors, order, ws, wsb, nullptr, stats);
-  if (rc == OK) {
-    if (cudaMemcpy(lam, dlam, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) rc = ERR_CUDA;
-    if (rc == OK && want_vectors &&
-        cudaMemcpy2D(Q, ldq * 8, dQ, n * 8, n * 8, n, cudaMemcpyDeviceToHost) != cudaSuccess)
-      rc = ERR_CUDA;
-    if (rc != OK) set_error("D2H copy failed");
+    rc = want_vectors ? pevd_syevd_device_host_q(n, b, dA, n, dlam, dQ, n, Q, ldq, 1, order, ws,
+                                                 wsb, st, stats)
+                      : pevd_syevd_device(n, b, dA, n, dlam, nullptr, n, 0, order, ws, wsb, st,
+                                          stats);
+  if (rc == OK && cudaMemcpy(lam, dlam, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    set_error("D2H copy failed");
+    rc = ERR_CUDA;
   }
   cudaFree(dA);
   cudaFree(dlam);
   cudaFree(dQ);
   cudaFree(ws);
+  cudaStreamDestroy(st);
   return rc;
 }
 

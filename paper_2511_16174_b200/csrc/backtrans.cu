@@ -687,14 +687,15 @@ int sbr_back_form(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_
 
 int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_t ldy,
                         const double* Tall, double* X, int64_t ldx, int64_t ncols, void* ws,
-                        bool prepared) {
+                        bool prepared, int64_t g_lo, int64_t g_hi) {
   // X <- Q_s X = H_0 (H_1 ( ... (H_{R-1} X))): aggregated blocks from the last panel backwards
   if (b < 1 || n <= b) return OK;
   if (!prepared) PEVD_TRY(sbr_back_prepare(st, n, b, Yfull, ldy, Tall, ws));
   const int NB = nb_agg();
   SbrBackWs W = sbr_back_carve(n, b, ws, NB);
   const int64_t R = sbr_num_rounds(n, b);
-  for (int64_t g = W.ngroups - 1; g >= 0; --g) {
+  if (g_hi < 0 || g_hi > W.ngroups) g_hi = W.ngroups;
+  for (int64_t g = g_hi - 1; g >= std::max<int64_t>(g_lo, 0); --g) {
     int64_t t0, c0, K;
     group_dims(n, b, NB, R, g, &t0, &c0, &K);
     const int64_t m = n - t0;

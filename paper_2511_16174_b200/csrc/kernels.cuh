@@ -69,9 +69,11 @@ int sbr_back_prepare(cudaStream_t st, int64_t n, int b, const double* Yfull, int
 int sbr_back_form(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_t ldy,
                   const double* Tall, double* Qs, int64_t ldq, void* ws, bool prepared = false);
 // Apply the SBR reflectors from the left to X (n x ncols): X <- Q_s X (conventional order).
+// g_lo/g_hi: only the aggregated blocks [g_lo, g_hi) (all when g_hi < 0); blocks are applied
+// from the last backwards, so [k, end) then [0, k) is the full product.
 int sbr_back_apply_left(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_t ldy,
                         const double* Tall, double* X, int64_t ldx, int64_t ncols, void* ws,
-                        bool prepared = false);
+                        bool prepared = false, int64_t g_lo = 0, int64_t g_hi = -1);
 // X (nrows x n) <- X Q_s: rows of Q_s from rows of the identity (distributed pipelined order).
 int sbr_back_apply_right(cudaStream_t st, int64_t n, int b, const double* Yfull, int64_t ldy,
                          const double* Tall, double* X, int64_t ldx, int64_t nrows, void* ws,

@@ -354,6 +354,17 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=F
     q = empty(n, n) if want_vectors else None
     ws = workspace(L.pevd_syevd_workspace_bytes(n, bb, int(want_vectors), oc))
     st = _lib.PevdStats() if stats is None else stats
+    if want_vectors and order == "conventional":
+        # Q comes down slab by slab while SBR-Back computes the next slab (native staging
+        # threads for the pageable numpy buffer), Fortran-ordered as the reference returns it
+        qf = np.empty((n, n), dtype=np.float64, order="F")
+        rc = L.pevd_syevd_device_host_q(n, bb, _p(da), n, _p(lam), _p(q), n,
+                                        qf.ctypes.data_as(ctypes.c_void_p), n, 1, oc, _p(ws),
+                                        ws.numel(), _stream(), ctypes.byref(st))
+        if rc == _lib.PEVD_ERR_CONVERGE:
+            raise RuntimeError(L.pevd_last_error().decode())
+        _lib.check(rc, "syevd")
+        return lam.cpu().numpy()[:n], qf, st
     rc = L.pevd_syevd_device(n, bb, _p(da), n, _p(lam), _p(q), n, int(want_vectors), oc, _p(ws),
                              ws.numel(), _stream(), ctypes.byref(st))
     if rc == _lib.PEVD_ERR_CONVERGE:
@@ -362,13 +373,10 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=F
     del ws, da
     qh = None
     if want_vectors:
-        if order == "conventional":
-            qh = _to_host(q).T                        # Fortran order, no host transpose
-        else:
-            qt = torch.empty_like(q)                  # C order: transposed on the device
-            _lib.check(L.pevd_transpose(n, n, _p(q), n, _p(qt), n, _stream()), "transpose")
-            del q
-            qh = _to_host(qt)
+        qt = torch.empty_like(q)                      # C order: transposed on the device
+        _lib.check(L.pevd_transpose(n, n, _p(q), n, _p(qt), n, _stream()), "transpose")
+        del q
+        qh = _to_host(qt)
     return lam.cpu().numpy()[:n], qh, st
 
 

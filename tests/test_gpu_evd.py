@@ -89,3 +89,81 @@ def test_padded_leading_dimensions(order):
     lam_h = lam.cpu().numpy()
     assert orc.backward_error(a, q, lam_h) <= 1e-15
     assert orc.orthogonality(q) <= 1e-15
+
+
+def _device_run(a, b, order, poison_upper=False):
+    """pevd_syevd_device on a column-major device copy of `a` (optionally with NaN in the
+    strictly upper triangle): (lam, Q column-major as a Fortran array)."""
+    import ctypes
+    import torch
+    from paper_2511_16174_b200 import _lib
+    L = _lib.load()
+    n = a.shape[0]
+    oc = _lib.ORDER_CODES[order]
+    A = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()  # rows of A^T = columns of A
+    if poison_upper:
+        iu = torch.triu_indices(n, n, 1)
+        A[iu[1], iu[0]] = float("nan")                      # A[r, c] for r < c, column-major
+    Q = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    lam = torch.empty(n, dtype=torch.float64, device="cuda")
+    ws = torch.empty(L.pevd_syevd_workspace_bytes(n, b, 1, oc), dtype=torch.uint8, device="cuda")
+    P = ctypes.c_void_p
+    rc = L.pevd_syevd_device(n, b, P(A.data_ptr()), n, P(lam.data_ptr()), P(Q.data_ptr()), n, 1,
+                             oc, P(ws.data_ptr()), ws.numel(),
+                             P(torch.cuda.current_stream().cuda_stream), None)
+    _lib.check(rc, "pevd_syevd_device")
+    return lam.cpu().numpy(), np.asfortranarray(Q.cpu().numpy().T)
+
+
+@pytest.mark.parametrize("order,b", [("conventional", 32), ("conventional", 12),
+                                     ("pipelined", 32), ("sequential", 16)])
+def test_strict_upper_triangle_never_read(order, b):
+    """include/pevd.h: only the lower triangle of A is read -- the contract pevd_syevd's
+    lower-trapezoid upload relies on.  NaN above the diagonal changes nothing, bit for bit."""
+    a = sym(600, 41)
+    l1, q1 = _device_run(a, b, order)
+    l2, q2 = _device_run(a, b, order, poison_upper=True)
+    np.testing.assert_array_equal(l1, l2)
+    np.testing.assert_array_equal(q1, q2)
+
+
+@pytest.mark.parametrize("n,order,pinned", [(700, "conventional", True),
+                                            (700, "pipelined", False),
+                                            (4500, "conventional", True),
+                                            (4500, "conventional", False)])
+def test_host_entry_point(n, order, pinned):
+    """pevd_syevd (HOST buffers): lower-trapezoid upload, Q delivered slab by slab (n >= 4096
+    runs SBR-Back in four column slabs whose copies overlap the next slab), pinned buffers by
+    the copy engines, pageable ones through the native staging threads.  Same eigenpairs as the
+    device entry point; the padding of Q (ldq > n) is left alone."""
+    import ctypes
+    import torch
+    from paper_2511_16174_b200 import _lib
+    L = _lib.load()
+    b = 32
+    a = sym(n, n + 3)
+    lda, ldq = n + 5, n + 2
+    if pinned:
+        A = torch.zeros((n, lda), dtype=torch.float64, pin_memory=True)
+        Qh = torch.full((n, ldq), -3.0, dtype=torch.float64, pin_memory=True)
+        lam = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        A[:, :n] = torch.from_numpy(np.ascontiguousarray(a.T))
+        A_np, Q_np, lam_np = A.numpy(), Qh.numpy(), lam.numpy()
+    else:
+        A_np = np.zeros((n, lda))
+        A_np[:, :n] = a.T
+        Q_np = np.full((n, ldq), -3.0)
+        lam_np = np.empty(n)
+    P = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    st = _lib.PevdStats()
+    rc = L.pevd_syevd(n, b, P(A_np), lda, P(lam_np), P(Q_np), ldq, 1, _lib.ORDER_CODES[order],
+                      ctypes.byref(st))
+    _lib.check(rc, "pevd_syevd")
+    assert np.all(Q_np[:, n:] == -3.0)
+    q = np.asfortranarray(Q_np[:, :n].T)
+    l_dev, q_dev = _device_run(a, b, order)
+    np.testing.assert_allclose(lam_np, l_dev, atol=1e-13 * np.abs(l_dev).max())
+    np.testing.assert_allclose(q, q_dev, atol=1e-11)
+    assert orc.backward_error(a, q, lam_np) <= (1e-15 if n <= 1024 else 1e-12)
+    assert orc.orthogonality(q) <= (1e-15 if n <= 1024 else 1e-12)
+    assert st.sbr_back_ms[1] > 0
