@@ -130,6 +130,13 @@ int pevd_syevd_device_host_q(int64_t n, int b, double* A, int64_t lda, double* l
 int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q,
                int64_t ldq, int want_vectors, int order, pevd_stats* stats);
 
+/* pevd_syevd with the input check of SymmetricMatrix (core.py:75-84, pipeline.py:517-518)
+ * folded in: all of A goes up and max |A_ij - A_ji| > sym_tol * max(1, ||A||_F) returns
+ * PEVD_ERR_VALUE ("asymmetry ... exceeds tolerance") before any reduction runs. */
+int pevd_syevd_checked(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q,
+                       int64_t ldq, int want_vectors, int order, double sym_tol,
+                       pevd_stats* stats);
+
 /* The input check of SymmetricMatrix (core.py:75-84) on the device: out2[0] = max |A_ij - A_ji|,
  * out2[1] = ||A||_F (HOST array of 2).  A device pointer (column-major, lda).  Synchronous. */
 int pevd_asymmetry(int64_t n, const double* A, int64_t lda, double* out2, void* stream);

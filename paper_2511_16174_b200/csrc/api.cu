@@ -10,6 +10,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <mutex>
 #include <vector>
 #include <memory>
@@ -501,6 +503,7 @@ int pevd_syevd_device_host_q(int64_t n, int b, double* A, int64_t lda, double* l
   } else {
     stager.reset(new Stager(dev));
     hq.stager = stager.get();
+    stager->touch(Qh, ldqh, n, n);  // fault the pages in while the GPU reduces
   }
   int rc = syevd_impl(n, b, A, lda, lam, Q, ldq, 1, order, workspace, workspace_bytes,
                       (cudaStream_t)stream, stats, &hq);
@@ -545,8 +548,15 @@ int pevd_asymmetry(int64_t n, const double* A, int64_t lda, double* out2, void* 
   return OK;
 }
 
-int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q, int64_t ldq,
-               int want_vectors, int order, pevd_stats* stats) {
+}  // extern "C"
+
+namespace {
+
+// pevd_syevd / pevd_syevd_checked.  sym_tol < 0: only the lower trapezoid of A goes up (the
+// device never reads the strictly upper triangle); otherwise all of A goes up and the
+// SymmetricMatrix test (core.py:75-84) runs on the device first.
+int host_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q,
+               int64_t ldq, int want_vectors, int order, double sym_tol, pevd_stats* stats) {
   if (n < 1 || lda < n || !A || !lam || (want_vectors && (!Q || ldq < n))) {
     set_error("pevd_syevd: bad arguments");
     return ERR_VALUE;
@@ -567,36 +577,62 @@ int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, doub
     set_error("CUDA context unavailable: %s", cudaGetErrorString(cudaGetLastError()));
     return ERR_CUDA;
   }
+  // PEVD_HOST_PHASES=1: wall time of each host-side phase on stderr (tools/hostio_probe.py)
+  static const bool phases = getenv("PEVD_HOST_PHASES") && getenv("PEVD_HOST_PHASES")[0] == '1';
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!phases) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "pevd_syevd phase %-8s %8.1f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   if (cudaMalloc(&dA, n * n * 8) != cudaSuccess) fail_alloc("A");
   else if (cudaMalloc(&dlam, n * 8) != cudaSuccess) fail_alloc("lam");
   else if (want_vectors && cudaMalloc(&dQ, n * n * 8) != cudaSuccess) fail_alloc("Q");
   else if (cudaMalloc(&ws, wsb) != cudaSuccess) fail_alloc("workspace");
+  phase("malloc");
   if (rc == OK) {
     // only the lower trapezoid of each column block goes up: the strictly upper triangle of A
     // is never referenced on the device (the SBR reads A through its lower triangle)
     const int64_t CB = 512;
+    const bool full = sym_tol >= 0.0;
     cudaError_t e = cudaSuccess;
     if (host_is_pinned(A)) {
-      for (int64_t j0 = 0; j0 < n && e == cudaSuccess; j0 += CB)
-        e = cudaMemcpy2DAsync(dA + j0 + j0 * n, n * 8, A + j0 + j0 * lda, lda * 8, (n - j0) * 8,
+      for (int64_t j0 = 0; j0 < n && e == cudaSuccess; j0 += CB) {
+        const int64_t r0 = full ? 0 : j0;
+        e = cudaMemcpy2DAsync(dA + r0 + j0 * n, n * 8, A + r0 + j0 * lda, lda * 8, (n - r0) * 8,
                               std::min(CB, n - j0), cudaMemcpyHostToDevice, st);
+      }
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     } else {
       Stager up(dev);
-      for (int64_t j0 = 0; j0 < n; j0 += CB)
-        up.h2d(A + j0 + j0 * lda, lda, dA + j0 + j0 * n, n, n - j0, std::min(CB, n - j0));
+      for (int64_t j0 = 0; j0 < n; j0 += CB) {
+        const int64_t r0 = full ? 0 : j0;
+        up.h2d(A + r0 + j0 * lda, lda, dA + r0 + j0 * n, n, n - r0, std::min(CB, n - j0));
+      }
       e = up.drain();
     }
     if (e != cudaSuccess) {
       set_error("H2D copy failed: %s", cudaGetErrorString(e));
       rc = ERR_CUDA;
     }
+    if (rc == OK && full) {
+      double out2[2] = {0.0, 0.0};
+      rc = pevd_asymmetry(n, dA, n, out2, st);
+      if (rc == OK && out2[0] > sym_tol * std::max(1.0, out2[1])) {
+        set_error("asymmetry %.3e exceeds tolerance", out2[0]);
+        rc = ERR_VALUE;
+      }
+    }
   }
+  phase("upload");
   if (rc == OK)
     rc = want_vectors ? pevd_syevd_device_host_q(n, b, dA, n, dlam, dQ, n, Q, ldq, 1, order, ws,
                                                  wsb, st, stats)
                       : pevd_syevd_device(n, b, dA, n, dlam, nullptr, n, 0, order, ws, wsb, st,
                                           stats);
+  phase("evd");
   if (rc == OK && cudaMemcpy(lam, dlam, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
     set_error("D2H copy failed");
     rc = ERR_CUDA;
@@ -606,7 +642,27 @@ int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, doub
   cudaFree(dQ);
   cudaFree(ws);
   cudaStreamDestroy(st);
+  phase("free");
   return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q, int64_t ldq,
+               int want_vectors, int order, pevd_stats* stats) {
+  return host_syevd(n, b, A, lda, lam, Q, ldq, want_vectors, order, -1.0, stats);
+}
+
+int pevd_syevd_checked(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q,
+                       int64_t ldq, int want_vectors, int order, double sym_tol,
+                       pevd_stats* stats) {
+  if (!(sym_tol >= 0.0)) {
+    set_error("pevd_syevd_checked: sym_tol must be >= 0");
+    return ERR_VALUE;
+  }
+  return host_syevd(n, b, A, lda, lam, Q, ldq, want_vectors, order, sym_tol, stats);
 }
 
 int pevd_dgemm(int transA, int transB, int64_t m, int64_t n, int64_t k, double alpha,

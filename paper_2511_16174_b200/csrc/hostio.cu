@@ -81,7 +81,7 @@ void Stager::enqueue(Task t) {
       Task s = t;
       s.rows = std::min(rstep, t.rows - r);
       s.cols = std::min(cstep, t.cols - c);
-      s.src = t.src + r + c * t.lds;
+      s.src = t.src ? t.src + r + c * t.lds : nullptr;
       s.dst = t.dst + r + c * t.ldd;
       q_.push_back(s);
       ++pending_;
@@ -92,13 +92,18 @@ void Stager::enqueue(Task t) {
 void Stager::d2h(const double* dsrc, int64_t ld, double* hdst, int64_t ldh, int64_t rows,
                  int64_t cols, cudaEvent_t after) {
   if (rows <= 0 || cols <= 0) return;
-  enqueue(Task{true, dsrc, hdst, ld, ldh, rows, cols, after});
+  enqueue(Task{DOWN, dsrc, hdst, ld, ldh, rows, cols, after});
 }
 
 void Stager::h2d(const double* hsrc, int64_t ldh, double* ddst, int64_t ld, int64_t rows,
                  int64_t cols) {
   if (rows <= 0 || cols <= 0) return;
-  enqueue(Task{false, hsrc, ddst, ldh, ld, rows, cols, nullptr});
+  enqueue(Task{UP, hsrc, ddst, ldh, ld, rows, cols, nullptr});
+}
+
+void Stager::touch(double* hdst, int64_t ldh, int64_t rows, int64_t cols) {
+  if (rows <= 0 || cols <= 0) return;
+  enqueue(Task{TOUCH, nullptr, hdst, 0, ldh, rows, cols, nullptr});
 }
 
 cudaError_t Stager::drain() {
@@ -125,7 +130,9 @@ void Stager::worker(int) {
     }
     cudaError_t e = (buf && st) ? cudaSuccess : cudaErrorMemoryAllocation;
     const size_t w = (size_t)t.rows * 8;
-    if (e == cudaSuccess && t.down) {
+    if (t.kind == TOUCH) {
+      for (int64_t c = 0; c < t.cols; ++c) memset(t.dst + c * t.ldd, 0, w);
+    } else if (e == cudaSuccess && t.kind == DOWN) {
       if (t.after) e = cudaEventSynchronize(t.after);
       if (e == cudaSuccess)
         e = cudaMemcpy2DAsync(buf, w, t.src, t.lds * 8, w, t.cols, cudaMemcpyDeviceToHost, st);

@@ -31,12 +31,16 @@ class Stager {
            cudaEvent_t after);
   // host -> device for a rectangle
   void h2d(const double* hsrc, int64_t ldh, double* ddst, int64_t ld, int64_t rows, int64_t cols);
+  // first-touch a pageable host destination (zero fill) so the later d2h chunks copy into
+  // resident pages instead of faulting them in on the critical path
+  void touch(double* hdst, int64_t ldh, int64_t rows, int64_t cols);
   // wait for every queued chunk; returns the first CUDA error seen (cudaSuccess if none)
   cudaError_t drain();
 
  private:
+  enum Kind { UP, DOWN, TOUCH };
   struct Task {
-    bool down;
+    Kind kind;
     const double* src;
     double* dst;
     int64_t lds, ldd, rows, cols;

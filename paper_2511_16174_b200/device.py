@@ -336,7 +336,9 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=F
     A column-major, a C-order one is A^T column-major (the same matrix when symmetric).
     check_sym: the SymmetricMatrix test (core.py:75-84) runs on the device (pevd_asymmetry)
     instead of over the host copy.  Q comes back Fortran-ordered in conventional order and
-    C-ordered otherwise (pipeline.py:495, 503) -- the device transposes, not the host."""
+    C-ordered otherwise (pipeline.py:495, 503) -- the device transposes, not the host.
+    Conventional order is one native call (pevd_syevd / pevd_syevd_checked): the library moves
+    the host buffers itself and overlaps Q's download with the last SBR-Back blocks."""
     L = _lib.load()
     torch = _torch()
     a = np.asarray(a, dtype=np.float64)
@@ -344,6 +346,23 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=F
     oc = _lib.ORDER_CODES[order]
     bb = max(1, min(b, n - 1)) if n > 1 else 1
     mem = a.T if a.flags.f_contiguous else np.ascontiguousarray(a)
+    st = _lib.PevdStats() if stats is None else stats
+    if want_vectors and order == "conventional":
+        # one native call: the upload (lower trapezoid, or all of A for the device symmetry
+        # check) and Q's download slab by slab under the last SBR-Back blocks go through the
+        # library's own staging threads; Q lands Fortran-ordered, as the reference returns it
+        lam_h = np.empty(n)
+        qf = np.empty((n, n), dtype=np.float64, order="F")
+        vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        if check_sym:
+            rc = L.pevd_syevd_checked(n, bb, vp(mem), n, vp(lam_h), vp(qf), n, 1, oc, sym_tol,
+                                      ctypes.byref(st))
+        else:
+            rc = L.pevd_syevd(n, bb, vp(mem), n, vp(lam_h), vp(qf), n, 1, oc, ctypes.byref(st))
+        if rc == _lib.PEVD_ERR_CONVERGE:
+            raise RuntimeError(L.pevd_last_error().decode())
+        _lib.check(rc, "syevd")
+        return lam_h, qf, st
     da = _to_device(mem)                  # (n, n): column-major A (or A^T)
     if check_sym:
         out = (ctypes.c_double * 2)()
@@ -353,18 +372,6 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=F
     lam = empty(n)
     q = empty(n, n) if want_vectors else None
     ws = workspace(L.pevd_syevd_workspace_bytes(n, bb, int(want_vectors), oc))
-    st = _lib.PevdStats() if stats is None else stats
-    if want_vectors and order == "conventional":
-        # Q comes down slab by slab while SBR-Back computes the next slab (native staging
-        # threads for the pageable numpy buffer), Fortran-ordered as the reference returns it
-        qf = np.empty((n, n), dtype=np.float64, order="F")
-        rc = L.pevd_syevd_device_host_q(n, bb, _p(da), n, _p(lam), _p(q), n,
-                                        qf.ctypes.data_as(ctypes.c_void_p), n, 1, oc, _p(ws),
-                                        ws.numel(), _stream(), ctypes.byref(st))
-        if rc == _lib.PEVD_ERR_CONVERGE:
-            raise RuntimeError(L.pevd_last_error().decode())
-        _lib.check(rc, "syevd")
-        return lam.cpu().numpy()[:n], qf, st
     rc = L.pevd_syevd_device(n, bb, _p(da), n, _p(lam), _p(q), n, int(want_vectors), oc, _p(ws),
                              ws.numel(), _stream(), ctypes.byref(st))
     if rc == _lib.PEVD_ERR_CONVERGE:

@@ -238,10 +238,17 @@ def test_large_input_checked_on_device():
         np.testing.assert_allclose(r.lam, lam_ref, atol=10 * n * EPS * np.abs(lam_ref).max())
     assert orc.backward_error(a, res_c.Q, res_c.lam) <= 1e-15
     assert orc.orthogonality(res_f.Q) <= 1e-15
+    # conventional order with a C-ordered input: one native call (pevd_syevd_checked) that
+    # uploads, checks, solves and streams Q back into a Fortran-ordered numpy array
+    res_cc, _, _, _ = pkg.run(a, pkg.PipelineConfig(workers=1, b=32, order="conventional"))
+    assert res_cc.Q.flags.f_contiguous
+    np.testing.assert_allclose(res_cc.lam, res_f.lam, atol=1e-13 * np.abs(lam_ref).max())
+    assert orc.backward_error(a, res_cc.Q, res_cc.lam) <= 1e-15
     bad = a.copy()
     bad[7, 3] += 1e-6
-    with pytest.raises(ValueError, match="asymmetry"):
-        pkg.run(bad, pkg.PipelineConfig(workers=1, b=32))
+    for order in ("pipelined", "conventional"):
+        with pytest.raises(ValueError, match="asymmetry"):
+            pkg.run(bad, pkg.PipelineConfig(workers=1, b=32, order=order))
 
 
 def test_device_asymmetry_kernel_matches_numpy():
