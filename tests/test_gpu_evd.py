@@ -167,3 +167,50 @@ def test_host_entry_point(n, order, pinned):
     assert orc.backward_error(a, q, lam_np) <= (1e-15 if n <= 1024 else 1e-12)
     assert orc.orthogonality(q) <= (1e-15 if n <= 1024 else 1e-12)
     assert st.sbr_back_ms[1] > 0
+
+
+def _structured_cases():
+    rng = np.random.default_rng(2024)
+    n = 333
+    yield "zero", np.zeros((n, n))
+    yield "identity", np.eye(n)
+    yield "diagonal", np.diag(rng.standard_normal(n))
+    t = np.diag(rng.standard_normal(n)) + np.diag(rng.standard_normal(n - 1), 1)
+    yield "tridiagonal", t + np.triu(t, 1).T
+    u = rng.standard_normal(n)
+    yield "rank1", np.outer(u, u)
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    yield "reflection", np.eye(n) - 2.0 * np.outer(v, v)     # eigenvalues -1 (once), +1 (n-1)
+    blk = np.zeros((n, n))
+    for s0 in range(0, n, 50):                               # decoupled blocks: exact zeros
+        s1 = min(n, s0 + 50)
+        g = rng.standard_normal((s1 - s0, s1 - s0))
+        blk[s0:s1, s0:s1] = g + g.T
+    yield "block_diagonal", blk
+    g = rng.standard_normal((n, n))
+    yield "tiny_scale", (g + g.T) * 1e-150
+    yield "large_scale", (g + g.T) * 1e150
+    for m in (33, 34, 65):                                   # n = b+1, b+2, 2b+1
+        g = rng.standard_normal((m, m))
+        yield f"n{m}", g + g.T
+
+
+@pytest.mark.parametrize("case", list(_structured_cases()), ids=lambda c: c[0])
+@pytest.mark.parametrize("order", ["pipelined", "conventional"])
+def test_structured_inputs(case, order):
+    """Inputs whose reductions hit the degenerate paths: zero columns below the band (tau = 0),
+    an input that is already banded, exactly repeated eigenvalues (full deflation in the
+    divide and conquer), decoupled blocks, extreme but representable scales, and n just above
+    the bandwidth.  Bars as the reference's acceptance test (test_acceptance.py:34-50)."""
+    name, a = case
+    n = a.shape[0]
+    lam, q, _ = dev().syevd(a, 32, True, order)
+    lam_np = np.linalg.eigvalsh(a)
+    nrm = np.abs(lam_np).max()
+    assert np.all(np.diff(lam) >= 0)
+    np.testing.assert_allclose(lam, lam_np, atol=10 * n * EPS * nrm)
+    assert orc.backward_error(a, q, lam) <= 1e-15
+    assert orc.orthogonality(q) <= 1e-15
+    if name == "zero":
+        np.testing.assert_array_equal(lam, np.zeros(n))
