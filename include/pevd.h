@@ -44,7 +44,7 @@ typedef struct pevd_stats {
   double bc_back_ms[2];
   double final_ms[2];
   double total_ms;         /* first start .. last end */
-  int64_t n_reflectors;    /* bulge reflector slots (sum_j (n-2-jb)) */
+  int64_t n_reflectors;    /* bulge reflector slots (sum_j (n-2-jb), b the chase bandwidth: roundup8(b) <= 64) */
   int64_t n_rounds;        /* SBR panels */
   /* EXECUTED flops per stage, in the order SBR, BC, SBR-Back, BC-Back, Solver, FinalMultiply
    * (FlopCounter stages, core.py:26-62): GEMM launches as issued (2 m n k; the lower-tile
@@ -211,7 +211,7 @@ int pevd_sbr_back_left(int64_t n, int b, const double* Ystair, int64_t ldy, cons
 
 /* BC-Back backtrans.py:277-310.  right: X (nrows x n, ldx) <- X Q_b ("reordered", i.e. the
  * transpose of Q_b^T X^T).  left: X (n x ncols, ldx) <- Q_b X ("conventional"; for the DMMA
- * bandwidths b in {8, 16, 24, 32} it runs on X^T in the workspace, the kernel's coalesced
+ * bandwidths b in {8, 16, ..., 64} it runs on X^T in the workspace, the kernel's coalesced
  * layout; other b apply the reflectors one by one).  The workspace
  * (pevd_bc_back_workspace_bytes(n, rows or cols, b)) holds scheduler counters, the (V, Z)
  * records of the reflector blocks and that transpose. */

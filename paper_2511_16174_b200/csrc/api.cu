@@ -116,16 +116,27 @@ bool values_by_bisection() {
   return v != 0;
 }
 
+// The bulge chase treats the SBR's b-band as a band of width roundup8(b) (its entries beyond b
+// are zero; the chase is valid for any band at most its width), so that its reflectors have the
+// geometry of the DMMA BC-Back kernel, whose 8-wide blocks need b a multiple of 8.  Same
+// eigenpairs to rounding; the per-stage entry points (pevd_bc, stages.bc_reduce) chase with b
+// itself, exactly as bulge.py does.
+int chase_bandwidth(int64_t n, int b) {
+  const int r = (b + 7) / 8 * 8;
+  return (r != b && r <= 64 && r <= n - 1) ? r : b;
+}
+
 Layout plan_layout(void* base, int64_t n, int b, int want_vectors, int order) {
   Carve c(base, 0);
   Layout L{};
   const int64_t R = sbr_num_rounds(n, b);
-  L.vld = (int)pad8(b);
+  const int bc_b = chase_bandwidth(n, b);
+  L.vld = (int)pad8(bc_b);
   L.bands = (double*)c.take((int64_t)(b + 1) * n * 8);
   L.Tall = (double*)c.take(std::max<int64_t>(R, 1) * b * b * 8);
   L.d = (double*)c.take(n * 8);
   L.e = (double*)c.take(std::max<int64_t>(n, 1) * 8);
-  const int64_t nref = (n >= 3) ? bc_num_reflectors(n, b) : 0;
+  const int64_t nref = (n >= 3) ? bc_num_reflectors(n, bc_b) : 0;
   if (want_vectors) {
     L.tau = (double*)c.take(std::max<int64_t>(nref, 1) * 8);
     L.V = (double*)c.take(std::max<int64_t>(nref, 1) * L.vld * 8);
@@ -134,10 +145,10 @@ Layout plan_layout(void* base, int64_t n, int b, int want_vectors, int order) {
   const bool bisect = !want_vectors && values_by_bisection();  // no Q_d, no merge buffers
   L.Qd = bisect ? nullptr : (double*)c.take(n * n * 8);
   L.ws_sbr = c.take(sbr_ws_bytes(n, b));
-  L.ws_bc = c.take(bc_ws_bytes(n, b));
+  L.ws_bc = c.take(bc_ws_bytes(n, bc_b));
   L.ws_dc = c.take(bisect ? stebz_ws_bytes(n) : stedc_ws_bytes(n));
   L.ws_back = c.take(sbr_back_ws_bytes(n, b));
-  L.ws_bcb = c.take(bc_back_ws_bytes(n, n, b));
+  L.ws_bcb = c.take(bc_back_ws_bytes(n, n, bc_b));
   L.total = c.off;
   return L;
 }
@@ -262,11 +273,12 @@ int syevd_impl(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
     return OK;
   }
   b = (int)std::min<int64_t>(b, n - 1);
-  if (b > 32) {
-    set_error("bandwidth b=%d > 32 is not supported by the device kernels", b);
+  if (b > 64) {
+    set_error("bandwidth b=%d > 64 is not supported by the device kernels", b);
     return ERR_VALUE;
   }
   Layout L = plan_layout(workspace, n, b, want_vectors, order);
+  const int bc_b = chase_bandwidth(n, b);
   if (workspace_bytes < L.total) {
     set_error("workspace too small: %lld < %lld bytes", (long long)workspace_bytes,
               (long long)L.total);
@@ -309,8 +321,9 @@ int syevd_impl(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
     //      (enqueued next, on the back stream) fill the SMs
     cudaEventRecord(ev[1].a, sm);
     flops_set_stage(ST_BC);
-    if ((rc = bc_reduce(sm, n, b, L.bands, L.d, L.e, want_vectors ? L.tau : nullptr,
-                        want_vectors ? L.V : nullptr, L.vld, L.ws_bc)))
+    if ((rc = bc_reduce_range(sm, n, bc_b, b, L.bands, n, L.d, L.e, nullptr,
+                              want_vectors ? L.tau : nullptr, want_vectors ? L.V : nullptr, L.vld,
+                              L.ws_bc)))
       break;
     cudaEventRecord(ev[1].b, sm);
     // ---- SBR-Back (forms Q_s) overlapping the chase
@@ -326,16 +339,17 @@ int syevd_impl(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
       if (two_streams) cudaStreamWaitEvent(sback, ev[1].b, 0);
       flops_set_stage(ST_BC_BACK);
       cudaEventRecord(ev[4].a, sback);
-      if ((rc = bc_back_right(sback, n, b, L.tau, L.V, L.vld, L.Qs, n, n, L.ws_bcb))) break;
+      if ((rc = bc_back_right(sback, n, bc_b, L.tau, L.V, L.vld, L.Qs, n, n, L.ws_bcb))) break;
       cudaEventRecord(ev[4].b, sback);
     }
     // ---- conventional: the back-transform preparations on the side stream: the SBR-Back T
     //      aggregation needs only the SBR output, so it runs beside the latency-bound chase
     //      (enqueued after it, so the chase's cooperative grid is resident first); the Z factor
     //      of every BC-Back block needs the chase output and runs beside the divide and conquer
-    // conventional order with b in {8, 16, 24, 32} runs BC-Back on the transpose (the DMMA
+    // conventional order with b a multiple of 8 up to 64 runs BC-Back on the transpose (the DMMA
     // kernel's layout)
-    const bool conv_t = want_vectors && order == PEVD_ORDER_CONVENTIONAL && bc_back_dmma_ok(b, L.vld);
+    const bool conv_t =
+        want_vectors && order == PEVD_ORDER_CONVENTIONAL && bc_back_dmma_ok(bc_b, L.vld);
     if (want_vectors && order == PEVD_ORDER_CONVENTIONAL) {
       cudaStreamWaitEvent(sb, ev[0].b, 0);
       flops_set_stage(ST_SBR_BACK);
@@ -343,7 +357,7 @@ int syevd_impl(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
       cudaStreamWaitEvent(sb, ev[1].b, 0);
       flops_set_stage(ST_BC_BACK);
       if (conv_t &&
-          (rc = bc_back_left_t(sb, n, b, L.tau, L.V, L.vld, nullptr, n, n, L.ws_bcb, false)))
+          (rc = bc_back_left_t(sb, n, bc_b, L.tau, L.V, L.vld, nullptr, n, n, L.ws_bcb, false)))
         break;
       cudaEventRecord(prep_done, sb);
     }
@@ -370,7 +384,7 @@ int syevd_impl(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
         flops_set_stage(ST_BC_BACK);
         cudaEventRecord(ev[4].a, sm);
         if ((rc = transpose(sm, n, n, L.Qd, n, Xt, n))) break;
-        if ((rc = bc_back_left_t(sm, n, b, L.tau, L.V, L.vld, Xt, n, n, L.ws_bcb, true))) break;
+        if ((rc = bc_back_left_t(sm, n, bc_b, L.tau, L.V, L.vld, Xt, n, n, L.ws_bcb, true))) break;
         cudaEventRecord(ev[4].b, sm);
         // back to column-major in the output, where SBR-Back's left application (its faster
         // GEMM shapes) finishes Q = Q_s (Q_b Q_d) in place
@@ -401,7 +415,7 @@ int syevd_impl(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
       } else if (order == PEVD_ORDER_CONVENTIONAL) {
         flops_set_stage(ST_BC_BACK);
         cudaEventRecord(ev[4].a, sm);
-        if ((rc = bc_back_left(sm, n, b, L.tau, L.V, L.vld, L.Qd, n, n, L.ws_bcb))) break;
+        if ((rc = bc_back_left(sm, n, bc_b, L.tau, L.V, L.vld, L.Qd, n, n, L.ws_bcb))) break;
         cudaEventRecord(ev[4].b, sm);
         flops_set_stage(ST_SBR_BACK);
         cudaEventRecord(ev[3].a, sm);
@@ -457,7 +471,7 @@ int syevd_impl(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
       double tot = stats->solver_ms[1];
       tot = std::max(tot, std::max(stats->final_ms[1], stats->sbr_back_ms[1]));
       stats->total_ms = tot;
-      stats->n_reflectors = bc_num_reflectors(n, b);
+      stats->n_reflectors = bc_num_reflectors(n, bc_b);
       stats->n_rounds = sbr_num_rounds(n, b);
       flops_read(stats->flops);
     }

@@ -74,15 +74,16 @@ __global__ void bc_back_right_generic(int64_t n, int b, const double* __restrict
   }
 }
 
-// conventional direction: X <- Q_b X on columns of X (thread per column; used for small n only)
-__global__ void bc_back_left_generic(int64_t n, int b, const double* __restrict__ tau,
-                                     const double* __restrict__ V, int vld, double* X, int64_t ldx,
-                                     int64_t ncols) {
-  const int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (col >= ncols) return;
-  double* x = X + col * ldx;
+// conventional direction on the transpose: Xt <- Xt Q_b^T, i.e. X <- Q_b X with X = Xt^T, one
+// thread per row of Xt (a column of X), reflectors in reverse creation order (sweeps
+// descending, steps descending): consecutive threads touch consecutive addresses of Xt
+__global__ void bc_back_left_t_generic(int64_t n, int b, const double* __restrict__ tau,
+                                       const double* __restrict__ V, int vld, double* Xt,
+                                       int64_t ldx, int64_t nrows) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= nrows) return;
+  double* x = Xt + row;
   const int64_t nsw = n - 2;
-  // reverse creation order: sweeps descending, steps descending
   for (int64_t i = nsw - 1; i >= 0; --i) {
     const int64_t jmax = (n - 3 - i) / b;
     for (int64_t j = jmax; j >= 0; --j) {
@@ -92,10 +93,11 @@ __global__ void bc_back_left_generic(int64_t n, int b, const double* __restrict_
       const int64_t r0 = i + 1 + j * b;
       const int L = (int)((b < n - r0) ? b : n - r0);
       const double* v = V + (off + i) * vld;
+      double* xr = x + r0 * ldx;
       double dot = 0.0;
-      for (int r = 0; r < L; ++r) dot += v[r] * x[r0 + r];
+      for (int r = 0; r < L; ++r) dot = fma(v[r], xr[r * ldx], dot);
       dot *= t;
-      for (int r = 0; r < L; ++r) x[r0 + r] -= dot * v[r];
+      for (int r = 0; r < L; ++r) xr[r * ldx] -= dot * v[r];
     }
   }
 }
@@ -132,7 +134,7 @@ constexpr int wy_pitch(int need) {  // smallest pitch >= need with pitch % 16 in
 
 template <int B>
 struct WyB {
-  static_assert(B % 8 == 0 && B >= 8 && B <= 32, "BC-Back DMMA kernel: b in {8, 16, 24, 32}");
+  static_assert(B % 8 == 0 && B >= 8 && B <= 64, "BC-Back DMMA kernel: b a multiple of 8 <= 64");
   static constexpr int SPAN = 8 + B;                       // window columns of one block
   static constexpr int PA = wy_pitch(SPAN / 2);
   static constexpr int PB = SPAN + 2;
@@ -146,7 +148,7 @@ struct WyB {
 };
 static_assert(WyB<32>::PA == 20 && WyB<32>::BLK == 656, "b = 32 layout");
 static_assert(WyB<16>::PA % 16 == 12 || WyB<16>::PA % 16 == 4, "pitch");
-static_assert(WyB<8>::PA >= 8 && WyB<24>::PA >= 16, "pitch covers the span");
+static_assert(WyB<8>::PA >= 8 && WyB<24>::PA >= 16 && WyB<64>::PA >= 36, "pitch covers the span");
 
 template <int B>
 struct WySmem {
@@ -322,7 +324,7 @@ __global__ void wy_tfactor_kernel(int64_t n, const double* __restrict__ tau,
 // finish with a buffer (a shared counter) launches the copy of the step after next into it, so
 // warps drift freely within the one-step slack the double buffer gives.
 template <int B, bool LEFT>
-__global__ void __launch_bounds__(WY_THREADS, 2)
+__global__ void __launch_bounds__(WY_THREADS, (B <= 40 ? 2 : 1))
     bc_back_wy_kernel(int64_t n, const double* __restrict__ VZ, double* X, int64_t ldx,
                       int64_t nrows, int* counter, int* progress, int64_t nunits, int nrb) {
   using C = WyB<B>;
@@ -782,7 +784,7 @@ int transpose(cudaStream_t st, int64_t rows, int64_t cols, const double* in, int
 
 static int64_t wy_counter_bytes(int64_t nrows) { return ((nrows / 32 + 64) * 4 + 255) / 256 * 256; }
 
-bool bc_back_dmma_ok(int b, int vld) { return (b == 8 || b == 16 || b == 24 || b == 32) && vld >= b; }
+bool bc_back_dmma_ok(int b, int vld) { return b % 8 == 0 && b >= 8 && b <= 64 && vld >= b; }
 
 template <int B>
 static int64_t wy_records(int64_t n) {
@@ -797,7 +799,11 @@ int64_t bc_back_ws_bytes(int64_t n, int64_t nrows, int b) {
     case 16: rec = wy_records<16>(n); break;
     case 24: rec = wy_records<24>(n); break;
     case 32: rec = wy_records<32>(n); break;
-    default: rec = 0;  // the reflector-by-reflector kernels need no workspace
+    case 40: rec = wy_records<40>(n); break;
+    case 48: rec = wy_records<48>(n); break;
+    case 56: rec = wy_records<56>(n); break;
+    case 64: rec = wy_records<64>(n); break;
+    default: rec = n * nrows;  // the reflector-by-reflector kernels: room for X^T
   }
   return wy_counter_bytes(nrows) + rec * 8 + 256;
 }
@@ -862,6 +868,10 @@ static int bc_back_wy_dispatch(cudaStream_t st, int64_t n, int b, const double* 
     case 8: return bc_back_wy_launch<8, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
     case 16: return bc_back_wy_launch<16, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
     case 24: return bc_back_wy_launch<24, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
+    case 40: return bc_back_wy_launch<40, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
+    case 48: return bc_back_wy_launch<48, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
+    case 56: return bc_back_wy_launch<56, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
+    case 64: return bc_back_wy_launch<64, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
     default: return bc_back_wy_launch<32, LEFT>(st, n, tau, V, vld, X, ldx, nrows, ws, prepared);
   }
 }
@@ -879,23 +889,39 @@ int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const do
   return OK;
 }
 
-// X (n x ncols, column-major) <- Q_b X one reflector at a time (any b; the b = 32 product paths
-// run bc_back_left_t on the transpose instead)
+// X (n x ncols, column-major) <- Q_b X: the DMMA kernel for b a multiple of 8 (up to 64) on the
+// transpose; any other b one reflector at a time, also on the transpose (held in ws), so that
+// the per-thread columns of X become coalesced rows
 int bc_back_left(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                  double* X, int64_t ldx, int64_t ncols, void* ws) {
-  (void)ws;
   if (n < 3 || ncols <= 0 || b < 2) return OK;
+  if (!ws) {
+    set_error("bc_back_left: needs the workspace (pevd_bc_back_workspace_bytes)");
+    return ERR_VALUE;
+  }
+  if (bc_back_dmma_ok(b, vld)) {
+    // the records live in ws too: the transpose goes to a separate allocation
+    double* Xt = nullptr;
+    PEVD_CUDA(cudaMallocAsync(&Xt, (size_t)n * ncols * 8, st));
+    int rc = transpose(st, n, ncols, X, ldx, Xt, ncols);
+    if (rc == OK) rc = bc_back_wy_dispatch<true>(st, n, b, tau, V, vld, Xt, ncols, ncols, ws, false);
+    if (rc == OK) rc = transpose(st, ncols, n, Xt, ncols, X, ldx);
+    cudaFreeAsync(Xt, st);
+    return rc;
+  }
   flops_add(4.0 * b * (double)bc_num_reflectors(n, b) * (double)ncols);
-  bc_back_left_generic<<<(unsigned)cdiv(ncols, 128), 128, 0, st>>>(n, b, tau, V, vld, X, ldx,
-                                                                   ncols);
+  double* Xt = (double*)((char*)ws + wy_counter_bytes(ncols));
+  PEVD_TRY(transpose(st, n, ncols, X, ldx, Xt, ncols));
+  bc_back_left_t_generic<<<(unsigned)cdiv(ncols, 128), 128, 0, st>>>(n, b, tau, V, vld, Xt, ncols,
+                                                                     ncols);
   PEVD_LAUNCH_CHECK();
-  return OK;
+  return transpose(st, ncols, n, Xt, ncols, X, ldx);
 }
 
 int bc_back_left_t(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,
                    double* Xt, int64_t ldx, int64_t nrows, void* ws, bool prepared) {
   if (!(bc_back_dmma_ok(b, vld) && ws)) {  // only the DMMA kernel has the transposed layout
-    set_error("bc_back_left_t: needs b in {8, 16, 24, 32} and a workspace");
+    set_error("bc_back_left_t: needs b a multiple of 8 up to 64 and a workspace");
     return ERR_VALUE;
   }
   if (n < 3 || nrows <= 0) return OK;

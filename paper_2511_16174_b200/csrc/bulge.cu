@@ -278,6 +278,207 @@ __global__ void __launch_bounds__(64)
   }
 }
 
+// ------------------------------------------------------------ 32 < b <= 64
+// The same wavefront, step and arithmetic for bandwidths past one warp's width: every "lane =
+// row / column" loop of bc_chase_kernel runs over rows lane and lane + 32, and the region is
+// staged straight into shared memory (the register staging would need 4 x 64 doubles per lane).
+// A fallback for the band-width parameter's wider settings, not a tuned path.
+constexpr int WMAX = 64;
+constexpr int LDW = WMAX + 1;
+
+struct ChaseWideSmem {
+  double SLC[2][WMAX * LDW];
+  double SW[WMAX * LDW];
+  double vs[WMAX];
+  double wv[WMAX];
+  double tau;
+};
+
+__global__ void __launch_bounds__(64)
+    bc_chase_wide_kernel(int64_t n, int b, double* __restrict__ Bd, int64_t LDB, int* prog,
+                         double* __restrict__ tau_out, double* __restrict__ V_out, int vld,
+                         int64_t sweep_end, int64_t slot_n, int64_t slot_col0, int poll_ns) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  ChaseWideSmem& S = *reinterpret_cast<ChaseWideSmem*>(smraw);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t gend = sweep_end < n - 2 ? sweep_end : n - 2;
+  for (int64_t gi = blockIdx.x; gi < gend; gi += gridDim.x) {
+    int cur = 0;
+    for (int64_t j = 0; gi + 1 + j * b <= n - 2; ++j) {
+      if (gi > 0) {
+        if (lane == 0) {
+          const int need = (int)(j + 3);
+          if (ld_relaxed(prog + gi - 1) < need) {
+            unsigned ns = (unsigned)poll_ns;
+            while (ld_relaxed(prog + gi - 1) < need) {
+              if (ns) __nanosleep(ns);
+            }
+          }
+          (void)ld_acquire(prog + gi - 1);
+        }
+        __syncwarp();
+      }
+      const int64_t cg = (j == 0) ? gi : gi + 1 + (j - 1) * b;
+      const int64_t w0 = gi + 1 + j * b;
+      const int L = (int)((b < n - w0) ? b : n - w0);
+      const int nleft = (int)(w0 - cg);
+      const int64_t tend = (w0 + L + b < n) ? w0 + L + b : n;
+      const int nT = (int)(tend - (w0 + L));
+      const bool last = gi + 1 + (j + 1) * b > n - 2;
+      const int64_t slot = (int64_t)j * (slot_n - 2) - (int64_t)b * j * (j - 1) / 2 + slot_col0 + gi;
+      double* SL = S.SLC[cur];
+      double* SC = S.SLC[cur ^ 1];
+      // ---- stage (zero outside the live region); 16 columns of independent loads per batch,
+      //      so a step pays 4 L2 round trips, not one per element
+      for (int q0 = 0; q0 < WMAX; q0 += 16) {
+        double ra[16][2], rb[16][2];
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int q = q0 + qq, r = lane + 32 * h;
+            if (wid == 0) {
+              ra[qq][h] = (j == 0 && q < nleft && r < L)
+                              ? __ldcg(Bd + (cg + q) * LDB + (w0 + r - cg - q)) : 0.0;
+              rb[qq][h] = (r >= q && r < L) ? __ldcg(Bd + (w0 + q) * LDB + (r - q)) : 0.0;
+            } else {
+              ra[qq][h] = (q < L && r < nT) ? __ldcg(Bd + (w0 + q) * LDB + (L + r - q)) : 0.0;
+              rb[qq][h] = 0.0;
+            }
+          }
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int q = q0 + qq, r = lane + 32 * h;
+            if (wid == 0) {
+              if (j == 0) SL[r * LDW + q] = ra[qq][h];
+              if (r >= q) {
+                S.SW[r * LDW + q] = rb[qq][h];
+                S.SW[q * LDW + r] = rb[qq][h];
+              }
+            } else {
+              SC[r * LDW + q] = ra[qq][h];
+            }
+          }
+      }
+      __syncthreads();
+      // ---- the Householder vector (warp 0)
+      if (wid == 0) {
+        double x[2], t2 = 0.0;
+        for (int h = 0; h < 2; ++h) {
+          const int r = lane + 32 * h;
+          x[h] = (r < L) ? SL[r * LDW] : 0.0;
+          if (r >= 1 && r < L) t2 += x[h] * x[h];
+        }
+        const double tail = warp_sum(t2);
+        if (tail == 0.0) {
+          if (lane == 0) S.tau = 0.0;
+        } else {
+          const double x0 = __shfl_sync(0xffffffffu, x[0], 0);
+          const double nrm = sqrt(x0 * x0 + tail);
+          const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+          const double denom = x0 - alpha;
+          double vv = 0.0;
+          for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h;
+            const double v = (r == 0) ? 1.0 : ((r < L) ? x[h] / denom : 0.0);
+            S.vs[r] = v;
+            if (r >= 1) vv += v * v;
+            if (r < L) SL[r * LDW] = (r == 0) ? alpha : 0.0;
+          }
+          const double vsq = 1.0 + warp_sum(vv);
+          if (lane == 0) S.tau = 2.0 / vsq;
+        }
+      }
+      __syncthreads();
+      const double tau = S.tau;
+      if (wid == 0) {
+        if (tau != 0.0) {
+          // ---- H from the left on the bulge columns strictly between (column q)
+          for (int q = lane; q < WMAX; q += 32) {
+            if (q >= 1 && q < nleft) {
+              double d0 = 0.0, d1 = 0.0;
+              for (int r = 0; r < WMAX; r += 2) {
+                d0 = fma(S.vs[r], SL[r * LDW + q], d0);
+                d1 = fma(S.vs[r + 1], SL[(r + 1) * LDW + q], d1);
+              }
+              const double dot = tau * (d0 + d1);
+              for (int r = 0; r < WMAX; ++r) SL[r * LDW + q] -= dot * S.vs[r];
+            }
+          }
+          // ---- H A H on the window (row r)
+          double u[2], vw = 0.0;
+          for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h;
+            double a0 = 0.0, a1 = 0.0;
+            for (int c = 0; c < WMAX; c += 2) {
+              a0 = fma(S.SW[r * LDW + c], S.vs[c], a0);
+              a1 = fma(S.SW[r * LDW + c + 1], S.vs[c + 1], a1);
+            }
+            u[h] = tau * (a0 + a1);
+            vw += S.vs[r] * u[h];
+          }
+          const double gam = 0.5 * tau * warp_sum(vw);
+          for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h;
+            S.wv[r] = u[h] - gam * S.vs[r];
+          }
+          __syncwarp();
+          for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h;
+            const double v = S.vs[r], w = S.wv[r];
+            for (int c = 0; c <= r; ++c) S.SW[r * LDW + c] -= v * S.wv[c] + w * S.vs[c];
+          }
+          __syncwarp();
+        }
+        // ---- write back: left block, window, reflector slot
+        if (tau != 0.0 || j > 0) {
+          for (int q = 0; q < nleft; ++q)
+            for (int r = lane; r < L; r += 32) Bd[(cg + q) * LDB + (w0 + r - cg - q)] = SL[r * LDW + q];
+        }
+        if (tau != 0.0) {
+          for (int c = 0; c < L; ++c)
+            for (int r = c + lane; r < L; r += 32) Bd[(w0 + c) * LDB + (r - c)] = S.SW[r * LDW + c];
+        }
+        if (tau_out) {
+          if (lane == 0) tau_out[slot] = tau;
+          for (int r = lane; r < vld; r += 32)
+            V_out[slot * vld + r] = (tau != 0.0) ? ((r < L) ? S.vs[r] : 0.0) : (r == 0 ? 1.0 : 0.0);
+        }
+      } else {
+        // ---- H from the right on the coupling rows (row t)
+        if (tau != 0.0) {
+          for (int t = lane; t < WMAX; t += 32) {
+            double d0 = 0.0, d1 = 0.0;
+            for (int c = 0; c < WMAX; c += 2) {
+              d0 = fma(SC[t * LDW + c], S.vs[c], d0);
+              d1 = fma(SC[t * LDW + c + 1], S.vs[c + 1], d1);
+            }
+            const double dot = tau * (d0 + d1);
+            for (int c = 0; c < WMAX; ++c) SC[t * LDW + c] -= dot * S.vs[c];
+          }
+        }
+        if (last) {
+          for (int c = 0; c < L; ++c)
+            for (int t = lane; t < nT; t += 32) Bd[(w0 + c) * LDB + (L + t - c)] = SC[t * LDW + c];
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_relaxed(prog + gi, (int)(j + 1));
+      }
+      cur ^= 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_relaxed(prog + gi, DONE);
+    }
+  }
+}
+
 }  // namespace
 
 int64_t bc_num_reflectors(int64_t n, int b) {
@@ -301,8 +502,8 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
                     int64_t sweep_end, double* d, double* e, double* band_out, double* tau,
                     double* V, int vld, void* ws, int64_t slot_n, int64_t slot_col0) {
   if (slot_n <= 0) slot_n = n;
-  if (b < 1 || b > BMAX) {
-    set_error("bc_reduce: bandwidth %d outside [1, %d] (device kernel limit)", b, BMAX);
+  if (b < 1 || b > WMAX) {
+    set_error("bc_reduce: bandwidth %d outside [1, %d] (device kernel limit)", b, WMAX);
     return ERR_VALUE;
   }
   if (tau && vld < b) {
@@ -327,14 +528,15 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
         nref += std::max<int64_t>(0, std::min<int64_t>(sweep_end, n - 2 - j * b));
       flops_add(14.0 * b * b * (double)nref);
     }
-    const size_t smem = sizeof(ChaseSmem);
-    auto kfn = bc_chase_kernel;
-    static int attr_dev = -1;
+    const bool wide = b > BMAX;
+    const size_t smem = wide ? sizeof(ChaseWideSmem) : sizeof(ChaseSmem);
+    auto kfn = wide ? bc_chase_wide_kernel : bc_chase_kernel;
+    static int attr_dev[2] = {-1, -1};
     int dev;
     PEVD_CUDA(cudaGetDevice(&dev));
-    if (attr_dev != dev) {
+    if (attr_dev[wide] != dev) {
       PEVD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_dev = dev;
+      attr_dev[wide] = dev;
     }
     int per_sm = 0;
     PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 64, smem));

@@ -582,9 +582,9 @@ int dist_syevd(Comm& C, int64_t n, int b, double* blk, int64_t ldb, const int64_
                const int64_t* back_lo, double* lam, double* Q, int64_t ldq, int want_vectors,
                int order, cudaStream_t user_stream, pevd_dist_stats* out) {
   const int G = C.size(), r = C.rank();
-  if (n < 3 || b < 1 || b >= n || b > 32 || col_lo[0] != 0 || col_lo[G] != n ||
+  if (n < 3 || b < 1 || b >= n || b > 64 || col_lo[0] != 0 || col_lo[G] != n ||
       back_lo[0] != 0 || back_lo[G] != n) {
-    set_error("dist_syevd: bad arguments (n=%lld, b=%d; need 3 <= n, 1 <= b <= 32, b < n, "
+    set_error("dist_syevd: bad arguments (n=%lld, b=%d; need 3 <= n, 1 <= b <= 64, b < n, "
               "partitions covering [0, n))", (long long)n, b);
     return ERR_VALUE;
   }

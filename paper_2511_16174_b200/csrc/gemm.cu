@@ -793,6 +793,14 @@ int gemm(cudaStream_t st, const GemmArgs& g0, double* ws, int64_t ws_elems) {
       if (ks > 1) PEVD_TRY(splitk_finish(st, g, ks, ws));
       return OK;
     }
+    if (g.n <= 64) {
+      // panels of 33..64 columns (b > 32): 128 x 64 tiles, 8 warps of 32 x 32
+      const int ks64 = ws ? pick_ks(cdiv(g.m, 128), g.k, 2 * sms, 512, g.m * g.n, ws_elems) : 1;
+      if (g.transB) PEVD_TRY((launch_fast<false, true, 128, 64, 16, 32, 32, 3, true>(st, g, ks64, ks64 > 1 ? ws : nullptr)));
+      else PEVD_TRY((launch_fast<false, false, 128, 64, 16, 32, 32, 3, true>(st, g, ks64, ks64 > 1 ? ws : nullptr)));
+      if (ks64 > 1) PEVD_TRY(splitk_finish(st, g, ks64, ws));
+      return OK;
+    }
     return launch_generic<128, 128, 16, 64, 32, 3>(st, g, 1, nullptr);
   }
   if (g.n <= 32) {

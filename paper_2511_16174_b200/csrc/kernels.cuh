@@ -81,7 +81,7 @@ int sbr_back_apply_right(cudaStream_t st, int64_t n, int b, const double* Yfull,
 // Right-apply the bulge reflectors to the rows of X (nrows x n, col-major ldx):
 // X <- X Q_b  (== (Q_b^T X^T)^T, the reordered BC-Back, backtrans.py:277-310).
 int64_t bc_back_ws_bytes(int64_t n, int64_t nrows, int b);
-// the DMMA compact-WY kernels handle b in {8, 16, 24, 32} (reflector stride vld >= b); other b
+// the DMMA compact-WY kernels handle b in {8, 16, ..., 64} (reflector stride vld >= b); other b
 // use the reflector-by-reflector kernels
 bool bc_back_dmma_ok(int b, int vld);
 int bc_back_right(cudaStream_t st, int64_t n, int b, const double* tau, const double* V, int vld,

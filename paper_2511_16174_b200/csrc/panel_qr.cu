@@ -20,13 +20,10 @@ namespace pevd {
 namespace {
 
 constexpr int QR_THREADS = 512;
-constexpr int KMAX = 32;
-constexpr int LDP = KMAX + 1;  // smem panel row stride (doubles)
-constexpr int NVAL = 2 * KMAX; // partial values per CTA per step: h[0..31], g[0..31]
-constexpr int NG = QR_THREADS / NVAL;  // thread groups splitting the rows of a partial
+constexpr int KMAX = 64;        // widest panel (b <= 64); 32-wide panels run the KM = 32 build
 
 struct QrWork {
-  double* part;     // [2][MAXCTA][NVAL], double-buffered by step parity
+  double* part;     // [2][MAXCTA][2 KMAX], double-buffered by step parity
   double* piv;      // [2][KMAX]
   unsigned* bar;    // [2] barrier count / generation
 };
@@ -51,19 +48,23 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
   __syncthreads();
 }
 
+template <int KM>
 __global__ void __launch_bounds__(QR_THREADS)
     panel_qr_kernel(int64_t m, int k, const double* panel, int64_t ldp, double* Rout,
                     double* Y1, int64_t ldy1, double* Y2, int64_t ldy2,
                     double* __restrict__ W, int64_t ldw, double* __restrict__ Tout,
                     QrWork wk, int64_t rows_per_cta) {
+  constexpr int LDP = KM + 1;            // smem panel row stride (doubles)
+  constexpr int NVAL = 2 * KM;           // partial values per CTA per step: h[0..KM), g[0..KM)
+  constexpr int NG = QR_THREADS / NVAL;  // thread groups splitting the rows of a partial
   extern __shared__ __align__(16) double sm[];
   double* P = sm;                                      // [rows_per_cta][LDP]
   double* red = P + rows_per_cta * LDP;                // [4][NVAL]
   double* hv = red + NG * NVAL;                        // [NVAL] reduced values
-  double* T = hv + NVAL;                               // [KMAX][KMAX] col-major T
-  double* coef = T + KMAX * KMAX;                      // [KMAX]
-  double* scal = coef + KMAX;                          // [4]: denom, tau, alpha, flag
-  double* taus = scal + 4;                             // [KMAX]
+  double* T = hv + NVAL;                               // [KM][KM] col-major T
+  double* coef = T + KM * KM;                      // [KM]
+  double* scal = coef + KM;                          // [4]: denom, tau, alpha, flag
+  double* taus = scal + 4;                             // [KM]
 
   const int tid = threadIdx.x;
   const unsigned ncta = gridDim.x;
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(QR_THREADS)
   // load the row chunk (coalesced along rows, column by column)
   for (int c = 0; c < k; ++c)
     for (int lr = tid; lr < nr; lr += QR_THREADS) P[lr * LDP + c] = panel[r0 + lr + c * ldp];
-  for (int i = tid; i < KMAX * KMAX; i += QR_THREADS) T[i] = 0.0;
+  for (int i = tid; i < KM * KM; i += QR_THREADS) T[i] = 0.0;
   __syncthreads();
 
   for (int j = 0; j <= k; ++j) {
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(QR_THREADS)
     {
       const int vi = tid % NVAL, grp = tid / NVAL;  // NG groups
       double s = 0.0;
-      if (vi < KMAX) {
+      if (vi < KM) {
         const int c = vi;
         if (j < k && c >= j && c < k) {
           double s1 = 0.0;
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(QR_THREADS)
           s += s1;
         }
       } else {
-        const int q = vi - KMAX;
+        const int q = vi - KM;
         const int jp = j - 1;  // previous reflector
         if (jp >= 1 && q < jp) {
           for (int lr = grp; lr < nr; lr += NG) {
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(QR_THREADS)
     // (buffers alternate by step parity: a CTA can run at most one barrier ahead, so it never
     //  overwrites values a slower CTA has yet to read)
     double* part = wk.part + (j & 1) * (MAXCTA * NVAL);
-    double* piv = wk.piv + (j & 1) * KMAX;
+    double* piv = wk.piv + (j & 1) * KM;
     if (j < k && j >= r0 && j < r1 && tid < k) {
       piv[tid] = P[(j - r0) * LDP + tid];
     }
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(QR_THREADS)
       for (int q = 0; q < NG; ++q) s += red[q * NVAL + tid];
       hv[tid] = s;
     }
-    if (tid < KMAX) coef[tid] = (j < k && tid >= j && tid < k) ? __ldcg(piv + tid) : 0.0;
+    if (tid < KM) coef[tid] = (j < k && tid >= j && tid < k) ? __ldcg(piv + tid) : 0.0;
     __syncthreads();
     // ---- T column j-1: T[0:jp, jp] = -tau_jp * T[0:jp, 0:jp] * g[0:jp]  (row q per thread;
     //      column jp only reads columns < jp, so all rows are independent)
@@ -165,11 +166,11 @@ __global__ void __launch_bounds__(QR_THREADS)
       const int jp = j - 1, q = tid;
       const double tj = taus[jp];
       if (q == jp) {
-        T[jp + jp * KMAX] = tj;
+        T[jp + jp * KM] = tj;
       } else {
         double s = 0.0;
-        for (int t = q; t < jp; ++t) s += T[q + t * KMAX] * hv[KMAX + t];
-        T[q + jp * KMAX] = -tj * s;
+        for (int t = q; t < jp; ++t) s += T[q + t * KM] * hv[KM + t];
+        T[q + jp * KM] = -tj * s;
       }
     }
     if (j == k) break;
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(QR_THREADS)
     const double denom = scal[0], tau = scal[1], alpha = scal[2];
     const bool active = scal[3] != 0.0;
     // coefficients tau * v^T a_c for c > j
-    if (tid < KMAX) {
+    if (tid < KM) {
       const int c = tid;
       double cf = 0.0;
       if (active && c > j && c < k) cf = tau * (coef[c] + hv[c] / denom);
@@ -206,8 +207,8 @@ __global__ void __launch_bounds__(QR_THREADS)
     }
     __syncthreads();
     if (active) {
-      for (int idx = tid; idx < nr * KMAX; idx += QR_THREADS) {
-        const int lr = idx / KMAX, c = idx % KMAX;
+      for (int idx = tid; idx < nr * KM; idx += QR_THREADS) {
+        const int lr = idx / KM, c = idx % KM;
         const int64_t r = r0 + lr;
         if (r < j || c <= j || c >= k) continue;
         const double v = (r == j) ? 1.0 : P[lr * LDP + j];
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(QR_THREADS)
       double s = 0.0;
       for (int q = 0; q <= c; ++q) {
         const double y = (r > q) ? P[lr * LDP + q] : (r == q ? 1.0 : 0.0);
-        s += y * T[q + c * KMAX];
+        s += y * T[q + c * KM];
       }
       W[r + c * ldw] = s;
     }
@@ -246,14 +247,14 @@ __global__ void __launch_bounds__(QR_THREADS)
   if (Tout && blockIdx.x == 0) {
     for (int i = tid; i < k * k; i += QR_THREADS) {
       const int q = i % k, c = i / k;
-      Tout[q + c * k] = T[q + c * KMAX];
+      Tout[q + c * k] = T[q + c * KM];
     }
   }
 }
 
 }  // namespace
 
-int64_t panel_qr_ws_bytes() { return (int64_t)(2 * MAXCTA * NVAL + 2 * KMAX + 16) * 8; }
+int64_t panel_qr_ws_bytes() { return (int64_t)(2 * MAXCTA * 2 * KMAX + 2 * KMAX + 16) * 8; }
 
 int panel_qr(cudaStream_t st, int64_t m, int k, const double* panel, int64_t ldp, double* R,
              double* Y1, int64_t ldy1, double* Y2, int64_t ldy2, double* W, int64_t ldw,
@@ -274,27 +275,29 @@ int panel_qr(cudaStream_t st, int64_t m, int k, const double* panel, int64_t ldp
   if (ncta < 1) ncta = 1;
   int64_t rows = cdiv(m, ncta);
   ncta = (int)cdiv(m, rows);
-  const size_t smem = (size_t)(rows * LDP + NG * NVAL + NVAL + KMAX * KMAX + KMAX + 4 + KMAX) * 8;
+  const int KM = k <= 32 ? 32 : 64;
+  const int NVAL = 2 * KM, NG = QR_THREADS / NVAL;
+  const size_t smem = (size_t)(rows * (KM + 1) + NG * NVAL + NVAL + KM * KM + KM + 4 + KM) * 8;
   if (smem > 227 * 1024) {
-    set_error("panel_qr: panel too tall for the resident-panel kernel (m=%lld)", (long long)m);
+    set_error("panel_qr: panel too tall for the resident-panel kernel (m=%lld, k=%d)",
+              (long long)m, k);
     return ERR_VALUE;
   }
-  static int attr_dev = -1;
+  const void* kern = KM == 32 ? (const void*)panel_qr_kernel<32> : (const void*)panel_qr_kernel<64>;
+  static int attr_dev[2] = {-1, -1};
   int dev;
   PEVD_CUDA(cudaGetDevice(&dev));
-  if (attr_dev != dev) {
-    PEVD_CUDA(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
-    attr_dev = dev;
+  if (attr_dev[KM == 64] != dev) {
+    PEVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_dev[KM == 64] = dev;
   }
   QrWork wk;
   wk.part = (double*)ws;
-  wk.piv = wk.part + 2 * MAXCTA * NVAL;
+  wk.piv = wk.part + 2 * MAXCTA * 2 * KMAX;
   wk.bar = (unsigned*)(wk.piv + 2 * KMAX);
   PEVD_CUDA(cudaMemsetAsync(wk.bar, 0, 2 * sizeof(unsigned), st));
   void* args[] = {&m, &k, &panel, &ldp, &R, &Y1, &ldy1, &Y2, &ldy2, &W, &ldw, &T, &wk, &rows};
-  PEVD_CUDA(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel, dim3(ncta),
-                                        dim3(QR_THREADS), args, smem, st));
+  PEVD_CUDA(cudaLaunchCooperativeKernel(kern, dim3(ncta), dim3(QR_THREADS), args, smem, st));
   count_launch();
   return OK;
 }

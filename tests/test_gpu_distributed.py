@@ -38,7 +38,8 @@ def _want_by_stage(n, b, G, vectors, skew=0.0):
 
 @pytest.mark.parametrize("G,n,b,order", [(2, 64, 8, "pipelined"), (2, 300, 32, "conventional"),
                                          (3, 300, 32, "pipelined"), (3, 257, 32, "sequential"),
-                                         (4, 512, 32, "conventional"), (4, 200, 16, "pipelined")])
+                                         (4, 512, 32, "conventional"), (4, 200, 16, "pipelined"),
+                                         (2, 400, 48, "conventional"), (3, 500, 64, "pipelined")])
 def test_workers_in_one_process(G, n, b, order):
     import paper_2511_16174_b200 as pkg
     from paper_2511_16174_b200.schedule import comm_broadcast_words, validate_trace

@@ -26,7 +26,11 @@ def sym(n, seed):
 @pytest.mark.parametrize("n,b,order", [(2, 4, "pipelined"), (3, 2, "pipelined"), (40, 4, "pipelined"),
                                        (64, 8, "sequential"), (64, 8, "conventional"),
                                        (97, 7, "pipelined"), (256, 32, "pipelined"),
-                                       (256, 32, "conventional"), (1024, 32, "pipelined")])
+                                       (256, 32, "conventional"), (1024, 32, "pipelined"),
+                                       (300, 40, "pipelined"), (300, 40, "conventional"),
+                                       (700, 64, "pipelined"), (700, 64, "conventional"),
+                                       (129, 33, "sequential"), (500, 48, "conventional"),
+                                       (400, 56, "pipelined")])
 def test_syevd_matches_oracle(n, b, order):
     a = sym(n, n + b)
     lam, q, st = dev().syevd(a, b, True, order)
@@ -214,3 +218,12 @@ def test_structured_inputs(case, order):
     assert orc.orthogonality(q) <= 1e-15
     if name == "zero":
         np.testing.assert_array_equal(lam, np.zeros(n))
+
+
+def test_bandwidth_above_64_rejected():
+    """b <= 64 runs on the device kernels (multiples of 8 on the DMMA BC-Back, the rest on
+    the generic paths); wider bands raise ValueError, as pipeline.py:57-82 does for bad configs."""
+    import paper_2511_16174_b200 as pkg
+    a = sym(200, 3)
+    with pytest.raises(ValueError, match="64"):
+        pkg.run(a, pkg.PipelineConfig(workers=1, b=65))

@@ -39,7 +39,8 @@ def test_dgemm_matches_numpy(m, n, k, ta, tb):
     np.testing.assert_allclose(got, want, atol=1e-12 * np.sqrt(k) * 4, rtol=0)
 
 
-@pytest.mark.parametrize("m,k", [(8, 8), (40, 8), (300, 32), (1000, 32), (5000, 17), (20000, 32)])
+@pytest.mark.parametrize("m,k", [(8, 8), (40, 8), (300, 32), (1000, 32), (5000, 17), (20000, 32),
+                                 (100, 33), (700, 48), (3000, 64), (40000, 64)])
 def test_panel_qr_matches_oracle(m, k):
     p = np.random.default_rng(m + k).standard_normal((m, k))
     R, Y, W, T = dev().panel_qr(p)
@@ -55,7 +56,8 @@ def test_panel_qr_matches_oracle(m, k):
                                    atol=1e-12 * np.abs(p).max() * np.sqrt(m))
 
 
-@pytest.mark.parametrize("n,b", [(12, 4), (11, 4), (64, 8), (91, 7), (200, 32), (513, 32), (1024, 32)])
+@pytest.mark.parametrize("n,b", [(12, 4), (11, 4), (64, 8), (91, 7), (200, 32), (513, 32), (1024, 32),
+                                 (300, 40), (600, 64)])
 def test_sbr_band_matches_oracle(n, b):
     a = sym(n, n + b)
     bands, ystair, tall = dev().sbr(a, b)
@@ -67,7 +69,8 @@ def test_sbr_band_matches_oracle(n, b):
         np.testing.assert_allclose(ystair[t0:, c0:c0 + Y.shape[1]], Y, atol=1e-11)
 
 
-@pytest.mark.parametrize("n,b", [(10, 2), (24, 3), (40, 4), (64, 8), (100, 16), (130, 32), (700, 32)])
+@pytest.mark.parametrize("n,b", [(10, 2), (24, 3), (40, 4), (64, 8), (100, 16), (130, 32), (700, 32),
+                                 (80, 33), (500, 48), (900, 64)])
 def test_bc_matches_oracle(n, b):
     rng = np.random.default_rng(n * b)
     a = rng.standard_normal((n, n))
@@ -124,7 +127,8 @@ def test_stedc_matches_reference_solver(case):
 
 
 @pytest.mark.parametrize("n,b", [(24, 3), (64, 8), (130, 32), (500, 32), (701, 32), (333, 8),
-                                 (400, 16), (515, 24), (257, 12)])
+                                 (400, 16), (515, 24), (257, 12), (300, 40), (350, 48),
+                                 (200, 56), (400, 64), (300, 44)])
 def test_bc_back_matches_oracle(n, b):
     rng = np.random.default_rng(n)
     a = rng.standard_normal((n, n))
