@@ -3,6 +3,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include "comm.h"
@@ -68,12 +69,27 @@ PeerComm::PeerComm(PeerWorld* w, int rank) : w_(w) {
   size_ = w->G;
   cudaEventCreateWithFlags(&w_->ready[rank], cudaEventDisableTiming);
   cudaEventCreateWithFlags(&w_->done[rank], cudaEventDisableTiming);
+  const char* e = getenv("PEVD_PEER_SERIAL");
+  serialize_ = e && e[0] == '1';
+  if (serialize_) cudaEventCreateWithFlags(&serial_, cudaEventDisableTiming);
 }
 
 PeerComm::~PeerComm() {
   if (w_->ready[rank_]) cudaEventDestroy(w_->ready[rank_]);
   if (w_->done[rank_]) cudaEventDestroy(w_->done[rank_]);
   w_->ready[rank_] = w_->done[rank_] = nullptr;
+  if (serial_) cudaEventDestroy(serial_);
+}
+
+void PeerComm::serial_begin(cudaStream_t st, bool involved) {
+  if (serialize_ && involved && serial_live_) cudaStreamWaitEvent(st, serial_, 0);
+}
+
+void PeerComm::serial_end(cudaStream_t st, bool involved) {
+  if (serialize_ && involved) {
+    cudaEventRecord(serial_, st);
+    serial_live_ = true;
+  }
 }
 
 int PeerComm::post(const void* p, cudaStream_t st) {
@@ -97,6 +113,7 @@ int PeerComm::finish(cudaStream_t st) {
 
 int PeerComm::bcast(void* buf, int64_t bytes, int root, cudaStream_t st) {
   if (size_ == 1 || bytes <= 0) return OK;
+  serial_begin(st, true);
   PEVD_TRY(post(buf, st));
   if (rank_ != root) {
     PEVD_CUDA(cudaStreamWaitEvent(st, w_->ready[root], 0));
@@ -109,6 +126,7 @@ int PeerComm::bcast(void* buf, int64_t bytes, int root, cudaStream_t st) {
     for (int x = 0; x < size_; ++x)
       if (x != root) PEVD_CUDA(cudaStreamWaitEvent(st, w_->done[x], 0));
   }
+  serial_end(st, true);
   return OK;
 }
 
@@ -119,6 +137,7 @@ int PeerComm::allgatherv(const void* send, const int64_t* counts, void* recv, cu
       PEVD_CUDA(cudaMemcpyAsync(recv, send, (size_t)counts[0], cudaMemcpyDeviceToDevice, st));
     return OK;
   }
+  serial_begin(st, true);
   PEVD_TRY(post(send, st));
   off = 0;
   for (int x = 0; x < size_; ++x) {
@@ -139,12 +158,15 @@ int PeerComm::allgatherv(const void* send, const int64_t* counts, void* recv, cu
   // every rank's send buffer was read by every other rank
   for (int x = 0; x < size_; ++x)
     if (x != rank_) PEVD_CUDA(cudaStreamWaitEvent(st, w_->done[x], 0));
+  serial_end(st, true);
   return OK;
 }
 
 int PeerComm::p2p(const void* send, void* recv, int64_t bytes, int src, int dst,
                   cudaStream_t st) {
   if (bytes <= 0 || src == dst) return OK;
+  const bool involved = rank_ == src || rank_ == dst;
+  serial_begin(st, involved);
   PEVD_TRY(post(rank_ == src ? send : nullptr, st));
   if (rank_ == dst) {
     PEVD_CUDA(cudaStreamWaitEvent(st, w_->ready[src], 0));
@@ -153,6 +175,7 @@ int PeerComm::p2p(const void* send, void* recv, int64_t bytes, int src, int dst,
   }
   PEVD_TRY(finish(st));
   if (rank_ == src) PEVD_CUDA(cudaStreamWaitEvent(st, w_->done[dst], 0));
+  serial_end(st, involved);
   return OK;
 }
 
@@ -161,10 +184,12 @@ int PeerComm::device_barrier(cudaStream_t st) {
   // (done events: a rank re-records them only after the next collective's first rendezvous,
   //  which this rank joins after enqueueing these waits; its ready event could already be
   //  re-recorded by its next post())
+  serial_begin(st, true);
   PEVD_TRY(post(nullptr, st));
   PEVD_TRY(finish(st));
   for (int x = 0; x < size_; ++x)
     if (x != rank_) PEVD_CUDA(cudaStreamWaitEvent(st, w_->done[x], 0));
+  serial_end(st, true);
   return OK;
 }
 

@@ -99,6 +99,13 @@ class PeerComm : public Comm {
   PeerWorld* w_;
   int post(const void* p, cudaStream_t st);   // publish pointer + ready event, rendezvous
   int finish(cudaStream_t st);                // publish done event, rendezvous, wait on all
+  // PEVD_PEER_SERIAL=1: every operation's device work starts after the previous operation's
+  // (in issue order, whatever the streams) -- the ordering NCCL imposes on the operations of
+  // one communicator, so the in-process tests catch a stream graph that would deadlock there
+  void serial_begin(cudaStream_t st, bool involved);
+  void serial_end(cudaStream_t st, bool involved);
+  bool serialize_ = false, serial_live_ = false;
+  cudaEvent_t serial_ = nullptr;
 };
 
 // ---------------------------------------------------------------- one process per GPU, NCCL

@@ -72,6 +72,25 @@ def test_workers_in_one_process(G, n, b, order):
     np.testing.assert_array_equal(res.Q, res2.Q)
 
 
+@pytest.mark.parametrize("G,n,b,order", [(3, 700, 32, "conventional"), (4, 600, 32, "pipelined"),
+                                         (2, 500, 40, "sequential")])
+def test_workers_with_nccl_ordering(G, n, b, order, monkeypatch):
+    """PEVD_PEER_SERIAL=1 makes the in-process communicator order every operation's device
+    work after the previous one's, whatever the streams -- what NCCL does to the operations of
+    one communicator.  The orchestrator's stream graph (lookahead on a second stream, the
+    back-transform stream, device barriers) must stay acyclic under that order, or the multi-
+    process NCCL run would deadlock where this run hangs.  Same results as without it."""
+    import paper_2511_16174_b200 as pkg
+    a = _sym(n, 5 * n + G)
+    cfg = pkg.PipelineConfig(workers=G, b=b, order=order)
+    ref, _, _, _ = pkg.run(a, cfg)
+    monkeypatch.setenv("PEVD_PEER_SERIAL", "1")
+    res, events, ledger, _ = pkg.run(a, cfg)
+    np.testing.assert_array_equal(res.lam, ref.lam)
+    np.testing.assert_array_equal(res.Q, ref.Q)
+    assert ledger.total_words > 0
+
+
 def test_comm_overlaps_trailing_update():
     """Lookahead, from the device events: the next group's first panel is factored and its
     broadcast runs while the previous group's rank-2K trailing update (a helper-lane SBR event,
