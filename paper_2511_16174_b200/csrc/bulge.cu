@@ -11,10 +11,11 @@
 // (e.g. beside another EVD on another stream).  Sweeps are assigned round-robin (sweep gi to
 // warp gi mod total): consecutive sweeps land on consecutive CTAs, i.e. on different SMs, which
 // spreads the ~n/(3b) in-flight sweeps evenly (an atomic sweep ticket gives a data-dependent
-// mapping that crowds some SMs: 1.54 s instead of 1.07 s at n = 49152).  The producer orders its
-// band stores before the progress flag with a gpu-scope fence; the consumer polls the flag
-// relaxed and then re-reads it once with ld.acquire before touching band data, which it reads
-// through L2 (ld.cg).
+// mapping that crowds some SMs: 1.54 s instead of 1.07 s at n = 49152).  The producer publishes
+// its progress with st.release.gpu (after a CTA barrier, so the release covers both warps' band
+// stores cumulatively; a fence.sc -- __threadfence, MEMBAR.SC -- is stronger than the pattern
+// needs); the consumer polls the flag relaxed and then re-reads it once with ld.acquire before
+// touching band data, which it reads through L2 (ld.cg).
 //
 // Per step the warp stages its region in shared memory (lane = row of the window):
 //   left block  S[w0:w0+L, cg:w0]     (the column to annihilate + the bulge columns between)
@@ -265,15 +266,13 @@ __global__ void __launch_bounds__(64)
       //      stores before thread 0's gpu-scope fence, whose release covers them cumulatively)
       __syncthreads();
       if (threadIdx.x == 0) {
-        __threadfence();
-        st_relaxed(prog + gi, (int)(j + 1));
+        st_release(prog + gi, (int)(j + 1));
       }
       cur ^= 1;  // this step's coupling block is the next step's left block
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
-      st_relaxed(prog + gi, DONE);
+      st_release(prog + gi, DONE);
     }
   }
 }
@@ -466,15 +465,13 @@ __global__ void __launch_bounds__(64)
       }
       __syncthreads();
       if (threadIdx.x == 0) {
-        __threadfence();
-        st_relaxed(prog + gi, (int)(j + 1));
+        st_release(prog + gi, (int)(j + 1));
       }
       cur ^= 1;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
-      st_relaxed(prog + gi, DONE);
+      st_release(prog + gi, DONE);
     }
   }
 }
