@@ -278,28 +278,32 @@ __global__ void __launch_bounds__(64)
 }
 
 // ------------------------------------------------------------ 32 < b <= 64
-// The same wavefront, step and arithmetic for bandwidths past one warp's width: every "lane =
-// row / column" loop of bc_chase_kernel runs over rows lane and lane + 32, and the region is
-// staged straight into shared memory (the register staging would need 4 x 64 doubles per lane).
-// A fallback for the band-width parameter's wider settings, not a tuned path.
+// The same wavefront, step and arithmetic for bandwidths past one warp's width, on four warps:
+// warps 0-1 own the rows [32 w, 32 w + 32) of the left block and the window (and split the left
+// application's columns the same way), warps 2-3 the coupling rows.  The region is staged
+// straight into shared memory in 16-column batches of independent loads.
 constexpr int WMAX = 64;
 constexpr int LDW = WMAX + 1;
+constexpr int WIDE_THREADS = 128;
 
 struct ChaseWideSmem {
   double SLC[2][WMAX * LDW];
   double SW[WMAX * LDW];
   double vs[WMAX];
   double wv[WMAX];
+  double red[2];
   double tau;
 };
 
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(WIDE_THREADS)
     bc_chase_wide_kernel(int64_t n, int b, double* __restrict__ Bd, int64_t LDB, int* prog,
                          double* __restrict__ tau_out, double* __restrict__ V_out, int vld,
                          int64_t sweep_end, int64_t slot_n, int64_t slot_col0, int poll_ns) {
   extern __shared__ __align__(16) unsigned char smraw[];
   ChaseWideSmem& S = *reinterpret_cast<ChaseWideSmem*>(smraw);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool winw = wid < 2;                    // window warps 0-1, coupling warps 2-3
+  const int r = 32 * (wid & 1) + lane;          // this thread's row (window or coupling)
   const int64_t gend = sweep_end < n - 2 ? sweep_end : n - 2;
   for (int64_t gi = blockIdx.x; gi < gend; gi += gridDim.x) {
     int cur = 0;
@@ -327,48 +331,43 @@ __global__ void __launch_bounds__(64)
       const int64_t slot = (int64_t)j * (slot_n - 2) - (int64_t)b * j * (j - 1) / 2 + slot_col0 + gi;
       double* SL = S.SLC[cur];
       double* SC = S.SLC[cur ^ 1];
-      // ---- stage (zero outside the live region); 16 columns of independent loads per batch,
-      //      so a step pays 4 L2 round trips, not one per element
+      // ---- stage this thread's row of its blocks (zero outside the live region)
       for (int q0 = 0; q0 < WMAX; q0 += 16) {
-        double ra[16][2], rb[16][2];
+        double ra[16], rb[16];
 #pragma unroll
-        for (int qq = 0; qq < 16; ++qq)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int q = q0 + qq, r = lane + 32 * h;
-            if (wid == 0) {
-              ra[qq][h] = (j == 0 && q < nleft && r < L)
-                              ? __ldcg(Bd + (cg + q) * LDB + (w0 + r - cg - q)) : 0.0;
-              rb[qq][h] = (r >= q && r < L) ? __ldcg(Bd + (w0 + q) * LDB + (r - q)) : 0.0;
-            } else {
-              ra[qq][h] = (q < L && r < nT) ? __ldcg(Bd + (w0 + q) * LDB + (L + r - q)) : 0.0;
-              rb[qq][h] = 0.0;
-            }
+        for (int qq = 0; qq < 16; ++qq) {
+          const int q = q0 + qq;
+          if (winw) {
+            ra[qq] = (j == 0 && q < nleft && r < L)
+                         ? __ldcg(Bd + (cg + q) * LDB + (w0 + r - cg - q)) : 0.0;
+            rb[qq] = (r >= q && r < L) ? __ldcg(Bd + (w0 + q) * LDB + (r - q)) : 0.0;
+          } else {
+            ra[qq] = (q < L && r < nT) ? __ldcg(Bd + (w0 + q) * LDB + (L + r - q)) : 0.0;
+            rb[qq] = 0.0;
           }
+        }
 #pragma unroll
-        for (int qq = 0; qq < 16; ++qq)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int q = q0 + qq, r = lane + 32 * h;
-            if (wid == 0) {
-              if (j == 0) SL[r * LDW + q] = ra[qq][h];
-              if (r >= q) {
-                S.SW[r * LDW + q] = rb[qq][h];
-                S.SW[q * LDW + r] = rb[qq][h];
-              }
-            } else {
-              SC[r * LDW + q] = ra[qq][h];
+        for (int qq = 0; qq < 16; ++qq) {
+          const int q = q0 + qq;
+          if (winw) {
+            if (j == 0) SL[r * LDW + q] = ra[qq];
+            if (r >= q) {
+              S.SW[r * LDW + q] = rb[qq];
+              S.SW[q * LDW + r] = rb[qq];
             }
+          } else {
+            SC[r * LDW + q] = ra[qq];
           }
+        }
       }
       __syncthreads();
-      // ---- the Householder vector (warp 0)
+      // ---- the Householder vector (warp 0, two rows per lane)
       if (wid == 0) {
         double x[2], t2 = 0.0;
         for (int h = 0; h < 2; ++h) {
-          const int r = lane + 32 * h;
-          x[h] = (r < L) ? SL[r * LDW] : 0.0;
-          if (r >= 1 && r < L) t2 += x[h] * x[h];
+          const int rr = lane + 32 * h;
+          x[h] = (rr < L) ? SL[rr * LDW] : 0.0;
+          if (rr >= 1 && rr < L) t2 += x[h] * x[h];
         }
         const double tail = warp_sum(t2);
         if (tail == 0.0) {
@@ -380,11 +379,11 @@ __global__ void __launch_bounds__(64)
           const double denom = x0 - alpha;
           double vv = 0.0;
           for (int h = 0; h < 2; ++h) {
-            const int r = lane + 32 * h;
-            const double v = (r == 0) ? 1.0 : ((r < L) ? x[h] / denom : 0.0);
-            S.vs[r] = v;
-            if (r >= 1) vv += v * v;
-            if (r < L) SL[r * LDW] = (r == 0) ? alpha : 0.0;
+            const int rr = lane + 32 * h;
+            const double v = (rr == 0) ? 1.0 : ((rr < L) ? x[h] / denom : 0.0);
+            S.vs[rr] = v;
+            if (rr >= 1) vv += v * v;
+            if (rr < L) SL[rr * LDW] = (rr == 0) ? alpha : 0.0;
           }
           const double vsq = 1.0 + warp_sum(vv);
           if (lane == 0) S.tau = 2.0 / vsq;
@@ -392,87 +391,76 @@ __global__ void __launch_bounds__(64)
       }
       __syncthreads();
       const double tau = S.tau;
-      if (wid == 0) {
-        if (tau != 0.0) {
-          // ---- H from the left on the bulge columns strictly between (column q)
-          for (int q = lane; q < WMAX; q += 32) {
-            if (q >= 1 && q < nleft) {
-              double d0 = 0.0, d1 = 0.0;
-              for (int r = 0; r < WMAX; r += 2) {
-                d0 = fma(S.vs[r], SL[r * LDW + q], d0);
-                d1 = fma(S.vs[r + 1], SL[(r + 1) * LDW + q], d1);
-              }
-              const double dot = tau * (d0 + d1);
-              for (int r = 0; r < WMAX; ++r) SL[r * LDW + q] -= dot * S.vs[r];
-            }
-          }
-          // ---- H A H on the window (row r)
-          double u[2], vw = 0.0;
-          for (int h = 0; h < 2; ++h) {
-            const int r = lane + 32 * h;
-            double a0 = 0.0, a1 = 0.0;
-            for (int c = 0; c < WMAX; c += 2) {
-              a0 = fma(S.SW[r * LDW + c], S.vs[c], a0);
-              a1 = fma(S.SW[r * LDW + c + 1], S.vs[c + 1], a1);
-            }
-            u[h] = tau * (a0 + a1);
-            vw += S.vs[r] * u[h];
-          }
-          const double gam = 0.5 * tau * warp_sum(vw);
-          for (int h = 0; h < 2; ++h) {
-            const int r = lane + 32 * h;
-            S.wv[r] = u[h] - gam * S.vs[r];
-          }
-          __syncwarp();
-          for (int h = 0; h < 2; ++h) {
-            const int r = lane + 32 * h;
-            const double v = S.vs[r], w = S.wv[r];
-            for (int c = 0; c <= r; ++c) S.SW[r * LDW + c] -= v * S.wv[c] + w * S.vs[c];
-          }
-          __syncwarp();
-        }
-        // ---- write back: left block, window, reflector slot
-        if (tau != 0.0 || j > 0) {
-          for (int q = 0; q < nleft; ++q)
-            for (int r = lane; r < L; r += 32) Bd[(cg + q) * LDB + (w0 + r - cg - q)] = SL[r * LDW + q];
-        }
-        if (tau != 0.0) {
-          for (int c = 0; c < L; ++c)
-            for (int r = c + lane; r < L; r += 32) Bd[(w0 + c) * LDB + (r - c)] = S.SW[r * LDW + c];
-        }
-        if (tau_out) {
-          if (lane == 0) tau_out[slot] = tau;
-          for (int r = lane; r < vld; r += 32)
-            V_out[slot * vld + r] = (tau != 0.0) ? ((r < L) ? S.vs[r] : 0.0) : (r == 0 ? 1.0 : 0.0);
-        }
-      } else {
-        // ---- H from the right on the coupling rows (row t)
-        if (tau != 0.0) {
-          for (int t = lane; t < WMAX; t += 32) {
+      double u = 0.0;
+      if (tau != 0.0) {
+        if (winw) {
+          // ---- H from the left on the bulge columns strictly between (column q = r)
+          const int q = r;
+          if (q >= 1 && q < nleft) {
             double d0 = 0.0, d1 = 0.0;
-            for (int c = 0; c < WMAX; c += 2) {
-              d0 = fma(SC[t * LDW + c], S.vs[c], d0);
-              d1 = fma(SC[t * LDW + c + 1], S.vs[c + 1], d1);
+#pragma unroll 8
+            for (int rr = 0; rr < WMAX; rr += 2) {
+              d0 = fma(S.vs[rr], SL[rr * LDW + q], d0);
+              d1 = fma(S.vs[rr + 1], SL[(rr + 1) * LDW + q], d1);
             }
             const double dot = tau * (d0 + d1);
-            for (int c = 0; c < WMAX; ++c) SC[t * LDW + c] -= dot * S.vs[c];
+#pragma unroll 8
+            for (int rr = 0; rr < WMAX; ++rr) SL[rr * LDW + q] -= dot * S.vs[rr];
           }
+          // ---- u = tau A v on this row of the window
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll 8
+          for (int c = 0; c < WMAX; c += 2) {
+            a0 = fma(S.SW[r * LDW + c], S.vs[c], a0);
+            a1 = fma(S.SW[r * LDW + c + 1], S.vs[c + 1], a1);
+          }
+          u = tau * (a0 + a1);
+          const double part = warp_sum(S.vs[r] * u);
+          if (lane == 0) S.red[wid] = part;
+        } else {
+          // ---- H from the right on this coupling row
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll 8
+          for (int c = 0; c < WMAX; c += 2) {
+            d0 = fma(SC[r * LDW + c], S.vs[c], d0);
+            d1 = fma(SC[r * LDW + c + 1], S.vs[c + 1], d1);
+          }
+          const double dot = tau * (d0 + d1);
+#pragma unroll 8
+          for (int c = 0; c < WMAX; ++c) SC[r * LDW + c] -= dot * S.vs[c];
         }
-        if (last) {
-          for (int c = 0; c < L; ++c)
-            for (int t = lane; t < nT; t += 32) Bd[(w0 + c) * LDB + (L + t - c)] = SC[t * LDW + c];
+      }
+      __syncthreads();  // S.red complete; the left block's columns are final
+      if (tau != 0.0 && winw) {
+        const double gam = 0.5 * tau * (S.red[0] + S.red[1]);
+        S.wv[r] = u - gam * S.vs[r];
+      }
+      __syncthreads();  // all of w visible
+      if (winw) {
+        if (tau != 0.0) {
+          const double v = S.vs[r], w = S.wv[r];
+          for (int c = 0; c <= r; ++c) S.SW[r * LDW + c] -= v * S.wv[c] + w * S.vs[c];
         }
+        // ---- write back this row: left block, window (lower part), reflector slot
+        if ((tau != 0.0 || j > 0) && r < L)
+          for (int q = 0; q < nleft; ++q) Bd[(cg + q) * LDB + (w0 + r - cg - q)] = SL[r * LDW + q];
+        if (tau != 0.0 && r < L)
+          for (int c = 0; c <= r; ++c) Bd[(w0 + c) * LDB + (r - c)] = S.SW[r * LDW + c];
+        if (tau_out) {
+          if (threadIdx.x == 0) tau_out[slot] = tau;
+          for (int rr = threadIdx.x; rr < vld; rr += 64)
+            V_out[slot * vld + rr] =
+                (tau != 0.0) ? ((rr < L) ? S.vs[rr] : 0.0) : (rr == 0 ? 1.0 : 0.0);
+        }
+      } else if (last && r < nT) {
+        for (int c = 0; c < L; ++c) Bd[(w0 + c) * LDB + (L + r - c)] = SC[r * LDW + c];
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        st_release(prog + gi, (int)(j + 1));
-      }
+      if (threadIdx.x == 0) st_release(prog + gi, (int)(j + 1));
       cur ^= 1;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      st_release(prog + gi, DONE);
-    }
+    if (threadIdx.x == 0) st_release(prog + gi, DONE);
   }
 }
 
@@ -535,8 +523,9 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
       PEVD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_dev[wide] = dev;
     }
+    const int threads = wide ? WIDE_THREADS : 64;
     int per_sm = 0;
-    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 64, smem));
+    PEVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, smem));
     if (per_sm < 1) {
       set_error("bc_reduce: chase kernel cannot be resident");
       return ERR_CUDA;
@@ -555,7 +544,7 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
     int poll_ns = poll;
     void* args[] = {&n_, &b_, &Bd, &LDB_, &prog, &tau, &V, &vld_, &sweep_end_, &slot_n, &slot_col0,
                     &poll_ns};
-    PEVD_CUDA(cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(64), args,
+    PEVD_CUDA(cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(threads), args,
                                           smem, st));
     PEVD_LAUNCH_CHECK();
   } else if (tau && n >= 3 && slot_n == n && slot_col0 == 0) {
