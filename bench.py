@@ -336,10 +336,10 @@ def run_b200_single(args):
     achieved = fl[dom] / (stage_ms[dom] * 1e-3) / 1e12
     traffic, traffic_src = None, None
     try:  # dram bytes of that kernel's launch from the committed ncu capture (same n only)
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json"))).get(dom)
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json"))).get(dom)
         if tr and tr.get("n") == n:
             traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
-            traffic_src = "profiles/r01_traffic.json (ncu dram__bytes_read+write, one launch)"
+            traffic_src = "profiles/r02_traffic.json (ncu dram__bytes_read+write, one launch)"
     except Exception:
         pass
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3),
