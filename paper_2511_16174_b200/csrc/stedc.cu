@@ -41,6 +41,13 @@ struct Level {
 // per-merge scalar block (device), 16 ints / doubles
 enum { M_K = 0, M_ND, M_NROT, M_K1, M_K2, M_K3, M_NINT };
 
+// U layout of a merge with K roots: a zero row after the first k1 rows when k1 is odd, an even
+// leading dimension, so the two merge GEMMs' B operands are 16-byte aligned (see merge_gemm_args)
+__host__ __device__ __forceinline__ int u_pad(int k1) { return k1 & 1; }
+__host__ __device__ __forceinline__ int64_t u_ld(int K, int k1) { return (K + u_pad(k1) + 1) & ~1; }
+// elements reserved for a merge of size s (K <= s roots), even so the next offset stays aligned
+__host__ __device__ __forceinline__ int64_t u_elems(int64_t s) { return (s * (s + 2) + 1) & ~1LL; }
+
 // ---------------------------------------------------------------- helpers
 
 __global__ void scale_kernel(int64_t n, const double* d, const double* e, double* dw, double* ew,
@@ -571,10 +578,15 @@ __global__ void merge_vectors(MergeBufs B) {
   ss = warp_sum(ss);
   const double inv = 1.0 / sqrt(ss);
   double* U = B.U + B.uoff[mi];
+  const int k1 = B.mint[mi * M_NINT + M_K1];
+  const int pad = u_pad(k1);
+  const int64_t ldu = u_ld(K, k1);
   for (int i = lane; i < K; i += 32) {
     const double u = zh[i] / delta_ij(dl, org, tau, i, j);
-    U[B.rpos[lo + i] + (int64_t)j * K] = u * inv;
+    const int r = B.rpos[lo + i];
+    U[r + (r >= k1 ? pad : 0) + (int64_t)j * ldu] = u * inv;
   }
+  if (pad && lane == 0) U[k1 + (int64_t)j * ldu] = 0.0;
   if (lane == 0) {
     const double lj = B.lam[lo + j];
     int a = 0, b = nd;  // deflated strictly below lambda_j
@@ -606,16 +618,21 @@ __global__ void merge_gemm_args(MergeBufs B, const double* X, int64_t ldx, doubl
     return a;
   };
   const int ja = lower(clo), jb = lower(chi);
+  // U (and the top block of X) carry a zero row (column) after the k1 block when k1 is odd, and
+  // U's leading dimension is even: both GEMMs' B operands start 16-byte aligned with an even
+  // stride, so they take the 16-byte cp.async path (vec_ok) whatever the deflation left
+  const int pad = u_pad(k1);
+  const int64_t ldu = u_ld(K, k1);
   GemmArgs t{};
-  t.m = mid - lo; t.n = jb - ja; t.k = k1 + k2; t.alpha = 1.0; t.beta = 0.0;
+  t.m = mid - lo; t.n = jb - ja; t.k = k1 + pad + k2; t.alpha = 1.0; t.beta = 0.0;
   t.A = X + lo + (int64_t)lo * ldx; t.lda = ldx; t.amap = nullptr;
-  t.B = U + (int64_t)ja * K; t.ldb = K;
+  t.B = U + (int64_t)ja * ldu; t.ldb = ldu;
   t.C = Y + lo + (int64_t)lo * ldy; t.ldc = ldy; t.cmap = cm + ja;
   t.transA = 0; t.transB = 0; t.amode = A_GENERAL; t.cmode = C_ALL;
   GemmArgs bt = t;
   bt.m = hi - mid; bt.k = k2 + k3;
   bt.A = X + mid + (int64_t)lo * ldx; bt.amap = nullptr;
-  bt.B = U + k1 + (int64_t)ja * K;
+  bt.B = U + k1 + pad + (int64_t)ja * ldu;
   bt.C = Y + mid + (int64_t)lo * ldy;
   if (K == 0) { t.m = 0; bt.m = 0; }
   B.gargs[2 * mi] = t;
@@ -635,10 +652,16 @@ __global__ void merge_gather_cols(MergeBufs B, const double* __restrict__ X, int
   const int K = mint[M_K], k1 = mint[M_K1], k2 = mint[M_K2], k3 = mint[M_K3];
   const int c = blockIdx.x;
   if (K == 0) return;
-  if (c < k1 + k2) {
-    const double* src = X + (int64_t)(lo + B.amapT[lo + c]) * ldx;
+  const int pad = u_pad(k1);
+  if (c < k1 + pad + k2) {  // top block, with the zero column at k1 when k1 is odd
     double* dst = Xc + (int64_t)(lo + c) * ldc;
-    for (int r = lo + threadIdx.x; r < mid; r += blockDim.x) dst[r] = src[r];
+    if (pad && c == k1) {
+      for (int r = lo + threadIdx.x; r < mid; r += blockDim.x) dst[r] = 0.0;
+    } else {
+      const int cs = (c < k1) ? c : c - pad;
+      const double* src = X + (int64_t)(lo + B.amapT[lo + cs]) * ldx;
+      for (int r = lo + threadIdx.x; r < mid; r += blockDim.x) dst[r] = src[r];
+    }
   }
   if (c < k2 + k3) {
     const double* src = X + (int64_t)(lo + B.amapB[lo + c]) * ldx;
@@ -770,7 +793,7 @@ int64_t u_elems_for(const Plan& p) {
     int64_t t = 0;
     for (size_t i = 0; i < p.mlo[l].size(); ++i) {
       const int64_t s = p.mhi[l][i] - p.mlo[l][i];
-      t += s * s;
+      t += u_elems(s);
     }
     mx = std::max(mx, t);
   }
@@ -784,7 +807,7 @@ int64_t stedc_ws_bytes(int64_t n) {
   const int64_t nm_total = std::max<int64_t>(1, (int64_t)p.cuts.size());
   WsLayout w;
   w.add(n * n * 8);                 // second ping-pong buffer
-  w.add(n * n * 8);                 // compacted merge-GEMM operands
+  w.add((n * n + n) * 8);           // compacted merge-GEMM operands (+ the pad column)
   w.add(u_elems_for(p) * 8);        // U
   w.add(24 * n * 8);                // per-element arrays
   w.add(nm_total * (M_NINT * 4 + 8 + 2 * (int64_t)sizeof(GemmArgs) + 8) + 4 * n * 4 + 4096);
@@ -809,7 +832,7 @@ int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int
   char* base = (char*)ws;
   WsLayout w;
   double* W2 = (double*)(base + w.add(n * n * 8));
-  double* Xc = (double*)(base + w.add(n * n * 8));
+  double* Xc = (double*)(base + w.add((n * n + n) * 8));
   double* Ubuf = (double*)(base + w.add(u_elems_for(p) * 8));
   double* arr = (double*)(base + w.add(24 * n * 8));
   char* misc = base + w.add(nm_total * (M_NINT * 4 + 8 + 2 * (int64_t)sizeof(GemmArgs) + 8) +
@@ -862,7 +885,7 @@ int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int
     for (size_t i = 0; i < p.mlo[l].size(); ++i) {
       const int64_t s = p.mhi[l][i] - p.mlo[l][i];
       huoff.push_back(o);
-      o += s * s;
+      o += u_elems(s);
     }
   }
   PEVD_CUDA(cudaMemcpyAsync(d_nodes, hnodes.data(), hnodes.size() * 4, cudaMemcpyHostToDevice, st));
@@ -931,7 +954,7 @@ int stedc(cudaStream_t st, int64_t n, double* d, const double* e, double* Q, int
     PEVD_LAUNCH_CHECK();
     // only the last level writes Q: it alone is restricted to the wanted columns
     const int64_t clo = (l == nlev - 1) ? col_lo : 0, chi = (l == nlev - 1) ? col_hi : n;
-    merge_gather_cols<<<dim3((unsigned)smax, nm), 256, 0, st>>>(B, X, ldx, Xc, n);
+    merge_gather_cols<<<dim3((unsigned)smax + 1, nm), 256, 0, st>>>(B, X, ldx, Xc, n);
     PEVD_LAUNCH_CHECK();
     merge_gemm_args<<<(unsigned)cdiv(nm, 128), 128, 0, st>>>(B, Xc, n, Y, ldy, nm, clo, chi);
     PEVD_LAUNCH_CHECK();
