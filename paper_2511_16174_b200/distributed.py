@@ -200,8 +200,8 @@ def _run_device(a, cfg, group, n, gather_q):
             SymmetricMatrix.from_dense(np.asarray(a, dtype=np.float64)).data
         n = dense.shape[0]
     b = min(cfg.b, n - 1)
-    if b > 32:
-        raise ValueError(f"bandwidth b={b} > 32 is not supported by the device kernels")
+    if b > 64:
+        raise ValueError(f"bandwidth b={b} > 64 is not supported by the device kernels")
     cols = partition(n, G)
     backs = back_ranges(n, G, cfg.back_skew)
     c0w, c1w = cols[rank]

@@ -188,8 +188,8 @@ def _run_multi(dense, n: int, b: int, cfg: PipelineConfig, device):
     protocol with one host thread per worker and peer-to-peer transfers.  Workers map
     round-robin onto the visible GPUs; on a box with fewer GPUs than workers several workers
     share one device (the same protocol and messages, without the extra parallelism)."""
-    if b > 32:
-        raise ValueError(f"bandwidth b={b} > 32 is not supported by the device kernels")
+    if b > 64:
+        raise ValueError(f"bandwidth b={b} > 64 is not supported by the device kernels")
     cols = partition(n, cfg.workers)
     backs = back_ranges(n, cfg.workers, cfg.back_skew)
     try:
