@@ -227,3 +227,37 @@ def test_bandwidth_above_64_rejected():
     a = sym(200, 3)
     with pytest.raises(ValueError, match="64"):
         pkg.run(a, pkg.PipelineConfig(workers=1, b=65))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 40])
+@pytest.mark.parametrize("want_vectors", [0, 1])
+def test_host_entry_small_and_values_only(n, want_vectors):
+    """pevd_syevd / pevd_syevd_checked on tiny sizes and without vectors (Q may be NULL), and
+    the checked entry's ValueError on an asymmetric input before any reduction."""
+    import ctypes
+    from paper_2511_16174_b200 import _lib
+    L = _lib.load()
+    a = sym(n, 90 + n)
+    af = np.asfortranarray(a)
+    lam = np.empty(n)
+    q = np.empty((n, n), order="F") if want_vectors else None
+    vp = lambda x: x.ctypes.data_as(ctypes.c_void_p) if x is not None else None  # noqa: E731
+    for checked in (False, True):
+        if checked:
+            rc = L.pevd_syevd_checked(n, 32, vp(af), n, vp(lam), vp(q), n, want_vectors, 2, 1e-13,
+                                      None)
+        else:
+            rc = L.pevd_syevd(n, 32, vp(af), n, vp(lam), vp(q), n, want_vectors, 2, None)
+        _lib.check(rc, "pevd_syevd")
+        lam_np = np.linalg.eigvalsh(a)
+        np.testing.assert_allclose(lam, lam_np, atol=10 * n * EPS * max(1.0, np.abs(lam_np).max()))
+        if want_vectors:
+            assert orc.backward_error(a, q, lam) <= 1e-15
+            assert orc.orthogonality(q) <= 1e-15
+    if n >= 2:
+        bad = af.copy(order="F")
+        bad[n - 1, 0] += 1e-3
+        rc = L.pevd_syevd_checked(n, 32, vp(bad), n, vp(lam), vp(q), n, want_vectors, 2, 1e-13,
+                                  None)
+        assert rc == _lib.PEVD_ERR_VALUE
+        assert "asymmetry" in L.pevd_last_error().decode()
