@@ -37,7 +37,7 @@ constexpr int DONE = 1 << 30;
 
 // one sweep per CTA (two warps)
 struct ChaseSmem {
-  double SLC[2][BMAX * LDS_];  // left block / coupling block, ping-ponged between steps
+  double SLC[3][BMAX * LDS_];  // left block / coupling block, a ring of three (see below)
   double SW[BMAX * LDS_];
   double vs[BMAX];
   double wv[BMAX];
@@ -89,29 +89,67 @@ __global__ void __launch_bounds__(64)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t gend = sweep_end < n - 2 ? sweep_end : n - 2;
   const int64_t stp = LDB - 1;  // pointer step from one band column to the next, same row
+  // step j's window (warp 0) / coupling rows (warp 1), loaded into registers: at the top of the
+  // step, or -- when the predecessor's flag for step j is already up at the end of step j-1's
+  // arithmetic -- before step j-1's write-back and publish, so the loads' L2 round trip hides
+  // under them (the regions are disjoint from step j-1's stores)
+  double rw[BMAX];
+  auto wait_flag = [&](int64_t gi, int need, bool block) -> bool {
+    bool ok = true;
+    if (gi > 0) {
+      if (lane == 0) {
+        ok = ld_relaxed(prog + gi - 1) >= need;
+        if (!ok && block) {
+          const unsigned ns = (unsigned)poll_ns;
+          while (ld_relaxed(prog + gi - 1) < need) {
+            if (ns) __nanosleep(ns);
+          }
+          ok = true;
+        }
+        if (ok) (void)ld_acquire(prog + gi - 1);
+      }
+      ok = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
+    }
+    return ok;
+  };
+  auto load_step = [&](int64_t gi, int64_t j) {
+    const int64_t w0 = gi + 1 + j * b;
+    const int L = (int)((b < n - w0) ? b : n - w0);
+    if (wid == 0) {
+      const double* pw = Bd + w0 * LDB + lane;
+#pragma unroll
+      for (int q = 0; q < BMAX; ++q) {
+        rw[q] = (q < L && lane >= q && lane < L) ? __ldcg(pw) : 0.0;
+        pw += stp;
+      }
+    } else {
+      const int64_t tend = (w0 + L + b < n) ? w0 + L + b : n;
+      const int nT = (int)(tend - (w0 + L));
+      const double* pc = Bd + w0 * LDB + lane + L;
+#pragma unroll
+      for (int q = 0; q < BMAX; ++q) {
+        rw[q] = (q < L && lane < nT) ? __ldcg(pc) : 0.0;
+        pc += stp;
+      }
+    }
+  };
   for (int64_t gi = blockIdx.x; gi < gend; gi += gridDim.x) {
     // The coupling block of step j (rows [w0+L, w0+L+b) x columns [w0, w0+L)) IS the left block
     // of step j+1 of the same sweep, and nobody else touches it in between (the next sweep
     // reaches it only after this one completed step j+2): it stays in shared memory -- the two
     // buffers swap roles -- and is neither stored at step j nor reloaded at step j+1.
-    int cur = 0;  // SLC[cur] = this step's left block, SLC[cur ^ 1] its coupling block
+    // SLC[cur] = this step's left block, SLC[(cur + 1) % 3] its coupling block; the third buffer
+    // keeps the previous step's left block readable while its deferred stores are issued
+    int cur = 0;
+    bool have = false;  // rw already holds this step's region (prefetched by the previous step)
     for (int64_t j = 0; gi + 1 + j * b <= n - 2; ++j) {
       // ---- wait for the predecessor sweep to complete step j+2 (both warps read band data).
       //      Polling is a relaxed L2 load; once the flag is seen one acquire load of it pairs
-      //      with the producer's fence + flag store (release pattern), and __syncwarp extends
-      //      the order to the other lanes, whose band reads then go through L2 (ld.cg).
-      if (gi > 0) {
-        if (lane == 0) {
-          const int need = (int)(j + 3);
-          if (ld_relaxed(prog + gi - 1) < need) {
-            unsigned ns = (unsigned)poll_ns;
-            while (ld_relaxed(prog + gi - 1) < need) {
-              if (ns) __nanosleep(ns);
-            }
-          }
-          (void)ld_acquire(prog + gi - 1);
-        }
-        __syncwarp();
+      //      with the producer's release store, and the shuffle extends the order to the other
+      //      lanes, whose band reads then go through L2 (ld.cg).
+      if (!have) {
+        wait_flag(gi, (int)(j + 3), true);
+        load_step(gi, j);
       }
       const int64_t cg = (j == 0) ? gi : gi + 1 + (j - 1) * b;
       const int64_t w0 = gi + 1 + j * b;
@@ -124,40 +162,36 @@ __global__ void __launch_bounds__(64)
       // the whole matrix's fixed slots)
       const int64_t slot = (int64_t)j * (slot_n - 2) - (int64_t)b * j * (j - 1) / 2 + slot_col0 + gi;
       double* SL = S.SLC[cur];
-      double* SC = S.SLC[cur ^ 1];
-      // ---- stage the region with independent loads (one L2 round trip per warp, not 3b)
+      double* SC = S.SLC[cur == 2 ? 0 : cur + 1];
+      // ---- stage the region into shared memory (the first step's left block loaded here)
       if (wid == 0) {
-        double rl[BMAX], rw[BMAX];
-        const double* pl = Bd + cg * LDB + (w0 - cg) + lane;
-        const double* pw = Bd + w0 * LDB + lane;
+        if (j == 0) {
+          double rl[BMAX];
+          const double* pl = Bd + cg * LDB + (w0 - cg) + lane;
 #pragma unroll
-        for (int q = 0; q < BMAX; ++q) {
-          rl[q] = (j == 0 && q < nleft && lane < L) ? __ldcg(pl) : 0.0;
-          rw[q] = (q < L && lane >= q && lane < L) ? __ldcg(pw) : 0.0;
-          pl += stp;
-          pw += stp;
+          for (int q = 0; q < BMAX; ++q) {
+            rl[q] = (q < nleft && lane < L) ? __ldcg(pl) : 0.0;
+            pl += stp;
+          }
+#pragma unroll
+          for (int q = 0; q < BMAX; ++q) SL[lane * LDS_ + q] = rl[q];
         }
 #pragma unroll
         for (int q = 0; q < BMAX; ++q) {
-          if (j == 0) SL[lane * LDS_ + q] = rl[q];
           if (lane >= q) {
             S.SW[lane * LDS_ + q] = rw[q];
             S.SW[q * LDS_ + lane] = rw[q];
           }
         }
       } else {
-        double rc[BMAX];
-        const double* pc = Bd + w0 * LDB + lane + L;
 #pragma unroll
-        for (int q = 0; q < BMAX; ++q) {
-          rc[q] = (q < L && lane < nT) ? __ldcg(pc) : 0.0;
-          pc += stp;
-        }
-#pragma unroll
-        for (int q = 0; q < BMAX; ++q) SC[lane * LDS_ + q] = rc[q];
+        for (int q = 0; q < BMAX; ++q) SC[lane * LDS_ + q] = rw[q];
       }
-      __syncthreads();  // staged; a step j >= 1 left block (warp 1's last coupling) is visible
-      // ---- the Householder vector (warp 0)
+      // ---- the Householder vector (warp 0).  No CTA barrier before it: warp 0 reads only its own
+      //      staging and (j >= 1) the left block warp 1 wrote before the previous step's last
+      //      barrier, so warp 1's publish of the previous step (its release fence waits for the
+      //      step's stores) runs in parallel with this
+      __syncwarp();
       if (wid == 0) {
         const double x = (lane < L) ? SL[lane * LDS_] : 0.0;
         const double tail = warp_sum((lane >= 1 && lane < L) ? x * x : 0.0);
@@ -183,21 +217,6 @@ __global__ void __launch_bounds__(64)
       if (wid == 0) {
         if (tau != 0.0) {
           const double v = S.vs[lane];
-          // ---- H from the left on the bulge columns strictly between (lane = column q)
-          if (lane >= 1 && lane < nleft) {
-            const int q = lane;
-            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-            for (int r = 0; r < BMAX; r += 4) {
-              d0 = fma(S.vs[r], SL[r * LDS_ + q], d0);
-              d1 = fma(S.vs[r + 1], SL[(r + 1) * LDS_ + q], d1);
-              d2 = fma(S.vs[r + 2], SL[(r + 2) * LDS_ + q], d2);
-              d3 = fma(S.vs[r + 3], SL[(r + 3) * LDS_ + q], d3);
-            }
-            const double dot = tau * ((d0 + d1) + (d2 + d3));
-#pragma unroll
-            for (int r = 0; r < BMAX; ++r) SL[r * LDS_ + q] -= dot * S.vs[r];
-          }
           // ---- H A H on the window (lane = row r)
           double u = 0.0;
           {
@@ -221,27 +240,36 @@ __global__ void __launch_bounds__(64)
           }
           __syncwarp();
         }
-        // ---- write back: the left block (it also carries the previous step's coupling update,
-        //      never stored) and, when a reflector was applied, the window; the reflector slot
-        if (tau != 0.0 || j > 0) {
-          double* pl = Bd + cg * LDB + (w0 - cg) + lane;
-#pragma unroll 4
-          for (int q = 0; q < nleft; ++q, pl += stp)
-            if (lane < L) *pl = SL[lane * LDS_ + q];
-        }
-        if (tau != 0.0) {
-          double* pw = Bd + w0 * LDB + lane;
-#pragma unroll 4
-          for (int c = 0; c < L; ++c, pw += stp)
-            if (lane >= c && lane < L) *pw = S.SW[lane * LDS_ + c];
-        }
-        if (tau_out) {
-          if (lane == 0) tau_out[slot] = tau;
-          for (int r = lane; r < vld; r += 32)
-            V_out[slot * vld + r] = (tau != 0.0) ? ((r < L) ? S.vs[r] : 0.0) : (r == 0 ? 1.0 : 0.0);
-        }
+        // ---- next step's window now if its flag is already up (see rw above)
+        have = !last && wait_flag(gi, (int)(j + 4), false);
+        if (have) load_step(gi, j + 1);
+        // ---- before the publish, only the one element of this step the successor sweep's newly
+        //      unblocked step (j - 2) reads: (row w0, column cg), the corner of that step's
+        //      coupling block.  The rest of the write-back follows the publish, so the release
+        //      fence waits for one store (plus the previous step's, long since landed); the next
+        //      publish covers them before any step that reads them is unblocked.
+        if ((tau != 0.0 || j > 0) && lane == 0) Bd[cg * LDB + (w0 - cg)] = SL[0];
       } else {
-        // ---- H from the right on the coupling rows (lane = row t)
+        // ---- H from the left on the bulge columns strictly between (lane = column q; warp 1
+        //      takes it so the two warps' shares of a step are about equal), then H from the
+        //      right on the coupling rows (lane = row t)
+        if (tau != 0.0) {
+          // ---- H from the left on the bulge columns strictly between (lane = column q)
+          if (lane >= 1 && lane < nleft) {
+            const int q = lane;
+            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+            for (int r = 0; r < BMAX; r += 4) {
+              d0 = fma(S.vs[r], SL[r * LDS_ + q], d0);
+              d1 = fma(S.vs[r + 1], SL[(r + 1) * LDS_ + q], d1);
+              d2 = fma(S.vs[r + 2], SL[(r + 2) * LDS_ + q], d2);
+              d3 = fma(S.vs[r + 3], SL[(r + 3) * LDS_ + q], d3);
+            }
+            const double dot = tau * ((d0 + d1) + (d2 + d3));
+#pragma unroll
+            for (int r = 0; r < BMAX; ++r) SL[r * LDS_ + q] -= dot * S.vs[r];
+          }
+        }
         if (tau != 0.0) {
           double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll
@@ -255,25 +283,47 @@ __global__ void __launch_bounds__(64)
 #pragma unroll
           for (int c = 0; c < BMAX; ++c) SC[lane * LDS_ + c] -= dot * S.vs[c];
         }
-        // the last step's coupling block has no next step to carry it: store it
-        if (last) {
-          double* pc = Bd + w0 * LDB + lane + L;
-          for (int c = 0; c < L; ++c, pc += stp)
-            if (lane < nT) *pc = SC[lane * LDS_ + c];
-        }
+        // ---- next step's coupling rows now if its flag is already up
+        have = !last && wait_flag(gi, (int)(j + 4), false);
+        if (have) load_step(gi, j + 1);
       }
-      // ---- publish progress once both warps' stores are issued (the barrier orders warp 1's
-      //      stores before thread 0's gpu-scope fence, whose release covers them cumulatively)
+      // ---- publish progress (the barrier orders warp 0's store before warp 1's release, which
+      //      covers it cumulatively); warp 1 publishes, so the fence's wait overlaps warp 0's
+      //      deferred stores and next Householder vector
       __syncthreads();
-      if (threadIdx.x == 0) {
-        st_release(prog + gi, (int)(j + 1));
+      if (threadIdx.x == 32) st_release(prog + gi, (int)(j + 1));
+      // ---- deferred write-back: the left block (it also carries the previous step's coupling
+      //      update, never stored), the window when a reflector was applied, the reflector slot;
+      //      the last step's coupling block (no next step carries it)
+      if (wid == 0) {
+        if (tau != 0.0 || j > 0) {
+          // (not the corner stored above: the successor may already be updating it)
+          double* pl = Bd + cg * LDB + (w0 - cg) + lane;
+#pragma unroll 4
+          for (int q = 0; q < nleft; ++q, pl += stp)
+            if (lane < L && (lane | q) != 0) *pl = SL[lane * LDS_ + q];
+        }
+        if (tau != 0.0) {
+          double* pw = Bd + w0 * LDB + lane;
+#pragma unroll 4
+          for (int c = 0; c < L; ++c, pw += stp)
+            if (lane >= c && lane < L) *pw = S.SW[lane * LDS_ + c];
+        }
+        if (tau_out) {
+          if (lane == 0) tau_out[slot] = tau;
+          for (int r = lane; r < vld; r += 32)
+            V_out[slot * vld + r] = (tau != 0.0) ? ((r < L) ? S.vs[r] : 0.0) : (r == 0 ? 1.0 : 0.0);
+        }
+        __syncwarp();  // these shared-memory reads precede the next step's staging (WAR)
+      } else if (last) {
+        double* pc = Bd + w0 * LDB + lane + L;
+        for (int c = 0; c < L; ++c, pc += stp)
+          if (lane < nT) *pc = SC[lane * LDS_ + c];
       }
-      cur ^= 1;  // this step's coupling block is the next step's left block
+      cur = (cur == 2) ? 0 : cur + 1;  // this step's coupling block is the next step's left block
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      st_release(prog + gi, DONE);
-    }
+    if (threadIdx.x == 32) st_release(prog + gi, DONE);
   }
 }
 
@@ -538,7 +588,9 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
     const int64_t want_warps =
         std::min<int64_t>(n - 2, std::max<int64_t>(110 * n / (300 * b), 2 * num_sms()));
     const int64_t need = want_warps;  // one sweep (two warps) per CTA
-    const int grid = (int)std::min<int64_t>((int64_t)per_sm * num_sms(), need);
+    int grid = (int)std::min<int64_t>((int64_t)per_sm * num_sms(), need);
+    if (const char* e = getenv("PEVD_CHASE_GRID"))  // probes: fewer CTAs (1 = sweeps in order)
+      grid = std::max(1, std::min(grid, atoi(e)));
     int64_t n_ = n, sweep_end_ = sweep_end, LDB_ = LDB;
     int b_ = b, vld_ = vld;
     int poll_ns = poll;
