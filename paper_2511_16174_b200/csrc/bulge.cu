@@ -203,9 +203,10 @@ __global__ void __launch_bounds__(64)
           const double alpha = (x0 >= 0.0) ? -nrm : nrm;
           const double denom = x0 - alpha;
           const double v = (lane == 0) ? 1.0 : ((lane < L) ? x / denom : 0.0);
-          const double vsq = 1.0 + warp_sum((lane >= 1) ? v * v : 0.0);
           S.vs[lane] = v;
-          if (lane == 0) S.tau = 2.0 / vsq;
+          // v^T v = 1 + tail / denom^2 in closed form (as the panel QR does): no second warp
+          // reduction on the step-to-step path
+          if (lane == 0) S.tau = 2.0 / (1.0 + tail / (denom * denom));
           if (lane < L) SL[lane * LDS_] = (lane == 0) ? alpha : 0.0;
         }
       }
