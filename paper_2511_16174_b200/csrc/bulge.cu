@@ -585,7 +585,8 @@ int bc_reduce_range(cudaStream_t st, int64_t n, int b, int bw, const double* ban
     // about n/(3b) sweeps are in flight at once; 10% more CTAs keeps a CTA ready when a sweep's
     // turn comes, more only adds spinning CTAs; waiting CTAs poll with a 64 ns back-off (at
     // n = 49152: 1.068 s with twice the in-flight count and tight polling, 1.037 s like this)
-    const int poll = 64;
+    int poll = 64;
+    if (const char* e = getenv("PEVD_CHASE_POLL_NS")) poll = std::max(0, atoi(e));  // probes
     const int64_t want_warps =
         std::min<int64_t>(n - 2, std::max<int64_t>(110 * n / (300 * b), 2 * num_sms()));
     const int64_t need = want_warps;  // one sweep (two warps) per CTA
