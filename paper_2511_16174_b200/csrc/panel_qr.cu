@@ -29,21 +29,25 @@ struct QrWork {
 };
 constexpr int MAXCTA = 1024;
 
+// Grid barrier as a release/acquire chain (no sequentially consistent fences): each CTA's
+// writes before it are ordered by the CTA barrier, released by thread 0's acq_rel arrival; the
+// last arriver resets the count and releases the new generation, which the others acquire.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned gen = *vgen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicExch(bar + 1, gen + 1);
+    unsigned gen, prev;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(gen) : "l"(bar + 1) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;\n"
+                 : "=r"(prev) : "l"(bar) : "memory");
+    if (prev == nblocks - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;\n" ::"l"(bar) : "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(bar + 1), "r"(gen + 1)
+                   : "memory");
     } else {
-      while (*vgen == gen) {
-      }
+      unsigned g = gen;
+      while (g == gen)
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(g) : "l"(bar + 1) : "memory");
     }
-    __threadfence();
   }
   __syncthreads();
 }
