@@ -115,14 +115,17 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
                       int64_t workspace_bytes, void* stream, pevd_stats* stats);
 
 /* As pevd_syevd_device, but Q (a DEVICE buffer it computes in) is also delivered to the HOST
- * buffer Qh (column-major, ldqh >= n): in conventional order the last back-transformation runs
- * in column slabs and each slab's copy overlaps the next slab's compute, so only the last
- * slab's copy is exposed.  Pinned Qh is copied by the copy engines; pageable Qh through pinned
+ * buffer Qh (ldqh >= n): in conventional order the last back-transformation runs in column
+ * slabs and each slab's copy overlaps the next slab's compute, so only the last slab's copy is
+ * exposed.  q_row_major = 0: Qh column-major.  q_row_major = 1 (pipelined / sequential orders
+ * only, PEVD_ERR_VALUE otherwise): Qh receives Q row-major -- the C-ordered Q of pipeline.py:503
+ * -- from a final GEMM that forms Q^T in slabs, streamed the same way (the device buffer Q then
+ * holds Q^T).  Pinned Qh is copied by the copy engines; pageable Qh through pinned
  * staging chunks worked by several host threads (PEVD_STAGE_THREADS, default 8). */
 int pevd_syevd_device_host_q(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
-                             int64_t ldq, double* Qh, int64_t ldqh, int want_vectors, int order,
-                             void* workspace, int64_t workspace_bytes, void* stream,
-                             pevd_stats* stats);
+                             int64_t ldq, double* Qh, int64_t ldqh, int q_row_major,
+                             int want_vectors, int order, void* workspace,
+                             int64_t workspace_bytes, void* stream, pevd_stats* stats);
 
 /* HOST pointers (A column-major, lda; only its lower triangle is read and copied to the
  * device); allocates device memory itself.  Q comes back as pevd_syevd_device_host_q delivers
@@ -132,9 +135,11 @@ int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, doub
 
 /* pevd_syevd with the input check of SymmetricMatrix (core.py:75-84, pipeline.py:517-518)
  * folded in: all of A goes up and max |A_ij - A_ji| > sym_tol * max(1, ||A||_F) returns
- * PEVD_ERR_VALUE ("asymmetry ... exceeds tolerance") before any reduction runs. */
+ * PEVD_ERR_VALUE ("asymmetry ... exceeds tolerance") before any reduction runs; sym_tol < 0
+ * skips the check (and uploads only the lower triangle).  q_row_major as in
+ * pevd_syevd_device_host_q. */
 int pevd_syevd_checked(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q,
-                       int64_t ldq, int want_vectors, int order, double sym_tol,
+                       int64_t ldq, int want_vectors, int order, double sym_tol, int q_row_major,
                        pevd_stats* stats);
 
 /* The input check of SymmetricMatrix (core.py:75-84) on the device: out2[0] = max |A_ij - A_ji|,

@@ -74,11 +74,11 @@ SIGNATURES = {
     "pevd_syevd_device": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _int, _int, _vp, _i64,
                                  _vp, ctypes.POINTER(PevdStats)]),
     "pevd_syevd_device_host_q": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _int,
-                                        _int, _vp, _i64, _vp, ctypes.POINTER(PevdStats)]),
+                                        _int, _int, _vp, _i64, _vp, ctypes.POINTER(PevdStats)]),
     "pevd_syevd": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _int, _int,
                           ctypes.POINTER(PevdStats)]),
     "pevd_syevd_checked": (_int, [_i64, _int, _vp, _i64, _vp, _vp, _i64, _int, _int, _dbl,
-                                  ctypes.POINTER(PevdStats)]),
+                                  _int, ctypes.POINTER(PevdStats)]),
     "pevd_dgemm": (_int, [_int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp,
                           _i64, _vp, _i64, _vp]),
     "pevd_dsymm_lower": (_int, [_i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp, _i64,

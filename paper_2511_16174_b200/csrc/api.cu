@@ -432,11 +432,26 @@ int syevd_impl(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
         if (two_streams) cudaStreamWaitEvent(sm, ev[4].b, 0);
         flops_set_stage(ST_FINAL);
         cudaEventRecord(ev[5].a, sm);
-        GemmArgs g{n, n, n, 1.0, 0.0, L.Qs, n, L.Qd, n, Q, ldq, 0, 0, A_GENERAL, C_ALL};
-        if ((rc = gemm(sm, g, nullptr, 0))) break;
+        if (hq && hq->row_major) {
+          // Q^T = Q_d^T (Q_s Q_b)^T in column slabs (rows of Q), each slab's copy to the host
+          // overlapping the next slab's GEMM
+          const std::vector<int64_t> sl = q_slab_bounds(n);
+          for (size_t s = 0; s + 1 < sl.size() && rc == OK; ++s) {
+            const int64_t c0 = sl[s], nc = sl[s + 1] - sl[s];
+            GemmArgs g{n, nc, n, 1.0, 0.0, L.Qd, n, L.Qs + c0, n, Q + c0 * ldq, ldq, 1, 1,
+                       A_GENERAL, C_ALL};
+            rc = gemm(sm, g, nullptr, 0);
+            if (rc == OK && hq->slab_ready(sm, Q, ldq, n, c0, nc)) rc = ERR_CUDA;
+          }
+          if (rc) break;
+        } else {
+          GemmArgs g{n, n, n, 1.0, 0.0, L.Qs, n, L.Qd, n, Q, ldq, 0, 0, A_GENERAL, C_ALL};
+          if ((rc = gemm(sm, g, nullptr, 0))) break;
+        }
         cudaEventRecord(ev[5].b, sm);
       }
-      if (hq && !conv_t && hq->slab_ready(sm, Q, ldq, n, 0, n)) {
+      if (hq && !conv_t && !(hq->row_major && order != PEVD_ORDER_CONVENTIONAL) &&
+          hq->slab_ready(sm, Q, ldq, n, 0, n)) {
         rc = ERR_CUDA;
         break;
       }
@@ -494,9 +509,9 @@ int pevd_syevd_device(int64_t n, int b, double* A, int64_t lda, double* lam, dou
 }
 
 int pevd_syevd_device_host_q(int64_t n, int b, double* A, int64_t lda, double* lam, double* Q,
-                             int64_t ldq, double* Qh, int64_t ldqh, int want_vectors, int order,
-                             void* workspace, int64_t workspace_bytes, void* stream,
-                             pevd_stats* stats) {
+                             int64_t ldq, double* Qh, int64_t ldqh, int q_row_major,
+                             int want_vectors, int order, void* workspace,
+                             int64_t workspace_bytes, void* stream, pevd_stats* stats) {
   if (want_vectors && (!Qh || ldqh < n)) {
     set_error("pevd_syevd_device_host_q: bad host Q (ldqh=%lld, n=%lld)", (long long)ldqh,
               (long long)n);
@@ -511,6 +526,12 @@ int pevd_syevd_device_host_q(int64_t n, int b, double* A, int64_t lda, double* l
   hq.Qh = Qh;
   hq.ldqh = ldqh;
   hq.pinned = host_is_pinned(Qh);
+  hq.row_major = q_row_major != 0 && order != PEVD_ORDER_CONVENTIONAL;
+  if (q_row_major && order == PEVD_ORDER_CONVENTIONAL) {
+    set_error("pevd_syevd_device_host_q: row-major Q is produced by the pipelined and "
+              "sequential orders only (conventional order returns it column-major)");
+    return ERR_VALUE;
+  }
   std::unique_ptr<Stager> stager;
   if (hq.pinned) {
     PEVD_CUDA(cudaStreamCreateWithFlags(&hq.cs, cudaStreamNonBlocking));
@@ -570,7 +591,8 @@ namespace {
 // device never reads the strictly upper triangle); otherwise all of A goes up and the
 // SymmetricMatrix test (core.py:75-84) runs on the device first.
 int host_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q,
-               int64_t ldq, int want_vectors, int order, double sym_tol, pevd_stats* stats) {
+               int64_t ldq, int want_vectors, int order, double sym_tol, int q_row_major,
+               pevd_stats* stats) {
   if (n < 1 || lda < n || !A || !lam || (want_vectors && (!Q || ldq < n))) {
     set_error("pevd_syevd: bad arguments");
     return ERR_VALUE;
@@ -642,8 +664,8 @@ int host_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, doub
   }
   phase("upload");
   if (rc == OK)
-    rc = want_vectors ? pevd_syevd_device_host_q(n, b, dA, n, dlam, dQ, n, Q, ldq, 1, order, ws,
-                                                 wsb, st, stats)
+    rc = want_vectors ? pevd_syevd_device_host_q(n, b, dA, n, dlam, dQ, n, Q, ldq, q_row_major,
+                                                 1, order, ws, wsb, st, stats)
                       : pevd_syevd_device(n, b, dA, n, dlam, nullptr, n, 0, order, ws, wsb, st,
                                           stats);
   phase("evd");
@@ -666,17 +688,22 @@ extern "C" {
 
 int pevd_syevd(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q, int64_t ldq,
                int want_vectors, int order, pevd_stats* stats) {
-  return host_syevd(n, b, A, lda, lam, Q, ldq, want_vectors, order, -1.0, stats);
+  return host_syevd(n, b, A, lda, lam, Q, ldq, want_vectors, order, -1.0, 0, stats);
 }
 
 int pevd_syevd_checked(int64_t n, int b, const double* A, int64_t lda, double* lam, double* Q,
-                       int64_t ldq, int want_vectors, int order, double sym_tol,
+                       int64_t ldq, int want_vectors, int order, double sym_tol, int q_row_major,
                        pevd_stats* stats) {
-  if (!(sym_tol >= 0.0)) {
-    set_error("pevd_syevd_checked: sym_tol must be >= 0");
+  if (sym_tol != sym_tol) {
+    set_error("pevd_syevd_checked: sym_tol is NaN");
     return ERR_VALUE;
   }
-  return host_syevd(n, b, A, lda, lam, Q, ldq, want_vectors, order, sym_tol, stats);
+  if (q_row_major && order == PEVD_ORDER_CONVENTIONAL) {
+    set_error("pevd_syevd_checked: row-major Q is produced by the pipelined and sequential "
+              "orders only (conventional order returns it column-major)");
+    return ERR_VALUE;
+  }
+  return host_syevd(n, b, A, lda, lam, Q, ldq, want_vectors, order, sym_tol, q_row_major, stats);
 }
 
 int pevd_dgemm(int transA, int transB, int64_t m, int64_t n, int64_t k, double alpha,

@@ -63,6 +63,9 @@ struct HostQ {
   double* Qh = nullptr;
   int64_t ldqh = 0;
   bool pinned = false;
+  // pipelined / sequential orders: Qh receives Q ROW-major (Q^T column-major, the C-ordered Q of
+  // pipeline.py:503); the final GEMM then forms Q^T slab by slab in the device buffer
+  bool row_major = false;
   cudaStream_t cs = nullptr;      // copy stream (pinned destination)
   Stager* stager = nullptr;       // staging threads (pageable destination)
   std::vector<cudaEvent_t> evs;   // one per slab, destroyed by finish()

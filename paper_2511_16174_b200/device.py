@@ -337,8 +337,8 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=F
     check_sym: the SymmetricMatrix test (core.py:75-84) runs on the device (pevd_asymmetry)
     instead of over the host copy.  Q comes back Fortran-ordered in conventional order and
     C-ordered otherwise (pipeline.py:495, 503) -- the device transposes, not the host.
-    Conventional order is one native call (pevd_syevd / pevd_syevd_checked): the library moves
-    the host buffers itself and overlaps Q's download with the last SBR-Back blocks."""
+    With vectors this is one native call (pevd_syevd_checked): the library moves the host
+    buffers itself and overlaps Q's download with the last GEMMs."""
     L = _lib.load()
     torch = _torch()
     a = np.asarray(a, dtype=np.float64)
@@ -347,22 +347,23 @@ def syevd(a, b=32, want_vectors=True, order="pipelined", stats=None, check_sym=F
     bb = max(1, min(b, n - 1)) if n > 1 else 1
     mem = a.T if a.flags.f_contiguous else np.ascontiguousarray(a)
     st = _lib.PevdStats() if stats is None else stats
-    if want_vectors and order == "conventional":
+    if want_vectors:
         # one native call: the upload (lower trapezoid, or all of A for the device symmetry
-        # check) and Q's download slab by slab under the last SBR-Back blocks go through the
-        # library's own staging threads; Q lands Fortran-ordered, as the reference returns it
+        # check) and Q's download slab by slab under the last GEMMs (SBR-Back in conventional
+        # order, the final multiply otherwise) go through the library's own staging threads.
+        # Q lands as the reference returns it: Fortran-ordered in conventional order, C-ordered
+        # otherwise (pipeline.py:495, 503; the final GEMM then forms Q^T slab by slab)
         lam_h = np.empty(n)
-        qf = np.empty((n, n), dtype=np.float64, order="F")
+        conv = order == "conventional"
+        qh = np.empty((n, n), dtype=np.float64, order="F" if conv else "C")
         vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
-        if check_sym:
-            rc = L.pevd_syevd_checked(n, bb, vp(mem), n, vp(lam_h), vp(qf), n, 1, oc, sym_tol,
-                                      ctypes.byref(st))
-        else:
-            rc = L.pevd_syevd(n, bb, vp(mem), n, vp(lam_h), vp(qf), n, 1, oc, ctypes.byref(st))
+        rc = L.pevd_syevd_checked(n, bb, vp(mem), n, vp(lam_h), vp(qh), n, 1, oc,
+                                  sym_tol if check_sym else -1.0, 0 if conv else 1,
+                                  ctypes.byref(st))
         if rc == _lib.PEVD_ERR_CONVERGE:
             raise RuntimeError(L.pevd_last_error().decode())
         _lib.check(rc, "syevd")
-        return lam_h, qf, st
+        return lam_h, qh, st
     da = _to_device(mem)                  # (n, n): column-major A (or A^T)
     if check_sym:
         out = (ctypes.c_double * 2)()

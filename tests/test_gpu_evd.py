@@ -245,7 +245,7 @@ def test_host_entry_small_and_values_only(n, want_vectors):
     for checked in (False, True):
         if checked:
             rc = L.pevd_syevd_checked(n, 32, vp(af), n, vp(lam), vp(q), n, want_vectors, 2, 1e-13,
-                                      None)
+                                      0, None)
         else:
             rc = L.pevd_syevd(n, 32, vp(af), n, vp(lam), vp(q), n, want_vectors, 2, None)
         _lib.check(rc, "pevd_syevd")
@@ -258,6 +258,36 @@ def test_host_entry_small_and_values_only(n, want_vectors):
         bad = af.copy(order="F")
         bad[n - 1, 0] += 1e-3
         rc = L.pevd_syevd_checked(n, 32, vp(bad), n, vp(lam), vp(q), n, want_vectors, 2, 1e-13,
-                                  None)
+                                  0, None)
         assert rc == _lib.PEVD_ERR_VALUE
         assert "asymmetry" in L.pevd_last_error().decode()
+
+
+@pytest.mark.parametrize("n,order,pinned", [(600, "pipelined", False), (4500, "pipelined", True),
+                                            (4500, "sequential", False)])
+def test_host_entry_row_major_q(n, order, pinned):
+    """pipelined / sequential orders with q_row_major = 1: the final GEMM forms Q^T in column
+    slabs streamed to the host, so the host buffer holds Q C-ordered (pipeline.py:503); the same
+    eigenpairs as the device entry point, and conventional order refuses row-major output."""
+    import ctypes
+    import torch
+    from paper_2511_16174_b200 import _lib
+    L = _lib.load()
+    a = sym(n, 7 * n)
+    af = np.asfortranarray(a)
+    lam = np.empty(n)
+    if pinned:
+        qt = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        q = qt.numpy()
+    else:
+        q = np.empty((n, n))                                   # C order
+    vp = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    oc = _lib.ORDER_CODES[order]
+    _lib.check(L.pevd_syevd_checked(n, 32, vp(af), n, vp(lam), vp(q), n, 1, oc, -1.0, 1, None),
+               "pevd_syevd_checked")
+    l_dev, q_dev = _device_run(a, 32, order)
+    np.testing.assert_allclose(lam, l_dev, atol=1e-13 * np.abs(l_dev).max())
+    np.testing.assert_allclose(q, q_dev, atol=1e-11)        # q (C order) is Q itself
+    assert orc.backward_error(a, q, lam) <= (1e-15 if n <= 1024 else 1e-12)
+    rc = L.pevd_syevd_checked(n, 32, vp(af), n, vp(lam), vp(q), n, 1, 2, -1.0, 1, None)
+    assert rc == _lib.PEVD_ERR_VALUE
