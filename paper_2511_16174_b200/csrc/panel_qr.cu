@@ -166,15 +166,16 @@ __global__ void __launch_bounds__(QR_THREADS)
     __syncthreads();
     // ---- T column j-1: T[0:jp, jp] = -tau_jp * T[0:jp, 0:jp] * g[0:jp]  (row q per thread;
     //      column jp only reads columns < jp, so all rows are independent)
-    if (j >= 1 && tid < j) {
-      const int jp = j - 1, q = tid;
+    //      one warp per row, warps 1.. only: warp 0's thread 0 computes the next reflector's
+    //      scalars meanwhile (a serial row loop on thread 0 was ~0.5 us of every column step)
+    if (j >= 1 && tid >= 32) {
+      const int jp = j - 1, lane = tid & 31;
       const double tj = taus[jp];
-      if (q == jp) {
-        T[jp + jp * KM] = tj;
-      } else {
+      for (int q = (tid >> 5) - 1; q <= jp; q += QR_THREADS / 32 - 1) {
         double s = 0.0;
-        for (int t = q; t < jp; ++t) s += T[q + t * KM] * hv[KM + t];
-        T[q + jp * KM] = -tj * s;
+        for (int t = q + lane; t < jp; t += 32) s += T[q + t * KM] * hv[KM + t];
+        s = warp_sum(s);
+        if (lane == 0) T[q + jp * KM] = (q == jp) ? tj : -tj * s;
       }
     }
     if (j == k) break;

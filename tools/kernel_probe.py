@@ -101,14 +101,16 @@ def main():
         out.update(m=m, n=n, k=k, ms=ms, tflops=2.0 * m * n * k / ms / 1e9)
     elif mode == "symm":
         m, n = int(sys.argv[2]), int(sys.argv[3])
-        A = torch.randn(m * m, dtype=torch.float64, device="cuda")
-        B = torch.randn(m * n, dtype=torch.float64, device="cuda")
-        C = torch.zeros(m * n, dtype=torch.float64, device="cuda")
-        ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
-        ms, ts = timed(lambda: _lib.check(L.pevd_dsymm_lower(m, n, 1.0, ptr(A), m, ptr(B), m, 0.0,
-                                                             ptr(C), m, ptr(ws), ws.numel(),
-                                                             stream()), "symm"), reps=5)
-        out.update(m=m, n=n, ms=ms, tflops=2.0 * m * m * n / ms / 1e9,
+        lda = int(sys.argv[4]) if len(sys.argv) > 4 else m  # the SBR passes lda = n_total
+        A = torch.randn(lda * m, dtype=torch.float64, device="cuda")
+        B = torch.randn(lda * n, dtype=torch.float64, device="cuda")
+        C = torch.zeros(lda * n, dtype=torch.float64, device="cuda")
+        ws = torch.empty(int(os.environ.get("PROBE_WS_MB", "32")) << 20, dtype=torch.uint8, device="cuda")
+        ms, ts = timed(lambda: _lib.check(L.pevd_dsymm_lower(m, n, 1.0, ptr(A), lda, ptr(B), lda,
+                                                             0.0, ptr(C), lda, ptr(ws),
+                                                             ws.numel(), stream()), "symm"),
+                       reps=5)
+        out.update(m=m, n=n, lda=lda, ms=ms, tflops=2.0 * m * m * n / ms / 1e9,
                    gbs=8.0 * m * m / ms / 1e6)
     elif mode == "sbr":
         n = int(sys.argv[2])
