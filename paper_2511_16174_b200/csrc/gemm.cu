@@ -222,8 +222,16 @@ __global__ void splitk_reduce(const double* __restrict__ ws, int ksplit, int64_t
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % m, j = idx / m;
-    double s = 0.0;
-    for (int z = 0; z < ksplit; ++z) s += ws[z * total + idx];  // fixed order: deterministic
+    // eight interleaved partial sums (loads in flight for deep splits), combined in a fixed
+    // order: deterministic
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    int z = 0;
+    for (; z + 8 <= ksplit; z += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += ws[(int64_t)(z + u) * total + idx];
+    }
+    for (int u = 0; z < ksplit; ++z, ++u) a[u] += ws[(int64_t)z * total + idx];
+    const double s = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     double* cp = C + i + (cmap ? (int64_t)cmap[j] : j) * ldc;
     const double v = alpha * s;
     *cp = (beta == 0.0) ? v : v + beta * *cp;
@@ -735,6 +743,14 @@ int splitk_finish(cudaStream_t st, const GemmArgs& g, int ks, double* ws) {
 static int pick_ks(int64_t tiles, int64_t k, int64_t slots, int64_t min_chunk, int64_t mn,
                    int64_t ws_elems) {
   if (tiles >= 8 * slots || k < 2 * min_chunk) return 1;
+  if (tiles * (k / min_chunk) < slots / 2) {
+    // a tiny output with a long K (W^T AW of the band reduction: 32 x 32, K = m): even the
+    // deepest split below leaves most SMs idle and each CTA latency-bound on a long K loop, so
+    // split to 128-deep chunks across the whole GPU (one reduction pass sums them in order)
+    int64_t ks = std::min<int64_t>(k / 128, slots / tiles);
+    while (ks > 1 && ks * mn > ws_elems) --ks;
+    return (int)std::max<int64_t>(ks, 1);
+  }
   const int64_t kmax = std::min<int64_t>(k / min_chunk, 32);
   int best = 1;
   double best_eff = 0.0;
@@ -806,7 +822,12 @@ int gemm(cudaStream_t st, const GemmArgs& g0, double* ws, int64_t ws_elems) {
   if (g.n <= 32) {
     // skinny: 128 x 32 tiles, split K when the grid is thin
     const int64_t tiles = cdiv(g.m, 128);
-    const int ks = (ws && g.cmode == C_ALL) ? pick_ks(tiles, g.k, 2 * sms, 512, g.m * g.n, ws_elems)
+    static int chunk = -1;  // PEVD_SKINNY_CHUNK: smallest split-K chunk (tuning knob)
+    if (chunk < 0) {
+      const char* e = getenv("PEVD_SKINNY_CHUNK");
+      chunk = e ? std::max(64, atoi(e)) : 512;
+    }
+    const int ks = (ws && g.cmode == C_ALL) ? pick_ks(tiles, g.k, 2 * sms, chunk, g.m * g.n, ws_elems)
                                             : 1;
     // 8 warps of 16 x 32, BK = 16, 3 stages (<= 92 KB: 2 CTAs/SM); 31 TF/s at 49152 x 32 x 49152
     PEVD_TRY((launch_fast_t<128, 32, 16, 16, 32, 3>(st, g, ks, ks > 1 ? ws : nullptr)));
