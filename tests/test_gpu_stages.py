@@ -28,7 +28,10 @@ def sym(n, seed):
 @pytest.mark.parametrize("m,n,k,ta,tb", [(1, 1, 1, 0, 0), (37, 29, 53, 0, 0), (130, 70, 300, 1, 0),
                                          (64, 200, 17, 0, 1), (257, 33, 1000, 1, 1),
                                          (300, 32, 5000, 1, 0), (32, 32, 20000, 1, 0),
-                                         (1000, 900, 64, 0, 1)])
+                                         (1000, 900, 64, 0, 1),
+                                         # deep split-K of tiny outputs (W^T AW) and t = P2^T W
+                                         (29, 31, 30001, 1, 0), (32, 32, 49152, 1, 0),
+                                         (960, 32, 49152, 1, 0)])
 def test_dgemm_matches_numpy(m, n, k, ta, tb):
     rng = np.random.default_rng(m * 7 + n)
     a = rng.standard_normal((k, m) if ta else (m, k))
@@ -40,6 +43,7 @@ def test_dgemm_matches_numpy(m, n, k, ta, tb):
 
 
 @pytest.mark.parametrize("m,k", [(8, 8), (40, 8), (300, 32), (1000, 32), (5000, 17), (20000, 32),
+                                 (4097, 31), (49152, 32),  # one-pass kernel, ragged / full grid
                                  (100, 33), (700, 48), (3000, 64), (40000, 64)])
 def test_panel_qr_matches_oracle(m, k):
     p = np.random.default_rng(m + k).standard_normal((m, k))
