@@ -307,8 +307,29 @@ __global__ void __launch_bounds__(QR_THREADS, 1)
     double acc = 0.0;
     // four rows per iteration (independent chains: the shuffles and the division of one row no
     // longer serialise the next)
+    // rows below the pivot (all but a few rows of CTA 0): branch-free.  cf is 0 on the lanes
+    // < jp, so those keep a; lane jp takes v; the partial's multiplier is v (T column, lanes
+    // < jp), x_j (tail dots, lanes >= j) or 0 (lane jp)
+    const bool tdot = lane < jp, hdot = lane >= j && j < k;
+    auto row_fast = [&](int lr, double& ac) {
+      double a = P[lr * LDP + lane];
+      if (jp >= 0) {
+        const double vj = active ? __shfl_sync(0xffffffffu, a, jp) * rdenom : 0.0;
+        a = (lane == jp) ? vj : fma(-cf, vj, a);
+        P[lr * LDP + lane] = a;
+        if (tdot) ac = fma(a, vj, ac);
+      }
+      if (j < k) {
+        const double xj = __shfl_sync(0xffffffffu, a, j);
+        if (hdot) ac = fma(xj, a, ac);
+      }
+    };
     auto row_pass = [&](int lr, double& ac) {
       const int64_t r = r0 + lr;
+      if (r > j) {
+        row_fast(lr, ac);
+        return;
+      }
       double a = P[lr * LDP + lane];
       if (jp >= 0 && r >= jp) {
         double vj = 1.0;

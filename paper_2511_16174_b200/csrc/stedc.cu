@@ -352,7 +352,6 @@ __global__ void merge_deflate(MergeBufs B) {
     dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
   }
-  if (lane != 0) return;
   const double rho = B.rho[mi];
   const double tol = 8.0 * DEPS * fmax(dmax, zmax);  // LAPACK dlaed2
   int K = 0, nd = 0, nrot = 0;
@@ -361,41 +360,67 @@ __global__ void merge_deflate(MergeBufs B) {
   int* colid = B.colid + lo;
   int* ctype = B.ctype + lo;
   if (rho * zmax <= tol) {
+    if (lane != 0) return;
     for (int p = 0; p < s; ++p) { B.dv[lo + nd] = Ds[p]; B.dcol[lo + nd] = colid[p]; ++nd; }
   } else {
+    // The scan is sequential (a Givens deflation changes the pole it chains to), so lane 0 runs
+    // it; the whole warp stages the next 32 entries in shared memory first, and the current
+    // pole pj lives in registers, so no iteration waits on an L2 round trip.
+    __shared__ double sD[32], sZ[32];
+    __shared__ int sC[32], sT[32];
     int pj = -1;
-    for (int p = 0; p < s; ++p) {
-      if (rho * fabs(zs[p]) <= tol) {
-        B.dv[lo + nd] = Ds[p]; B.dcol[lo + nd] = colid[p]; ++nd;
-        continue;
+    double dpj = 0.0, zpj = 0.0;
+    int cpj = 0, tpj = 0;
+    for (int base = 0; base < s; base += 32) {
+      __syncwarp();
+      if (base + lane < s) {
+        sD[lane] = Ds[base + lane];
+        sZ[lane] = zs[base + lane];
+        sC[lane] = colid[base + lane];
+        sT[lane] = ctype[base + lane];
       }
-      if (pj < 0) { pj = p; continue; }
-      double S = zs[pj], C = zs[p];
-      const double tau = hypot(C, S);
-      const double t = Ds[p] - Ds[pj];
-      C /= tau;
-      S = -S / tau;
-      if (fabs(t * C * S) <= tol) {
-        zs[p] = tau;
-        zs[pj] = 0.0;
-        B.rp[lo + nrot] = colid[pj]; B.rq[lo + nrot] = colid[p];
-        B.rc[lo + nrot] = C; B.rs[lo + nrot] = S; ++nrot;
-        if (ctype[p] != ctype[pj]) ctype[p] = 2;
-        const double dpj = Ds[pj], dp = Ds[p];
-        const double tmp = dpj * C * C + dp * S * S;
-        Ds[p] = dpj * S * S + dp * C * C;
-        Ds[pj] = tmp;
-        B.dv[lo + nd] = tmp; B.dcol[lo + nd] = colid[pj]; ++nd;
-        pj = p;
-      } else {
-        B.dl[lo + K] = Ds[pj]; B.zl[lo + K] = zs[pj];
-        B.ncol[lo + K] = colid[pj]; B.ntype[lo + K] = ctype[pj]; ++K;
-        pj = p;
+      __syncwarp();
+      if (lane == 0) {
+        const int cnt = s - base < 32 ? s - base : 32;
+        for (int q = 0; q < cnt; ++q) {
+          const int p = base + q;
+          double dp = sD[q], zp = sZ[q];
+          const int cp = sC[q];
+          int tp = sT[q];
+          if (rho * fabs(zp) <= tol) {
+            B.dv[lo + nd] = dp; B.dcol[lo + nd] = cp; ++nd;
+            continue;
+          }
+          if (pj < 0) { pj = p; dpj = dp; zpj = zp; cpj = cp; tpj = tp; continue; }
+          double S = zpj, C = zp;
+          const double tau = hypot(C, S);
+          const double t = dp - dpj;
+          C /= tau;
+          S = -S / tau;
+          if (fabs(t * C * S) <= tol) {
+            zp = tau;
+            zs[p] = tau;
+            zs[pj] = 0.0;
+            B.rp[lo + nrot] = cpj; B.rq[lo + nrot] = cp;
+            B.rc[lo + nrot] = C; B.rs[lo + nrot] = S; ++nrot;
+            if (tp != tpj) { tp = 2; ctype[p] = 2; }
+            const double tmp = dpj * C * C + dp * S * S;
+            dp = dpj * S * S + dp * C * C;
+            Ds[p] = dp;
+            Ds[pj] = tmp;
+            B.dv[lo + nd] = tmp; B.dcol[lo + nd] = cpj; ++nd;
+          } else {
+            B.dl[lo + K] = dpj; B.zl[lo + K] = zpj;
+            B.ncol[lo + K] = cpj; B.ntype[lo + K] = tpj; ++K;
+          }
+          pj = p; dpj = dp; zpj = zp; cpj = cp; tpj = tp;
+        }
       }
     }
+    if (lane != 0) return;
     if (pj >= 0) {
-      B.dl[lo + K] = Ds[pj]; B.zl[lo + K] = zs[pj];
-      B.ncol[lo + K] = colid[pj]; B.ntype[lo + K] = ctype[pj]; ++K;
+      B.dl[lo + K] = dpj; B.zl[lo + K] = zpj;
+      B.ncol[lo + K] = cpj; B.ntype[lo + K] = tpj; ++K;
     }
   }
   // U row order [top-only | mixed | bottom-only]; column maps of the two merge GEMMs
