@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <thread>
+#include <ctime>
 #include "comm.h"
 
 namespace pevd {
@@ -30,7 +31,36 @@ PeerWorld::PeerWorld(int G_, const int* devs) : G(G_), dev(devs, devs + G_), ptr
   cudaSetDevice(cur);
 }
 
-PeerWorld::~PeerWorld() {}
+PeerWorld::~PeerWorld() {
+  if (base_ev) cudaEventDestroy(base_ev);
+}
+
+static double comm_mono_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec * 1e9 + (double)ts.tv_nsec;
+}
+
+cudaEvent_t Comm::time_base(cudaEvent_t mine, cudaStream_t st, double& t0_ns) {
+  cudaEventRecord(mine, st);
+  t0_ns = comm_mono_ns();
+  return mine;
+}
+
+cudaEvent_t PeerComm::time_base(cudaEvent_t mine, cudaStream_t st, double& t0_ns) {
+  bool same = true;
+  for (int x = 0; x < size_; ++x) same = same && w_->dev[x] == w_->dev[0];
+  if (size_ == 1 || !same) return Comm::time_base(mine, st, t0_ns);
+  if (rank_ == 0) {
+    if (!w_->base_ev) cudaEventCreate(&w_->base_ev);
+    cudaEventRecord(w_->base_ev, st);
+    w_->base_t0 = comm_mono_ns();
+  }
+  if (!w_->rendezvous()) return Comm::time_base(mine, st, t0_ns);
+  if (rank_ != 0) cudaStreamWaitEvent(st, w_->base_ev, 0);
+  t0_ns = w_->base_t0;
+  return w_->base_ev;
+}
 
 bool PeerWorld::rendezvous() {
   std::unique_lock<std::mutex> lk(mu);

@@ -54,6 +54,12 @@ class Comm {
   virtual int barrier() = 0;
   // device-side barrier: work after it on `st` starts once every rank's `st` reached it
   virtual int device_barrier(cudaStream_t st) = 0;
+  // The trace's time base, taken right after barrier(): an event recorded on `st` (returned)
+  // and the host CLOCK_MONOTONIC ns it stands for.  Ranks on different devices each record
+  // `mine`; ranks sharing a device share ONE event and t0 (PeerComm), so their spans are on one
+  // clock -- per-rank bases a few microseconds apart made cross-rank orderings (every final
+  // multiply after every solver) flip in the trace.
+  virtual cudaEvent_t time_base(cudaEvent_t mine, cudaStream_t st, double& t0_ns);
   // measured ledger of this rank's sends
   void record(int src, int dst, int stage, int64_t words) {
     if (words > 0) msgs_.push_back(Message{src, dst, stage, 0, words});
@@ -77,6 +83,9 @@ struct PeerWorld {
   int arrived = 0;
   std::atomic<int64_t> generation{0};
   std::atomic<bool> aborted{false};
+  // the shared trace time base of ranks on one device (created by rank 0, freed here)
+  cudaEvent_t base_ev = nullptr;
+  double base_t0 = 0.0;
   // exchanged per collective
   std::vector<const void*> ptr;
   std::vector<cudaEvent_t> ready, done;
@@ -94,6 +103,7 @@ class PeerComm : public Comm {
   int p2p(const void* send, void* recv, int64_t bytes, int src, int dst, cudaStream_t st) override;
   int barrier() override;
   int device_barrier(cudaStream_t st) override;
+  cudaEvent_t time_base(cudaEvent_t mine, cudaStream_t st, double& t0_ns) override;
 
  private:
   PeerWorld* w_;

@@ -664,8 +664,7 @@ int dist_syevd(Comm& C, int64_t n, int b, double* blk, int64_t ldb, const int64_
     K.base = K.new_event();
     if ((rc = (cudaStreamSynchronize(cs) == cudaSuccess) ? OK : ERR_CUDA)) break;
     if ((rc = C.barrier())) break;
-    cudaEventRecord(K.base, cs);
-    t0_ns = mono_ns();
+    K.base = C.time_base(K.base, cs, t0_ns);
     if (want_vectors)
       if ((rc = cudaMemsetAsync(K.Ystair, 0, n * n * 8, cs) == cudaSuccess ? OK : ERR_CUDA)) break;
     // ---------------- SBR
