@@ -34,8 +34,19 @@ def main():
     tau = torch.empty(nref, dtype=torch.float64, device="cuda")
     V = torch.empty(nref * b, dtype=torch.float64, device="cuda")
     wsb = torch.empty(L.pevd_bc_workspace_bytes(n, b), dtype=torch.uint8, device="cuda")
-    dh0 = torch.randn(h, dtype=torch.float64, device="cuda")
-    eh = torch.randn(h, dtype=torch.float64, device="cuda")
+    # the half-size tridiagonal of a GOE matrix (SBR + chase: little deflation, as in the EVD)
+    dh0 = torch.empty(h, dtype=torch.float64, device="cuda")
+    eh = torch.empty(h, dtype=torch.float64, device="cuda")
+    A = torch.randn((h, h), dtype=torch.float64, device="cuda")
+    A = (A + A.t()) / 2
+    bh = torch.empty((b + 1) * h, dtype=torch.float64, device="cuda")
+    ws = torch.empty(L.pevd_sbr_workspace_bytes(h, b), dtype=torch.uint8, device="cuda")
+    _lib.check(L.pevd_sbr(h, b, ptr(A), h, ptr(bh), None, ptr(ws), None), "sbr")
+    del A, ws
+    ws = torch.empty(L.pevd_bc_workspace_bytes(h, b), dtype=torch.uint8, device="cuda")
+    _lib.check(L.pevd_bc(h, b, ptr(bh), ptr(dh0), ptr(eh), None, None, 32, ptr(ws), None), "bc")
+    torch.cuda.synchronize()
+    del ws, bh
     dh = torch.empty_like(dh0)
     Q = torch.empty((h, h), dtype=torch.float64, device="cuda")
     wsd = torch.empty(L.pevd_stedc_workspace_bytes(h), dtype=torch.uint8, device="cuda")
