@@ -713,6 +713,19 @@ int pevd_dgemm(int transA, int transB, int64_t m, int64_t n, int64_t k, double a
   return gemm((cudaStream_t)stream, g, (double*)workspace, workspace_bytes / 8);
 }
 
+// Measurement helper (tools/kernel_probe.py gemm_grouped; not part of include/pevd.h): ONE
+// problem through the grouped-GEMM path the divide and conquer's merges take, with an optional
+// identity-free column map, so its rate can be set beside pevd_dgemm's on the same shape.
+int pevd_probe_gemm_grouped(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                            const double* B, int64_t ldb, double* C, int64_t ldc,
+                            const int* d_cmap, void* d_args, void* stream) {
+  GemmArgs g{m, n, k, 1.0, 0.0, A, lda, B, ldb, C, ldc, 0, 0, A_GENERAL, C_ALL};
+  g.cmap = d_cmap;
+  cudaStream_t st = (cudaStream_t)stream;
+  PEVD_CUDA(cudaMemcpyAsync(d_args, &g, sizeof(GemmArgs), cudaMemcpyHostToDevice, st));
+  return gemm_grouped(st, (const GemmArgs*)d_args, 1, m, n);
+}
+
 int pevd_dsymm_lower(int64_t m, int64_t n, double alpha, const double* A, int64_t lda,
                      const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                      void* workspace, int64_t workspace_bytes, void* stream) {

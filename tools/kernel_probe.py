@@ -99,6 +99,26 @@ def main():
                                                        beta, ptr(C), m, ptr(ws), ws.numel(), stream()),
                                           "gemm"), reps=5)
         out.update(m=m, n=n, k=k, ms=ms, tflops=2.0 * m * n * k / ms / 1e9)
+    elif mode == "gemm_grouped":
+        # pevd_dgemm vs the grouped path (D&C merges) on one shape; cmap = 1 adds a column map
+        m, n, k = (int(x) for x in sys.argv[2:5])
+        use_map = len(sys.argv) > 5 and sys.argv[5] == "1"
+        A = torch.randn(m * k, dtype=torch.float64, device="cuda")
+        B = torch.randn(k * n, dtype=torch.float64, device="cuda")
+        C = torch.zeros(m * n, dtype=torch.float64, device="cuda")
+        cmap = torch.arange(n, dtype=torch.int32, device="cuda") if use_map else None
+        dargs = torch.empty(4096, dtype=torch.uint8, device="cuda")
+        L.pevd_probe_gemm_grouped.argtypes = [ctypes.c_int64] * 3 + [P, ctypes.c_int64, P,
+                                              ctypes.c_int64, P, ctypes.c_int64, P, P, P]
+        msg, _ = timed(lambda: _lib.check(L.pevd_probe_gemm_grouped(
+            m, n, k, ptr(A), m, ptr(B), k, ptr(C), m, ptr(cmap) if use_map else None,
+            ptr(dargs), stream()), "grouped"), reps=3)
+        ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+        msp, _ = timed(lambda: _lib.check(L.pevd_dgemm(0, 0, m, n, k, 1.0, ptr(A), m, ptr(B), k,
+                                                       0.0, ptr(C), m, ptr(ws), ws.numel(),
+                                                       stream()), "gemm"), reps=3)
+        out.update(m=m, n=n, k=k, cmap=use_map, grouped_tflops=2.0 * m * n * k / msg / 1e9,
+                   plain_tflops=2.0 * m * n * k / msp / 1e9)
     elif mode == "symm":
         m, n = int(sys.argv[2]), int(sys.argv[3])
         lda = int(sys.argv[4]) if len(sys.argv) > 4 else m  # the SBR passes lda = n_total
