@@ -40,6 +40,7 @@ constexpr int MAXCTA = 1024;
 // invalidate per iteration.)  The count starts at 0 per launch (panel_qr's memset).
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& gen) {
   __syncthreads();
+  if (nblocks == 1) return;  // one CTA: the CTA barrier is the whole barrier
   if (threadIdx.x == 0) {
     ++gen;
     const unsigned target = gen * nblocks;
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(QR_THREADS, 1)
     active = scal[3] != 0.0;
     const double tau = scal[1];
     // tau v^T a_c = tau (a_c[j] + x_tail^T a_c,tail / denom)  for c > j
-    cf = (active && lane > j && lane < k) ? tau * (pv + hv[lane] / denom) : 0.0;
+    cf = (active && lane > j && lane < k) ? tau * (pv + hv[lane] * rdenom) : 0.0;
   }
   __syncthreads();
 
@@ -485,6 +486,8 @@ int panel_qr(cudaStream_t st, int64_t m, int k, const double* panel, int64_t ldp
   flops_add(4.0 * (double)m * k * k - 2.0 / 3.0 * (double)k * k * k);
   const int sms = num_sms();
   // fewer, fatter CTAs for short panels: every grid step pays one arrival + one partial per CTA
+  // (one CTA per 192 rows: a single CTA for a short panel measured slower -- 304 vs 158 us at
+  //  m = 768 -- its per-column pass grows faster than the grid barrier it saves)
   int ncta = (int)std::min<int64_t>(sms, cdiv(m, 192));
   if (ncta < 1) ncta = 1;
   int64_t rows = cdiv(m, ncta);
